@@ -1,0 +1,26 @@
+// ychg/scan_b200.hpp -- extensions of the B200 library beyond the reference API.
+//
+// scan() returns every output of the hot path from one pass over the mask:
+// counts (runscan.cpp:122-128), boundaries (runscan.cpp:145-153) and the
+// hyperedge total that the reference only obtains as
+// hyperedge_count(decompose(build_profile(image))) (hypergraph.cpp:192).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "ychg/image.hpp"
+
+namespace ychg {
+
+struct ScanResult {
+    std::vector<int> counts;
+    std::vector<int> boundaries;
+    std::int64_t total_runs = 0;
+    std::int64_t links = 0;
+    std::int64_t hyperedges = 0;
+};
+
+ScanResult scan(const BinaryImage& image);
+
+}  // namespace ychg

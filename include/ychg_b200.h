@@ -1,0 +1,163 @@
+/*
+ * ychg_b200.h -- C ABI of the B200-native yCHG hot path (arXiv 1307.2560).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary and
+ * no exception ever does.  Every function returns an int status (YCHG_OK or a
+ * negative YCHG_ERR_*); ychg_last_error() returns a thread-local message.
+ *
+ * Image layout = the reference BinaryImage (proj/include/ychg/image.hpp:10-22,
+ * 35-36): row-major, 1 bit per pixel, MSB-first bytes (x = 0 is bit 0x80),
+ * rows of row_stride >= (width+7)/8 bytes, padding bits zero.
+ *
+ * The reference has no FFI of its own; these entry points are what a binding
+ * of its runscan API would bind:
+ *   ychg_cut_vertex_counts         replaces ychg::cut_vertex_counts
+ *                                   (runscan.hpp:59-62, runscan.cpp:122-128)
+ *   ychg_detect_boundary_columns   replaces ychg::detect_boundary_columns
+ *                                   (runscan.hpp:68-71, runscan.cpp:145-153)
+ *   ychg_scan_host                  counts + boundaries + hyperedge total in one
+ *                                   pass; its hyperedge total equals
+ *                                   hyperedge_count(decompose(build_profile(img)))
+ *                                   (hypergraph.cpp:192, :94-170, runscan.cpp:130-143)
+ *   ychg_plan_* / ychg_scan_device  the same pass on device-resident buffers and a
+ *                                   caller stream (benchmarks, multi-GPU strips)
+ *   ychg_synth_device               bit-exact on-device synth (synth.cpp:38-104)
+ *
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point fails with YCHG_ERR_NO_DEVICE.
+ */
+#ifndef YCHG_B200_H
+#define YCHG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define YCHG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define YCHG_API __attribute__((visibility("default")))
+#else
+#define YCHG_API
+#endif
+
+enum {
+    YCHG_OK = 0,
+    YCHG_ERR_INVALID = -1,   /* bad argument: maps to ychg::ValidationError */
+    YCHG_ERR_CUDA = -2,      /* CUDA runtime/driver failure: maps to ychg::Error */
+    YCHG_ERR_OOM = -3,       /* device or pinned allocation failed */
+    YCHG_ERR_NO_DEVICE = -4, /* no CUDA device (no CPU fallback exists) */
+    YCHG_ERR_INTERNAL = -5
+};
+
+/* ScanStrategy::Kind (runscan.hpp:26-36) */
+enum { YCHG_STRATEGY_SERIAL = 0, YCHG_STRATEGY_PARALLEL = 1 };
+
+/* Synthetic patterns in the reference enum order (synth.hpp:27-34). */
+enum {
+    YCHG_PATTERN_FULL = 0,
+    YCHG_PATTERN_EMPTY = 1,
+    YCHG_PATTERN_FRAME = 2,
+    YCHG_PATTERN_HBANDS = 3,
+    YCHG_PATTERN_CHECKER = 4,
+    YCHG_PATTERN_RANDOM = 5
+};
+
+/* Scalars produced by one scan.  Device-resident in ychg_scan_device. */
+typedef struct {
+    int64_t total_runs;   /* sum of counts == ColumnProfile::total_runs() (runscan.hpp:46-50) */
+    int64_t links;        /* mutually-unique overlaps linked by decompose (hypergraph.cpp:137-143) */
+    int64_t hyperedges;   /* total_runs - links == hyperedge_count(decompose(...)); -1 if not computed */
+    int64_t n_boundaries; /* detect_boundary_columns(counts).size() */
+} ychg_totals;
+
+typedef struct {
+    int32_t n_strips;       /* 1024-column strips */
+    int32_t n_blocks;       /* 32-row blocks */
+    int32_t seg_per_strip;  /* row segments per strip */
+    int32_t n_segments;
+    int32_t grid;           /* CTAs of the streaming kernel (persistent, <= SM count) */
+    int32_t kernels_per_scan;
+    int64_t workspace_bytes;
+} ychg_plan_info;
+
+typedef struct ychg_plan ychg_plan;
+
+/* ---- diagnostics ---- */
+YCHG_API const char* ychg_last_error(void);
+YCHG_API int ychg_abi_version(void);
+YCHG_API int ychg_device_count(int* n);
+
+/* ---- host-buffer entry points (what the C++ drop-in calls) ----
+ * Inputs and outputs are host memory (pinned or pageable).  Thread-safe: calls
+ * serialise on a per-device context that caches the plan and device buffers. */
+
+/* counts_out[width].  width == 0 -> nothing written; height == 0 -> all zeros.
+ * strategy is validated like runscan.cpp:24-26 (parallel needs threads >= 1) and
+ * otherwise ignored: every strategy runs the same GPU path. */
+YCHG_API int ychg_cut_vertex_counts(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                           int32_t strategy_kind, int32_t threads, int32_t* counts_out);
+
+/* boundaries_out must hold n entries; *n_out receives the number written. */
+YCHG_API int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, int32_t* boundaries_out,
+                                 int64_t* n_out);
+
+/* Fused pass.  counts_out[width] (may be NULL), boundaries_out[width] (may be NULL),
+ * totals_out (may be NULL).  with_hyperedges = 0 skips K3 (hyperedges = -1). */
+YCHG_API int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                   int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
+                   ychg_totals* totals_out);
+
+/* ---- device-resident plans ----
+ * A plan fixes the geometry and owns its device workspace.  width_img columns
+ * are present in the buffer, width_cnt <= width_img are counted; columns
+ * [width_cnt, width_img) only serve as the right halo of the K3 pair step
+ * (multi-GPU column strips).  A plan is not safe for concurrent use. */
+YCHG_API int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t height,
+                     ychg_plan** out);
+YCHG_API void ychg_plan_destroy(ychg_plan* plan);
+YCHG_API int ychg_plan_get_info(const ychg_plan* plan, ychg_plan_info* out);
+
+/* d_bits: device rows of `pitch` bytes (pitch % 16 == 0, pitch >= (width_img+7)/8).
+ * Outputs are device pointers: d_counts[width_cnt], d_flags[(width_cnt+31)/32]
+ * (bit j of word w = change flag of column 32w+j), d_boundaries[width_cnt],
+ * d_totals[1].  stream is a cudaStream_t (NULL = legacy default stream).
+ * Asynchronous: returns after enqueueing the kernels. */
+YCHG_API int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int32_t with_hyperedges,
+                     int32_t* d_counts, uint32_t* d_flags, int32_t* d_boundaries,
+                     ychg_totals* d_totals, void* stream);
+
+/* Optional CUDA-event timing of the streaming kernel of the next scans on this
+ * plan: after a scan completes, ychg_plan_last_ms reports the streaming kernel
+ * and the finish (flags/compaction) kernels separately. */
+YCHG_API int ychg_plan_set_timing(ychg_plan* plan, int32_t enabled);
+YCHG_API int ychg_plan_last_ms(ychg_plan* plan, float* scan_ms, float* finish_ms);
+
+/* ---- helpers ---- */
+/* Bit-exact with reference synth() for every pattern (synth.cpp:38-104);
+ * writes height rows of `pitch` bytes, padding bytes and bits zeroed. */
+YCHG_API int ychg_synth_device(int32_t pattern, int32_t width, int32_t height, int32_t bands, int32_t cell,
+                      double density, uint64_t seed, uint8_t* d_bits, int64_t pitch, void* stream);
+
+/* Device memory helpers so hosts without a CUDA runtime binding can drive the
+ * device API (tests, ctypes). */
+YCHG_API int ychg_device_alloc(int device, int64_t bytes, void** out);
+YCHG_API int ychg_device_free(int device, void* p);
+YCHG_API int ychg_host_alloc_pinned(int64_t bytes, void** out);
+YCHG_API int ychg_host_free_pinned(void* p);
+YCHG_API int ychg_memcpy(void* dst, const void* src, int64_t bytes, void* stream);
+YCHG_API int ychg_memcpy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                   int64_t height, void* stream);
+YCHG_API int ychg_memset(void* dst, int32_t value, int64_t bytes, void* stream);
+YCHG_API int ychg_stream_create(int device, void** out);
+YCHG_API int ychg_stream_destroy(void* stream);
+YCHG_API int ychg_stream_synchronize(void* stream);
+YCHG_API int ychg_set_device(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* YCHG_B200_H */

@@ -1,0 +1,163 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" wrappers around the UNMODIFIED reference implementation, which
+// oracle/Makefile compiles from /root/reference/proj/src with -Dychg=ychg_ref
+// into oracle/_ref/libychg_ref.so.  Used by tests (to pin the oracle and generate
+// golden fixtures) and by bench.py's reference arm / cpu_baseline leg (to time
+// the reference's own CPU path on the GPU box's host cores).  Never linked by
+// the product.
+//
+// This file is ours; it only calls the reference's public API:
+//   synth (synth.hpp:66), cut_vertex_counts (runscan.hpp:59-62),
+//   detect_boundary_columns (runscan.hpp:68-71), build_profile (runscan.hpp:64-66),
+//   decompose + hyperedge_count (hypergraph.hpp:82,96).
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "ychg/errors.hpp"
+#include "ychg/hypergraph.hpp"
+#include "ychg/image.hpp"
+#include "ychg/runscan.hpp"
+#include "ychg/synth.hpp"
+
+#define YR_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+thread_local std::string g_err;
+
+ychg::ScanStrategy strategy_of(int kind, int threads) {
+    return kind == 0 ? ychg::ScanStrategy::serial() : ychg::ScanStrategy::parallel(threads);
+}
+
+// -1 = ValidationError, -2 = other ychg::Error, -3 = anything else.
+int code_of(const std::exception& e) {
+    g_err = e.what();
+    if (dynamic_cast<const ychg::ValidationError*>(&e)) return -1;
+    if (dynamic_cast<const ychg::Error*>(&e)) return -2;
+    return -3;
+}
+
+ychg::BinaryImage image_of(const uint8_t* bits, int w, int h, int64_t stride) {
+    ychg::BinaryImage img(w, h);
+    const int s = img.row_stride();
+    for (int y = 0; y < h; ++y) std::memcpy(img.row(y), bits + y * stride, static_cast<size_t>(s));
+    return img;
+}
+
+}  // namespace
+
+YR_EXPORT const char* yr_last_error() { return g_err.c_str(); }
+
+YR_EXPORT int yr_synth(int pattern, int w, int h, int bands, int cell, double density,
+                       uint64_t seed, uint8_t* out) {
+    try {
+        ychg::SynthSpec spec{static_cast<ychg::Pattern>(pattern), w, h, bands, cell, density, seed};
+        const ychg::BinaryImage img = ychg::synth(spec);
+        std::memcpy(out, img.bytes().data(), img.bytes().size());
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+YR_EXPORT uint64_t yr_splitmix64(uint64_t seed, int n_skip) {
+    ychg::Splitmix64 rng(seed);
+    uint64_t v = 0;
+    for (int i = 0; i <= n_skip; ++i) v = rng.next();
+    return v;
+}
+
+// Opaque handle so benchmarks time only the reference call, not the copy-in.
+YR_EXPORT void* yr_image_create(const uint8_t* bits, int w, int h, int64_t stride) {
+    try {
+        return new ychg::BinaryImage(image_of(bits, w, h, stride));
+    } catch (const std::exception& e) {
+        code_of(e);
+        return nullptr;
+    }
+}
+
+YR_EXPORT void* yr_image_synth(int pattern, int w, int h, int bands, int cell, double density,
+                               uint64_t seed) {
+    try {
+        ychg::SynthSpec spec{static_cast<ychg::Pattern>(pattern), w, h, bands, cell, density, seed};
+        return new ychg::BinaryImage(ychg::synth(spec));
+    } catch (const std::exception& e) {
+        code_of(e);
+        return nullptr;
+    }
+}
+
+YR_EXPORT void yr_image_destroy(void* img) { delete static_cast<ychg::BinaryImage*>(img); }
+
+YR_EXPORT const uint8_t* yr_image_bytes(void* img) {
+    return static_cast<ychg::BinaryImage*>(img)->bytes().data();
+}
+
+YR_EXPORT int yr_counts(void* img, int kind, int threads, int32_t* out) {
+    try {
+        const auto counts = ychg::cut_vertex_counts(*static_cast<ychg::BinaryImage*>(img),
+                                                    strategy_of(kind, threads));
+        if (!counts.empty()) std::memcpy(out, counts.data(), counts.size() * sizeof(int));
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+YR_EXPORT int64_t yr_boundaries(const int32_t* counts, int64_t n, int32_t* out) {
+    const auto b = ychg::detect_boundary_columns(std::span<const int>(counts, static_cast<size_t>(n)));
+    if (out && !b.empty()) std::memcpy(out, b.data(), b.size() * sizeof(int));
+    return static_cast<int64_t>(b.size());
+}
+
+YR_EXPORT int64_t yr_hyperedges(void* img, int kind, int threads) {
+    try {
+        const auto prof = ychg::build_profile(*static_cast<ychg::BinaryImage*>(img),
+                                              strategy_of(kind, threads));
+        return static_cast<int64_t>(ychg::hyperedge_count(ychg::decompose(prof)));
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// The reference's full hot path (counts + boundaries + hyperedge total), timed
+// with the reference protocol (bench.cpp:37-57: warmup untimed, reps timed with
+// steady_clock).  with_hyperedges=0 times counts + boundaries only.
+// ns_out gets one entry per rep; the outputs of the last rep go to the out args.
+YR_EXPORT int yr_time_path(void* img, int kind, int threads, int warmup, int reps,
+                           int with_hyperedges, int64_t* ns_out, int32_t* counts_out,
+                           int64_t* n_boundaries_out, int64_t* hyperedges_out) {
+    try {
+        const auto& image = *static_cast<ychg::BinaryImage*>(img);
+        const auto strategy = strategy_of(kind, threads);
+        for (int r = 0; r < warmup + reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const auto counts = ychg::cut_vertex_counts(image, strategy);
+            const auto bounds = ychg::detect_boundary_columns(counts);
+            std::int64_t he = -1;
+            if (with_hyperedges)
+                he = static_cast<int64_t>(
+                    ychg::hyperedge_count(ychg::decompose(ychg::build_profile(image, strategy))));
+            const auto t1 = std::chrono::steady_clock::now();
+            if (r >= warmup) {
+                ns_out[r - warmup] =
+                    std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+                if (r == warmup + reps - 1) {
+                    if (counts_out && !counts.empty())
+                        std::memcpy(counts_out, counts.data(), counts.size() * sizeof(int));
+                    if (n_boundaries_out) *n_boundaries_out = static_cast<int64_t>(bounds.size());
+                    if (hyperedges_out) *hyperedges_out = he;
+                }
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}

@@ -1,0 +1,245 @@
+/*
+ * ychg_oracle.c -- TEST INFRASTRUCTURE ONLY (the parity checker, never the product).
+ *
+ * A plain-C, scalar, per-pixel restatement of the reference CPU algorithm for the
+ * yCHG hot path of arXiv 1307.2560.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline leg of bench.py may load this library.  The product path
+ * (paper_1307_2560_b200/, libychg_b200.so) never links or calls it.
+ *
+ * Parity is PINNED two ways (see tests/test_oracle.py):
+ *   - against the reference's own known-answer vectors (test_runscan.cpp:35-49,
+ *     :129-143, test_hypergraph.cpp:75-88, test_bench.cpp:139-160,
+ *     test_imagekit.cpp:81-91, acceptance.cpp:101-121), and
+ *   - against the reference itself, compiled unmodified from /root/reference into
+ *     oracle/_ref/libychg_ref.so by oracle/Makefile, on the 1170-image corpus
+ *     (tests/golden/make_golden.py commits the resulting fixtures).
+ *
+ * Layout of an image (reference image.hpp:10-22,35-36): row-major, 1 bit per pixel,
+ * MSB-first in each byte (x = 0 is bit 0x80), rows padded to stride = (w+7)/8 bytes,
+ * padding bits zero.  All entry points take (bits, w, h, stride).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define YO_EXPORT __attribute__((visibility("default")))
+
+static inline int yo_get(const uint8_t* bits, int64_t stride, int x, int y) {
+    return (bits[(int64_t)y * stride + (x >> 3)] >> (7 - (x & 7))) & 1;
+}
+
+static inline void yo_set(uint8_t* bits, int64_t stride, int x, int y) {
+    bits[(int64_t)y * stride + (x >> 3)] |= (uint8_t)(0x80u >> (x & 7));
+}
+
+/* ---------------------------------------------------------------- SplitMix64
+ * synth.hpp:14-25: state += golden; two xor-shift-multiply rounds; final xor-shift. */
+YO_EXPORT uint64_t yo_splitmix64_next(uint64_t* state) {
+    uint64_t z = (*state += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+/* ---------------------------------------------------------------- synth
+ * Patterns in the reference's enum order (synth.hpp:27-34).
+ * Returns 0 on success, -1 on a spec that synth.cpp:10-34 rejects. */
+enum { YO_FULL = 0, YO_EMPTY = 1, YO_FRAME = 2, YO_HBANDS = 3, YO_CHECKER = 4, YO_RANDOM = 5 };
+
+YO_EXPORT int yo_synth_validate(int pattern, int w, int h, int bands, int cell, double density) {
+    if (w < 0 || h < 0) return -1;
+    if (pattern == YO_HBANDS && (bands < 1 || bands > h / 2)) return -1;
+    if (pattern == YO_CHECKER && cell < 1) return -1;
+    if (pattern == YO_RANDOM && !(density >= 0.0 && density <= 1.0)) return -1;
+    if (pattern < YO_FULL || pattern > YO_RANDOM) return -1;
+    return 0;
+}
+
+/* out must hold h * ((w+7)/8) bytes; it is fully overwritten. */
+YO_EXPORT int yo_synth(int pattern, int w, int h, int bands, int cell, double density,
+                       uint64_t seed, uint8_t* out) {
+    if (yo_synth_validate(pattern, w, h, bands, cell, density) != 0) return -1;
+    const int64_t stride = (w + 7) / 8;
+    memset(out, 0, (size_t)(stride * h));
+    switch (pattern) {
+    case YO_FULL: /* synth.cpp:38-43 */
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) yo_set(out, stride, x, y);
+        break;
+    case YO_EMPTY:
+        break;
+    case YO_FRAME: /* synth.cpp:45-51 */
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x)
+                if (x == 0 || y == 0 || x == w - 1 || y == h - 1) yo_set(out, stride, x, y);
+        break;
+    case YO_HBANDS: { /* synth.cpp:55-64: equal maximal bands from the top, 1-row gaps */
+        const int bh = (h - (bands - 1)) / bands;
+        for (int b = 0; b < bands; ++b)
+            for (int y = b * (bh + 1); y < b * (bh + 1) + bh; ++y)
+                for (int x = 0; x < w; ++x) yo_set(out, stride, x, y);
+        break;
+    }
+    case YO_CHECKER: /* synth.cpp:66-72 */
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x)
+                if (((x / cell) + (y / cell)) % 2 == 0) yo_set(out, stride, x, y);
+        break;
+    case YO_RANDOM: { /* synth.cpp:74-87: one draw per pixel, row-major, draw < density*2^64 */
+        if (density <= 0.0) break;
+        const double scaled = density * 18446744073709551616.0; /* 0x1p64 */
+        const int all = scaled >= 18446744073709551616.0;
+        const uint64_t threshold = all ? 0 : (uint64_t)scaled;
+        uint64_t st = seed;
+        for (int y = 0; y < h; ++y)
+            for (int x = 0; x < w; ++x) {
+                const uint64_t draw = yo_splitmix64_next(&st);
+                if (all || draw < threshold) yo_set(out, stride, x, y);
+            }
+        break;
+    }
+    }
+    return 0;
+}
+
+/* ---------------------------------------------------------------- step 1
+ * Cut-vertex count of every column = number of maximal vertical foreground runs,
+ * counted per pixel as background->foreground transitions scanning down with a
+ * virtual background row -1 (runscan.cpp:41-74 semantics; the per-pixel form is
+ * the reference's own independent checker corpus.hpp:91-102). */
+YO_EXPORT void yo_cut_vertex_counts(const uint8_t* bits, int w, int h, int64_t stride,
+                                    int32_t* counts) {
+    for (int c = 0; c < w; ++c) {
+        int prev = 0, n = 0;
+        for (int y = 0; y < h; ++y) {
+            const int cur = yo_get(bits, stride, c, y);
+            n += cur & !prev;
+            prev = cur;
+        }
+        counts[c] = n;
+    }
+}
+
+/* ---------------------------------------------------------------- step 2
+ * runscan.cpp:145-153: ascending c with counts[c] != counts[c-1], counts[-1] := 0.
+ * Returns the number of boundaries written to out (out may be NULL to only count). */
+YO_EXPORT int64_t yo_detect_boundary_columns(const int32_t* counts, int64_t n, int32_t* out) {
+    int64_t k = 0;
+    int32_t previous = 0;
+    for (int64_t c = 0; c < n; ++c) {
+        if (counts[c] != previous) {
+            if (out) out[k] = (int32_t)c;
+            ++k;
+        }
+        previous = counts[c];
+    }
+    return k;
+}
+
+/* ---------------------------------------------------------------- hyperedge total
+ * hyperedge_count(decompose(build_profile(img))) (hypergraph.cpp:94-170,192).
+ * decompose links a run r of column c to a run s of column c+1 iff they overlap
+ * vertically and each is the other's only overlap (two-pointer sweep, :116-143);
+ * hyperedges are the resulting chains, so
+ *     hyperedges = total runs - number of links.
+ * Runs are extracted per column directly from pixels (column_runs, runscan.cpp:104-120).
+ * Memory is two columns of runs at a time. */
+typedef struct { int top, bot; } yo_run;
+
+static int64_t yo_column_runs(const uint8_t* bits, int h, int64_t stride, int c, yo_run* out) {
+    int64_t n = 0;
+    int start = -1;
+    for (int y = 0; y < h; ++y) {
+        if (yo_get(bits, stride, c, y)) {
+            if (start < 0) start = y;
+        } else if (start >= 0) {
+            out[n].top = start; out[n].bot = y - 1; ++n;
+            start = -1;
+        }
+    }
+    if (start >= 0) { out[n].top = start; out[n].bot = h - 1; ++n; }
+    return n;
+}
+
+/* Links between two adjacent columns' sorted run lists (hypergraph.cpp:108-143). */
+static int64_t yo_pair_links(const yo_run* a, int64_t na, const yo_run* b, int64_t nb,
+                             uint32_t* ov_a, uint32_t* pa, uint32_t* ov_b, uint32_t* pb) {
+    if (na == 0 || nb == 0) return 0;
+    memset(ov_a, 0, sizeof(uint32_t) * (size_t)na);
+    memset(ov_b, 0, sizeof(uint32_t) * (size_t)nb);
+    int64_t i = 0, j = 0;
+    while (i < na && j < nb) {
+        if (a[i].bot < b[j].top) {
+            ++i;
+        } else if (b[j].bot < a[i].top) {
+            ++j;
+        } else {
+            ++ov_a[i]; pa[i] = (uint32_t)j;
+            ++ov_b[j]; pb[j] = (uint32_t)i;
+            if (a[i].bot < b[j].bot) ++i;
+            else if (b[j].bot < a[i].bot) ++j;
+            else { ++i; ++j; }
+        }
+    }
+    int64_t links = 0;
+    for (int64_t k = 0; k < na; ++k)
+        if (ov_a[k] == 1 && ov_b[pa[k]] == 1) ++links;
+    return links;
+}
+
+/* Returns the hyperedge count; *total_runs_out and *links_out (if non-NULL) get the parts.
+ * Returns -1 on allocation failure. */
+YO_EXPORT int64_t yo_hyperedge_count(const uint8_t* bits, int w, int h, int64_t stride,
+                                     int64_t* total_runs_out, int64_t* links_out) {
+    int64_t total = 0, links = 0;
+    if (w > 0 && h > 0) {
+        const size_t cap = (size_t)h / 2 + 1;
+        yo_run* ra = malloc(sizeof(yo_run) * cap);
+        yo_run* rb = malloc(sizeof(yo_run) * cap);
+        uint32_t* scratch = malloc(sizeof(uint32_t) * cap * 4);
+        if (!ra || !rb || !scratch) { free(ra); free(rb); free(scratch); return -1; }
+        int64_t na = yo_column_runs(bits, h, stride, 0, ra);
+        total += na;
+        for (int c = 0; c + 1 < w; ++c) {
+            const int64_t nb = yo_column_runs(bits, h, stride, c + 1, rb);
+            total += nb;
+            links += yo_pair_links(ra, na, rb, nb, scratch, scratch + cap, scratch + 2 * cap,
+                                   scratch + 3 * cap);
+            yo_run* t = ra; ra = rb; rb = t;
+            na = nb;
+        }
+        free(ra); free(rb); free(scratch);
+    }
+    if (total_runs_out) *total_runs_out = total;
+    if (links_out) *links_out = links;
+    return total - links;
+}
+
+/* Number of mutually-unique links per column pair (out[c] for pair (c, c+1), c < w-1).
+ * Used by tests to localise a mismatch. */
+YO_EXPORT int yo_pair_link_counts(const uint8_t* bits, int w, int h, int64_t stride,
+                                  int32_t* out) {
+    if (w < 2 || h <= 0) return 0;
+    const size_t cap = (size_t)h / 2 + 1;
+    yo_run* ra = malloc(sizeof(yo_run) * cap);
+    yo_run* rb = malloc(sizeof(yo_run) * cap);
+    uint32_t* scratch = malloc(sizeof(uint32_t) * cap * 4);
+    if (!ra || !rb || !scratch) { free(ra); free(rb); free(scratch); return -1; }
+    int64_t na = yo_column_runs(bits, h, stride, 0, ra);
+    for (int c = 0; c + 1 < w; ++c) {
+        const int64_t nb = yo_column_runs(bits, h, stride, c + 1, rb);
+        out[c] = (int32_t)yo_pair_links(ra, na, rb, nb, scratch, scratch + cap,
+                                        scratch + 2 * cap, scratch + 3 * cap);
+        yo_run* t = ra; ra = rb; rb = t;
+        na = nb;
+    }
+    free(ra); free(rb); free(scratch);
+    return 0;
+}
+
+/* Popcount of the whole buffer (image.cpp:7-12 foreground_count). */
+YO_EXPORT int64_t yo_foreground_count(const uint8_t* bits, int64_t nbytes) {
+    int64_t n = 0;
+    for (int64_t i = 0; i < nbytes; ++i) n += __builtin_popcount(bits[i]);
+    return n;
+}

@@ -1,0 +1,324 @@
+"""B200-native yCHG hot path (arXiv 1307.2560): Python mirror of the reference API.
+
+The reference's hot path is the C++ runscan API (proj/include/ychg/runscan.hpp):
+``cut_vertex_counts(image, strategy)``, ``detect_boundary_columns(counts)`` and,
+for hyperedge totals, ``hyperedge_count(decompose(build_profile(image)))``.
+This module exposes the same names with the same argument meaning and error
+behaviour, executed by the sm_100a kernels in ``libychg_b200.so`` through its C
+ABI (``include/ychg_b200.h``).  PyTorch is not needed by this module; bench.py
+uses it only for streams, events and torch.distributed plumbing.
+
+There is no CPU fallback: if the native library is missing the import fails,
+and on a machine without a CUDA device every compute call raises ``Error``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libychg_b200.so")
+CXX_LIB_PATH = os.path.join(_PKG, "libychg.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build the CUDA extension first "
+        "(python -c 'import __graft_entry__ as g; g.build()').  There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- C ABI
+OK, ERR_INVALID, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL = 0, -1, -2, -3, -4, -5
+STRATEGY_SERIAL, STRATEGY_PARALLEL = 0, 1
+PATTERNS = {"full": 0, "empty": 1, "frame": 2, "hbands": 3, "checker": 4, "random": 5}
+
+
+class Totals(ctypes.Structure):
+    _fields_ = [("total_runs", ctypes.c_int64), ("links", ctypes.c_int64),
+                ("hyperedges", ctypes.c_int64), ("n_boundaries", ctypes.c_int64)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("n_strips", ctypes.c_int32), ("n_blocks", ctypes.c_int32),
+                ("seg_per_strip", ctypes.c_int32), ("n_segments", ctypes.c_int32),
+                ("grid", ctypes.c_int32), ("kernels_per_scan", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_int64)]
+
+
+_vp, _i32, _i64, _u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+_SIGS = {
+    "ychg_last_error": (ctypes.c_char_p, []),
+    "ychg_abi_version": (ctypes.c_int, []),
+    "ychg_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    "ychg_set_device": (ctypes.c_int, [ctypes.c_int]),
+    "ychg_cut_vertex_counts": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp]),
+    "ychg_detect_boundary_columns": (ctypes.c_int, [_vp, _i64, _vp, ctypes.POINTER(_i64)]),
+    "ychg_scan_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, ctypes.POINTER(Totals)]),
+    "ychg_plan_create": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    "ychg_plan_destroy": (None, [_vp]),
+    "ychg_plan_get_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
+    "ychg_scan_device": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "ychg_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
+    "ychg_plan_last_ms": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
+    "ychg_synth_device": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64, _vp, _i64, _vp]),
+    "ychg_device_alloc": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.POINTER(_vp)]),
+    "ychg_device_free": (ctypes.c_int, [ctypes.c_int, _vp]),
+    "ychg_host_alloc_pinned": (ctypes.c_int, [_i64, ctypes.POINTER(_vp)]),
+    "ychg_host_free_pinned": (ctypes.c_int, [_vp]),
+    "ychg_memcpy": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
+    "ychg_memcpy_2d": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+    "ychg_memset": (ctypes.c_int, [_vp, _i32, _i64, _vp]),
+    "ychg_stream_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    "ychg_stream_destroy": (ctypes.c_int, [_vp]),
+    "ychg_stream_synchronize": (ctypes.c_int, [_vp]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+# ---------------------------------------------------------------- errors (errors.hpp:11-40)
+class Error(RuntimeError):
+    """Base of everything the library raises on purpose (ychg::Error)."""
+
+
+class ValidationError(Error):
+    """Precondition violation (ychg::ValidationError)."""
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == OK:
+        return
+    msg = f"{what}: {_lib.ychg_last_error().decode(errors='replace')}"
+    if rc == ERR_INVALID:
+        raise ValidationError(msg)
+    raise Error(msg)
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    _lib.ychg_device_count(ctypes.byref(n))
+    return n.value
+
+
+# ---------------------------------------------------------------- data model
+class BinaryImage:
+    """Bit-per-pixel raster with the reference layout (image.hpp:10-22,35-36):
+    row-major, MSB-first bytes, rows of ceil(width/8) bytes, padding bits zero."""
+
+    __slots__ = ("width", "height", "_bits")
+
+    def __init__(self, width: int, height: int, bits: np.ndarray | None = None):
+        if width < 0 or height < 0:
+            raise ValidationError(f"negative dimensions {width}x{height}")
+        self.width, self.height = int(width), int(height)
+        stride = (self.width + 7) // 8
+        if bits is None:
+            self._bits = np.zeros((self.height, stride), dtype=np.uint8)
+        else:
+            bits = np.asarray(bits, dtype=np.uint8)
+            if bits.shape != (self.height, stride):
+                raise ValidationError(f"bits shape {bits.shape} != {(self.height, stride)}")
+            self._bits = np.ascontiguousarray(bits)
+
+    @property
+    def row_stride(self) -> int:
+        return (self.width + 7) // 8
+
+    def bytes(self) -> np.ndarray:
+        return self._bits
+
+    def get(self, x: int, y: int) -> bool:
+        return bool((self._bits[y, x >> 3] >> (7 - (x & 7))) & 1)
+
+    def set(self, x: int, y: int, value: bool) -> None:
+        m = np.uint8(0x80 >> (x & 7))
+        if value:
+            self._bits[y, x >> 3] |= m
+        else:
+            self._bits[y, x >> 3] &= np.uint8(~m & 0xFF)
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, BinaryImage) and self.width == other.width
+                and self.height == other.height and np.array_equal(self._bits, other._bits))
+
+    def _ptr(self):
+        return self._bits.ctypes.data_as(_vp) if self._bits.size else None
+
+
+@dataclass(frozen=True)
+class ScanStrategy:
+    """runscan.hpp:26-36.  Validated, then irrelevant: every strategy runs the
+    same GPU pass, so results are strategy-independent by construction."""
+    kind: int = STRATEGY_SERIAL
+    threads: int = 1
+
+    @staticmethod
+    def serial() -> "ScanStrategy":
+        return ScanStrategy(STRATEGY_SERIAL, 1)
+
+    @staticmethod
+    def parallel(threads: int) -> "ScanStrategy":
+        return ScanStrategy(STRATEGY_PARALLEL, int(threads))
+
+
+@dataclass
+class ScanResult:
+    counts: np.ndarray
+    boundaries: np.ndarray
+    total_runs: int
+    links: int
+    hyperedges: int
+    n_boundaries: int = field(default=0)
+
+
+# ---------------------------------------------------------------- the runscan API
+def cut_vertex_counts(image: BinaryImage, strategy: ScanStrategy = ScanStrategy.serial()) -> np.ndarray:
+    """Paper §2 step 1 (runscan.cpp:122-128): runs per column, int32[width]."""
+    out = np.zeros(max(image.width, 1), dtype=np.int32)
+    _check(_lib.ychg_cut_vertex_counts(image._ptr(), image.width, image.height, image.row_stride,
+                                       strategy.kind, strategy.threads, out.ctypes.data_as(_vp)),
+           "cut_vertex_counts")
+    return out[: image.width]
+
+
+def detect_boundary_columns(counts) -> np.ndarray:
+    """Paper §2 step 2 (runscan.cpp:145-153): ascending c with counts[c] != counts[c-1]."""
+    counts = np.ascontiguousarray(np.asarray(counts, dtype=np.int32))
+    out = np.zeros(max(counts.size, 1), dtype=np.int32)
+    n = _i64(0)
+    _check(_lib.ychg_detect_boundary_columns(counts.ctypes.data_as(_vp) if counts.size else None,
+                                             counts.size, out.ctypes.data_as(_vp), ctypes.byref(n)),
+           "detect_boundary_columns")
+    return out[: n.value].copy()
+
+
+def scan(image: BinaryImage, with_hyperedges: bool = True) -> ScanResult:
+    """Counts, boundaries and the hyperedge total from one pass over the mask.
+    hyperedges == hyperedge_count(decompose(build_profile(image))) (hypergraph.cpp:192)."""
+    counts = np.zeros(max(image.width, 1), dtype=np.int32)
+    bounds = np.zeros(max(image.width, 1), dtype=np.int32)
+    t = Totals()
+    _check(_lib.ychg_scan_host(image._ptr(), image.width, image.height, image.row_stride,
+                               int(with_hyperedges), counts.ctypes.data_as(_vp),
+                               bounds.ctypes.data_as(_vp), ctypes.byref(t)), "scan")
+    return ScanResult(counts[: image.width], bounds[: t.n_boundaries].copy(), t.total_runs,
+                      t.links, t.hyperedges, t.n_boundaries)
+
+
+def hyperedge_count(image: BinaryImage) -> int:
+    """hyperedge_count(decompose(build_profile(image))) without materialising runs."""
+    return scan(image).hyperedges
+
+
+# ---------------------------------------------------------------- device-resident plumbing
+class Plan:
+    """Geometry-specific launch plan + workspace on one device (ychg_plan_*)."""
+
+    def __init__(self, width_img: int, height: int, width_cnt: int | None = None, device: int = 0):
+        self.device = device
+        self.width_img, self.height = int(width_img), int(height)
+        self.width_cnt = self.width_img if width_cnt is None else int(width_cnt)
+        h = _vp()
+        _check(_lib.ychg_plan_create(device, self.width_img, self.width_cnt, self.height, ctypes.byref(h)),
+               "plan_create")
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.ychg_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def info(self) -> PlanInfo:
+        i = PlanInfo()
+        _check(_lib.ychg_plan_get_info(self._h, ctypes.byref(i)), "plan_get_info")
+        return i
+
+    def set_timing(self, on: bool) -> None:
+        _check(_lib.ychg_plan_set_timing(self._h, int(on)), "plan_set_timing")
+
+    def last_ms(self) -> tuple[float, float]:
+        a, b = ctypes.c_float(0), ctypes.c_float(0)
+        _check(_lib.ychg_plan_last_ms(self._h, ctypes.byref(a), ctypes.byref(b)), "plan_last_ms")
+        return a.value, b.value
+
+    def scan_device(self, d_bits: int, pitch: int, d_counts: int, d_flags: int, d_boundaries: int,
+                    d_totals: int, stream: int = 0, with_hyperedges: bool = True) -> None:
+        """Enqueue the fused scan on `stream` (raw cudaStream_t); all pointers are device addresses."""
+        _check(_lib.ychg_scan_device(self._h, d_bits, int(pitch), int(with_hyperedges), d_counts, d_flags,
+                                     d_boundaries, d_totals, stream or None), "scan_device")
+
+
+def pitch_for(width: int) -> int:
+    """Device row pitch used by the library: ceil(width/8) rounded up to 16 B (TMA stride rule)."""
+    return ((width + 7) // 8 + 15) // 16 * 16
+
+
+def synth_device(pattern: str, width: int, height: int, d_bits: int, pitch: int, *, bands: int = 0,
+                 cell: int = 0, density: float = 0.0, seed: int = 0, stream: int = 0) -> None:
+    """K0: bit-exact reference synth() (synth.cpp:38-104) written straight into device memory."""
+    _check(_lib.ychg_synth_device(PATTERNS[pattern], width, height, bands, cell, float(density),
+                                  int(seed) & 0xFFFFFFFFFFFFFFFF, d_bits, int(pitch), stream or None),
+           "synth_device")
+
+
+class DeviceBuffer:
+    """Minimal owning device allocation (for hosts without torch)."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        self.device, self.nbytes = device, int(nbytes)
+        p = _vp()
+        _check(_lib.ychg_device_alloc(device, self.nbytes, ctypes.byref(p)), "device_alloc")
+        self.ptr = p.value
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None):
+            _lib.ychg_device_free(self.device, self.ptr)
+            self.ptr = None
+
+    __del__ = close
+
+    def to_host(self, out: np.ndarray) -> np.ndarray:
+        _check(_lib.ychg_memcpy(out.ctypes.data_as(_vp), self.ptr, out.nbytes, None), "memcpy")
+        _check(_lib.ychg_stream_synchronize(None), "sync")
+        return out
+
+    def from_host(self, src: np.ndarray) -> None:
+        src = np.ascontiguousarray(src)
+        _check(_lib.ychg_memcpy(self.ptr, src.ctypes.data_as(_vp), src.nbytes, None), "memcpy")
+        _check(_lib.ychg_stream_synchronize(None), "sync")
+
+
+def synth(pattern: str, width: int, height: int, *, bands: int = 0, cell: int = 0, density: float = 0.0,
+          seed: int = 0, device: int = 0) -> BinaryImage:
+    """Generate a reference synthetic image on the GPU (K0) and return it on the host."""
+    img = BinaryImage(width, height)
+    if width == 0 or height == 0:
+        synth_device(pattern, width, height, 0, max(1, pitch_for(width)), bands=bands, cell=cell,
+                     density=density, seed=seed)
+        return img
+    pitch = pitch_for(width)
+    buf = DeviceBuffer(pitch * height, device)
+    try:
+        synth_device(pattern, width, height, buf.ptr, pitch, bands=bands, cell=cell, density=density, seed=seed)
+        dev = np.zeros((height, pitch), dtype=np.uint8)
+        buf.to_host(dev)
+        img._bits[:] = dev[:, : img.row_stride]
+    finally:
+        buf.close()
+    return img
+
+
+__all__ = [
+    "BinaryImage", "ScanStrategy", "ScanResult", "Error", "ValidationError", "cut_vertex_counts",
+    "detect_boundary_columns", "scan", "hyperedge_count", "Plan", "DeviceBuffer", "synth", "synth_device",
+    "pitch_for", "device_count", "Totals", "PlanInfo", "LIB_PATH", "CXX_LIB_PATH", "EXPORTED_SYMBOLS",
+]

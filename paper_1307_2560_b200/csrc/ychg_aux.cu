@@ -1,0 +1,187 @@
+// ychg_aux.cu -- K0 on-device synth and the stand-alone boundary detector.
+//
+// K0 reproduces the reference generators bit for bit (synth.cpp:38-104).  The
+// random pattern draws one SplitMix64 value per pixel in row-major order
+// (synth.hpp:19-24): draw i is mix(seed + (i+1) * golden), so every pixel is an
+// independent function of its index and the image is generated in parallel.
+//
+// ychg_boundaries_* implement detect_boundary_columns (runscan.cpp:145-153) for
+// counts that arrive from the host (the reference API takes a span of ints).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ychg_kernels.h"
+
+namespace {
+
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+struct SynthArgs {
+    int pattern, width, height, bands, cell, all;
+    uint64_t seed, threshold;
+    int64_t pitch;
+    int row_bytes, band_h;
+};
+
+__device__ __forceinline__ bool synth_pixel(const SynthArgs& a, int x, int y) {
+    switch (a.pattern) {
+    case 0: return true;                                              // full
+    case 1: return false;                                             // empty
+    case 2: return x == 0 || y == 0 || x == a.width - 1 || y == a.height - 1;  // frame
+    case 3: {                                                         // hbands
+        const int b = y / (a.band_h + 1);
+        return b < a.bands && (y - b * (a.band_h + 1)) < a.band_h;
+    }
+    case 4: return ((x / a.cell) + (y / a.cell)) % 2 == 0;            // checker
+    default: {                                                        // random
+        if (a.all) return true;
+        const uint64_t i = static_cast<uint64_t>(y) * static_cast<uint64_t>(a.width) +
+                           static_cast<uint64_t>(x);
+        const uint64_t z = a.seed + (i + 1) * 0x9e3779b97f4a7c15ull;
+        return splitmix_mix(z) < a.threshold;
+    }
+    }
+}
+
+__global__ void synth_kernel(const SynthArgs a, uint8_t* __restrict__ out) {
+    const int64_t total = a.pitch * a.height;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int y = static_cast<int>(idx / a.pitch);
+        const int xb = static_cast<int>(idx - static_cast<int64_t>(y) * a.pitch);
+        uint32_t v = 0;
+        if (xb < a.row_bytes && !(a.pattern == 5 && a.threshold == 0 && !a.all)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int x = xb * 8 + i;
+                if (x < a.width && synth_pixel(a, x, y)) v |= 0x80u >> i;
+            }
+        }
+        out[idx] = static_cast<uint8_t>(v);
+    }
+}
+
+// ---- boundaries from a counts array: flags words, then ordered compaction.
+constexpr int kColsPerBlock = 1024;
+
+__global__ void bflags_kernel(const int32_t* __restrict__ counts, int64_t n,
+                              uint32_t* __restrict__ flags, int32_t* __restrict__ block_nb) {
+    __shared__ int red[8];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kColsPerBlock;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int nb = 0;
+    for (int wi = warp; wi < kColsPerBlock / 32; wi += 8) {
+        const int64_t c = base + wi * 32 + lane;
+        bool f = false;
+        if (c < n) {
+            const int32_t prev = c == 0 ? 0 : counts[c - 1];  // counts[-1] := 0
+            f = counts[c] != prev;
+        }
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+        const int64_t w = (base >> 5) + wi;
+        if (lane == 0 && w * 32 < n) flags[w] = m;
+        nb += __popc(m);
+    }
+    if (lane == 0) red[warp] = nb;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        block_nb[blockIdx.x] = t;
+    }
+}
+
+__global__ void bcompact_kernel(const uint32_t* __restrict__ flags, int64_t n,
+                                const int32_t* __restrict__ block_nb, int32_t* __restrict__ out,
+                                long long* __restrict__ n_out) {
+    __shared__ long long red[8];
+    __shared__ int wpre[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long off = 0;
+    for (int t = threadIdx.x; t < static_cast<int>(blockIdx.x); t += blockDim.x) off += block_nb[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
+    if (lane == 0) red[warp] = off;
+    const int64_t nwords = (n + 31) >> 5;
+    const int64_t w0 = static_cast<int64_t>(blockIdx.x) * (kColsPerBlock / 32);
+    if (warp == 0) {
+        const uint32_t m = w0 + lane < nwords ? flags[w0 + lane] : 0u;
+        const int c = __popc(m);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        wpre[lane] = incl - c;
+    }
+    __syncthreads();
+    long long base = 0;
+    for (int i = 0; i < 8; ++i) base += red[i];
+    for (int wi = warp; wi < 32; wi += 8) {
+        const int64_t w = w0 + wi;
+        if (w >= nwords) break;
+        const uint32_t m = flags[w];
+        if ((m >> lane) & 1u) out[base + wpre[wi] + __popc(m & ((1u << lane) - 1u))] =
+            static_cast<int32_t>(w * 32 + lane);
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_out = base + block_nb[blockIdx.x];
+}
+
+}  // namespace
+
+extern "C" int ychg_launch_synth(int pattern, int width, int height, int bands, int cell,
+                                 double density, uint64_t seed, uint8_t* d_bits, int64_t pitch,
+                                 cudaStream_t stream) {
+    SynthArgs a{};
+    a.pattern = pattern;
+    a.width = width;
+    a.height = height;
+    a.bands = bands;
+    a.cell = cell < 1 ? 1 : cell;
+    a.seed = seed;
+    a.pitch = pitch;
+    a.row_bytes = (width + 7) / 8;
+    a.band_h = (pattern == 3 && bands > 0) ? (height - (bands - 1)) / bands : 0;
+    if (pattern == 5) {
+        // synth.cpp:76-79: threshold = (uint64)(density * 2^64), "all" when it saturates.
+        if (density <= 0.0) {
+            a.all = 0;
+            a.threshold = 0;
+        } else {
+            const double scaled = density * 18446744073709551616.0;
+            a.all = scaled >= 18446744073709551616.0;
+            a.threshold = a.all ? 0 : static_cast<uint64_t>(scaled);
+        }
+    }
+    const int64_t total = pitch * height;
+    if (total == 0) return 0;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    synth_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(a, d_bits);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// d_flags needs ceil(n/32) words rounded up to a multiple of 32; d_n is one long long.
+// Scratch for per-block counts lives after the flags (caller allocates
+// ceil(n/1024) extra int32 in d_flags' tail: see ychg_capi.cu).
+extern "C" int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
+                                      int32_t* d_boundaries, long long* d_n, cudaStream_t stream) {
+    const int64_t blocks = (n + kColsPerBlock - 1) / kColsPerBlock;
+    if (blocks == 0) {
+        cudaMemsetAsync(d_n, 0, sizeof(long long), stream);
+        return 0;
+    }
+    int32_t* block_nb = reinterpret_cast<int32_t*>(d_flags + blocks * (kColsPerBlock / 32));
+    bflags_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_counts, n, d_flags, block_nb);
+    bcompact_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_flags, n, block_nb,
+                                                                   d_boundaries, d_n);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}

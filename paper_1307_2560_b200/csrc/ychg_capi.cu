@@ -1,0 +1,541 @@
+// ychg_capi.cu -- the C ABI (include/ychg_b200.h): plans, device/host entry
+// points, error convention.  No exception crosses this boundary; statuses map
+// to the reference's error classes in the C++ shim (errors.hpp:11-40).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ychg_b200.h"
+#include "ychg_device.cuh"
+#include "ychg_kernels.h"
+
+using ychg_dev::ScanParams;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation)
+        return fail(YCHG_ERR_OOM, "%s: %s", what, cudaGetErrorString(e));
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+        return fail(YCHG_ERR_NO_DEVICE, "%s: %s (no CPU fallback exists)", what, cudaGetErrorString(e));
+    return fail(YCHG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call)                                         \
+    do {                                                 \
+        const cudaError_t e_ = (call);                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+int require_device(int device) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(YCHG_ERR_NO_DEVICE, "no CUDA device available (%s); the yCHG path has no CPU fallback",
+                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    if (device < 0 || device >= n) return fail(YCHG_ERR_INVALID, "device %d out of range [0, %d)", device, n);
+    return YCHG_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------- plans
+struct ychg_plan {
+    int device = 0;
+    ScanParams prm{};
+    int grid = 0;
+    int64_t ws_bytes = 0;
+    void* ws = nullptr;
+    // tensor-map cache
+    const void* map_ptr = nullptr;
+    int64_t map_pitch = 0;
+    alignas(64) CUtensorMap map{};
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    bool ev_recorded = false;
+};
+
+namespace {
+
+// Pick the number of row segments per strip minimising the modelled makespan of
+// the persistent streaming kernel: waves of segments over the SMs, 8 warp bands
+// per segment, +1 block-time per segment for pipeline fill and the CTA merge.
+int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out) {
+    const int max_seg_blocks = ychg_dev::kMaxSegmentRows / ychg_dev::kBlockRows;
+    int kmin = (n_blocks + max_seg_blocks - 1) / max_seg_blocks;
+    if (kmin < 1) kmin = 1;
+    double best = 1e300;
+    int best_k = kmin;
+    for (int k = kmin; k <= std::max(kmin, n_blocks); ++k) {
+        const long long segs = static_cast<long long>(n_strips) * k;
+        const long long G = std::min<long long>(sms, segs);
+        const long long waves = (segs + G - 1) / G;
+        const long long segb = (n_blocks + k - 1) / k;
+        const long long bpw = (segb + ychg_dev::kWarps - 1) / ychg_dev::kWarps;
+        const double cost = static_cast<double>(waves) * static_cast<double>(bpw + 1);
+        if (cost < best - 1e-9) {
+            best = cost;
+            best_k = k;
+        }
+        if (segs > 64LL * sms) break;
+    }
+    const long long segs = static_cast<long long>(n_strips) * best_k;
+    *grid_out = static_cast<int>(std::min<long long>(sms, segs));
+    return best_k;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ychg_last_error(void) { return g_error.c_str(); }
+
+int ychg_abi_version(void) { return YCHG_ABI_VERSION; }
+
+int ychg_device_count(int* n) {
+    int c = 0;
+    const cudaError_t e = cudaGetDeviceCount(&c);
+    if (n) *n = (e == cudaSuccess) ? c : 0;
+    return YCHG_OK;
+}
+
+int ychg_set_device(int device) {
+    if (const int rc = require_device(device)) return rc;
+    CK(cudaSetDevice(device));
+    return YCHG_OK;
+}
+
+int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t height, ychg_plan** out) {
+    if (!out) return fail(YCHG_ERR_INVALID, "plan_create: out is NULL");
+    *out = nullptr;
+    if (width_img < 0 || height < 0 || width_cnt < 0 || width_cnt > width_img)
+        return fail(YCHG_ERR_INVALID, "plan_create: bad geometry width_img=%d width_cnt=%d height=%d",
+                    width_img, width_cnt, height);
+    if (const int rc = require_device(device)) return rc;
+    CK(cudaSetDevice(device));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+
+    auto plan = std::make_unique<ychg_plan>();
+    plan->device = device;
+    ScanParams& p = plan->prm;
+    p.width_img = width_img;
+    p.width_cnt = width_cnt;
+    p.height = height;
+    p.row_bytes = (width_img + 7) / 8;
+    p.n_strips = (width_cnt + ychg_dev::kStripCols - 1) / ychg_dev::kStripCols;
+    p.n_blocks = (height + ychg_dev::kBlockRows - 1) / ychg_dev::kBlockRows;
+    if (p.n_strips > 0 && p.n_blocks > 0) {
+        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid);
+        p.n_segments = p.n_strips * p.seg_per_strip;
+        const int64_t part = int64_t(p.n_segments) * ychg_dev::kStripCols * 4;
+        const int64_t sums = int64_t(p.n_segments) * ychg_dev::kSumPlanes * 32 * 4;
+        const int64_t links = int64_t(p.n_segments) * 8;
+        const int64_t snb = int64_t(p.n_strips) * 4;
+        plan->ws_bytes = part + sums + links + snb + 256;
+        cudaError_t e = cudaMalloc(&plan->ws, plan->ws_bytes);
+        if (e != cudaSuccess) return cuda_fail(e, "plan workspace cudaMalloc");
+        char* w = static_cast<char*>(plan->ws);
+        p.part = reinterpret_cast<uint32_t*>(w);
+        p.sums = reinterpret_cast<uint32_t*>(w + part);
+        p.seg_links = reinterpret_cast<unsigned long long*>(w + part + sums);
+        p.strip_nb = reinterpret_cast<int32_t*>(w + part + sums + links);
+    }
+    *out = plan.release();
+    return YCHG_OK;
+}
+
+void ychg_plan_destroy(ychg_plan* plan) {
+    if (!plan) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(plan->device);
+    if (plan->ws) cudaFree(plan->ws);
+    for (auto& e : plan->ev)
+        if (e) cudaEventDestroy(e);
+    cudaSetDevice(prev);
+    delete plan;
+}
+
+int ychg_plan_get_info(const ychg_plan* plan, ychg_plan_info* out) {
+    if (!plan || !out) return fail(YCHG_ERR_INVALID, "plan_get_info: NULL argument");
+    out->n_strips = plan->prm.n_strips;
+    out->n_blocks = plan->prm.n_blocks;
+    out->seg_per_strip = plan->prm.seg_per_strip;
+    out->n_segments = plan->prm.n_segments;
+    out->grid = plan->grid;
+    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 3 : 0;
+    out->workspace_bytes = plan->ws_bytes;
+    return YCHG_OK;
+}
+
+int ychg_plan_set_timing(ychg_plan* plan, int32_t enabled) {
+    if (!plan) return fail(YCHG_ERR_INVALID, "plan_set_timing: NULL plan");
+    CK(cudaSetDevice(plan->device));
+    if (enabled && !plan->ev[0])
+        for (auto& e : plan->ev) CK(cudaEventCreate(&e));
+    plan->timing = enabled != 0;
+    plan->ev_recorded = false;
+    return YCHG_OK;
+}
+
+int ychg_plan_last_ms(ychg_plan* plan, float* scan_ms, float* finish_ms) {
+    if (!plan || !plan->ev_recorded) return fail(YCHG_ERR_INVALID, "plan_last_ms: no timed scan recorded");
+    CK(cudaEventSynchronize(plan->ev[2]));
+    float a = 0, b = 0;
+    CK(cudaEventElapsedTime(&a, plan->ev[0], plan->ev[1]));
+    CK(cudaEventElapsedTime(&b, plan->ev[1], plan->ev[2]));
+    if (scan_ms) *scan_ms = a;
+    if (finish_ms) *finish_ms = b;
+    return YCHG_OK;
+}
+
+int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int32_t with_hyperedges,
+                     int32_t* d_counts, uint32_t* d_flags, int32_t* d_boundaries, ychg_totals* d_totals,
+                     void* stream) {
+    if (!plan) return fail(YCHG_ERR_INVALID, "scan_device: NULL plan");
+    ScanParams& p = plan->prm;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CK(cudaSetDevice(plan->device));
+    if (!d_totals) return fail(YCHG_ERR_INVALID, "scan_device: d_totals is required");
+    if (p.n_strips == 0 || p.n_blocks == 0) {
+        // W == 0 or H == 0: all-zero counts, no boundaries, no runs (runscan.cpp:122-128).
+        CK(cudaMemsetAsync(d_totals, 0, sizeof(ychg_totals), st));
+        if (!with_hyperedges) {
+            const long long m1 = -1;
+            CK(cudaMemcpyAsync(&d_totals->hyperedges, &m1, sizeof(m1), cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        if (d_counts && p.width_cnt > 0) CK(cudaMemsetAsync(d_counts, 0, int64_t(p.width_cnt) * 4, st));
+        if (d_flags && p.width_cnt > 0) CK(cudaMemsetAsync(d_flags, 0, int64_t((p.width_cnt + 31) / 32) * 4, st));
+        return YCHG_OK;
+    }
+    if (!d_bits || !d_counts || !d_flags || !d_boundaries)
+        return fail(YCHG_ERR_INVALID, "scan_device: NULL device buffer");
+    if (pitch < p.row_bytes || pitch % 16 != 0)
+        return fail(YCHG_ERR_INVALID, "scan_device: pitch %lld must be >= %d and a multiple of 16",
+                    static_cast<long long>(pitch), p.row_bytes);
+    if (reinterpret_cast<uintptr_t>(d_bits) % 16 != 0)
+        return fail(YCHG_ERR_INVALID, "scan_device: image base must be 16-byte aligned");
+
+    if (plan->map_ptr != d_bits || plan->map_pitch != pitch) {
+        auto encode = tensor_map_encoder();
+        if (!encode) return fail(YCHG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.row_bytes), static_cast<cuuint64_t>(p.height)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch)};
+        cuuint32_t box[2] = {ychg_dev::kBoxBytes, ychg_dev::kBlockRows};
+        cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(&plan->map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_bits),
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(YCHG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+        plan->map_ptr = d_bits;
+        plan->map_pitch = pitch;
+    }
+    p.bits = d_bits;
+    p.pitch = pitch;
+    p.counts = d_counts;
+    p.flags = d_flags;
+    p.boundaries = d_boundaries;
+    p.totals = reinterpret_cast<long long*>(d_totals);
+
+    if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
+    const int rc = ychg_launch_scan(&plan->map, &p, plan->grid, with_hyperedges ? 1 : 0, st,
+                                    plan->timing ? plan->ev[1] : nullptr);
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "scan kernels launch");
+    if (plan->timing) {
+        CK(cudaEventRecord(plan->ev[2], st));
+        plan->ev_recorded = true;
+    }
+    return YCHG_OK;
+}
+
+int ychg_synth_device(int32_t pattern, int32_t width, int32_t height, int32_t bands, int32_t cell,
+                      double density, uint64_t seed, uint8_t* d_bits, int64_t pitch, void* stream) {
+    // Validation as synth.cpp:10-34.
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "synth: negative dimensions %dx%d", width, height);
+    if (pattern < 0 || pattern > 5) return fail(YCHG_ERR_INVALID, "synth: unknown pattern %d", pattern);
+    if (pattern == YCHG_PATTERN_HBANDS && (bands < 1 || bands > height / 2))
+        return fail(YCHG_ERR_INVALID, "synth: hbands(%d) needs 1 <= k <= height/2 = %d", bands, height / 2);
+    if (pattern == YCHG_PATTERN_CHECKER && cell < 1)
+        return fail(YCHG_ERR_INVALID, "synth: checker cell must be >= 1, got %d", cell);
+    if (pattern == YCHG_PATTERN_RANDOM && !(density >= 0.0 && density <= 1.0))
+        return fail(YCHG_ERR_INVALID, "synth: random density must lie in [0, 1], got %f", density);
+    if (pitch < (width + 7) / 8) return fail(YCHG_ERR_INVALID, "synth: pitch too small");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (const int rc = require_device(dev)) return rc;
+    const int rc = ychg_launch_synth(pattern, width, height, bands, cell, density, seed, d_bits, pitch,
+                                     static_cast<cudaStream_t>(stream));
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "synth kernel launch");
+    return YCHG_OK;
+}
+
+// ---------------------------------------------------------------------------- memory helpers
+int ychg_device_alloc(int device, int64_t bytes, void** out) {
+    if (!out) return fail(YCHG_ERR_INVALID, "device_alloc: out is NULL");
+    if (const int rc = require_device(device)) return rc;
+    CK(cudaSetDevice(device));
+    CK(cudaMalloc(out, bytes > 0 ? bytes : 16));
+    return YCHG_OK;
+}
+int ychg_device_free(int device, void* p) {
+    CK(cudaSetDevice(device));
+    CK(cudaFree(p));
+    return YCHG_OK;
+}
+int ychg_host_alloc_pinned(int64_t bytes, void** out) {
+    if (!out) return fail(YCHG_ERR_INVALID, "host_alloc_pinned: out is NULL");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return fail(YCHG_ERR_NO_DEVICE, "no CUDA device available for pinned allocation");
+    CK(cudaMallocHost(out, bytes > 0 ? bytes : 16));
+    return YCHG_OK;
+}
+int ychg_host_free_pinned(void* p) {
+    CK(cudaFreeHost(p));
+    return YCHG_OK;
+}
+int ychg_memcpy(void* dst, const void* src, int64_t bytes, void* stream) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    return YCHG_OK;
+}
+int ychg_memcpy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width_bytes,
+                   int64_t height, void* stream) {
+    CK(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width_bytes, height, cudaMemcpyDefault,
+                         static_cast<cudaStream_t>(stream)));
+    return YCHG_OK;
+}
+int ychg_memset(void* dst, int32_t value, int64_t bytes, void* stream) {
+    CK(cudaMemsetAsync(dst, value, bytes, static_cast<cudaStream_t>(stream)));
+    return YCHG_OK;
+}
+int ychg_stream_create(int device, void** out) {
+    if (const int rc = require_device(device)) return rc;
+    CK(cudaSetDevice(device));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *out = s;
+    return YCHG_OK;
+}
+int ychg_stream_destroy(void* stream) {
+    CK(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+    return YCHG_OK;
+}
+int ychg_stream_synchronize(void* stream) {
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return YCHG_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------- host entry points
+namespace {
+
+// Per-device cached state for the host-buffer API.  One mutex per device
+// serialises callers (the reference functions are reentrant; so are these).
+struct HostContext {
+    std::mutex mu;
+    int device = 0;
+    bool ready = false;
+    cudaStream_t stream = nullptr;
+    ychg_plan* plan = nullptr;
+    int32_t plan_w = -1, plan_h = -1;
+    uint8_t* d_bits = nullptr;
+    int64_t bits_cap = 0;
+    int32_t* d_counts = nullptr;
+    uint32_t* d_flags = nullptr;
+    int32_t* d_bounds = nullptr;
+    int64_t cols_cap = 0;
+    ychg_totals* d_totals = nullptr;
+    ychg_totals* h_totals = nullptr;  // pinned
+};
+
+HostContext& host_context(int device) {
+    static HostContext ctx[64];
+    ctx[device].device = device;
+    return ctx[device];
+}
+
+int ensure_context(HostContext& c) {
+    CK(cudaSetDevice(c.device));
+    if (!c.ready) {
+        CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        CK(cudaMalloc(&c.d_totals, sizeof(ychg_totals)));
+        CK(cudaMallocHost(&c.h_totals, sizeof(ychg_totals)));
+        c.ready = true;
+    }
+    return YCHG_OK;
+}
+
+int ensure_columns(HostContext& c, int64_t cols) {
+    if (cols <= c.cols_cap) return YCHG_OK;
+    cudaFree(c.d_counts);
+    cudaFree(c.d_flags);
+    cudaFree(c.d_bounds);
+    c.d_counts = nullptr;
+    c.d_flags = nullptr;
+    c.d_bounds = nullptr;
+    c.cols_cap = 0;
+    const int64_t cap = std::max<int64_t>(cols, 1024);
+    // flags: one word per 32 columns, rounded to whole 1024-column blocks, + per-block scratch
+    const int64_t fwords = ((cap + 1023) / 1024) * 32 + (cap + 1023) / 1024 + 32;
+    CK(cudaMalloc(&c.d_counts, cap * 4));
+    CK(cudaMalloc(&c.d_flags, fwords * 4));
+    CK(cudaMalloc(&c.d_bounds, cap * 4));
+    c.cols_cap = cap;
+    return YCHG_OK;
+}
+
+int pick_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    return dev;
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                              int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
+                              ychg_totals* totals_out) {
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan: negative geometry %dx%d", width, height);
+    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
+        return fail(YCHG_ERR_INVALID, "scan: row_stride %lld < %lld", static_cast<long long>(row_stride),
+                    static_cast<long long>(row_bytes));
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+
+    if (width == 0 || height == 0) {
+        if (counts_out && width > 0) std::memset(counts_out, 0, size_t(width) * 4);
+        if (totals_out) *totals_out = ychg_totals{0, 0, with_hyperedges ? 0 : -1, 0};
+        return YCHG_OK;
+    }
+    if (c.plan_w != width || c.plan_h != height) {
+        ychg_plan_destroy(c.plan);
+        c.plan = nullptr;
+        c.plan_w = c.plan_h = -1;
+        if (const int rc = ychg_plan_create(device, width, width, height, &c.plan)) return rc;
+        c.plan_w = width;
+        c.plan_h = height;
+    }
+    const int64_t pitch = (row_bytes + 15) / 16 * 16;
+    const int64_t need = pitch * height;
+    if (need > c.bits_cap) {
+        cudaFree(c.d_bits);
+        c.d_bits = nullptr;
+        c.bits_cap = 0;
+        CK(cudaMalloc(&c.d_bits, need));
+        c.bits_cap = need;
+    }
+    if (const int rc = ensure_columns(c, width)) return rc;
+
+    // H2D: pinned sources go straight to the copy engine; pageable ones are staged by the driver.
+    (void)is_pinned;
+    CK(cudaMemcpy2DAsync(c.d_bits, pitch, bits, row_stride, row_bytes, height, cudaMemcpyHostToDevice,
+                         c.stream));
+    if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, c.d_counts, c.d_flags,
+                                        c.d_bounds, c.d_totals, c.stream))
+        return rc;
+    CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
+    if (counts_out)
+        CK(cudaMemcpyAsync(counts_out, c.d_counts, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    const ychg_totals t = *c.h_totals;
+    if (boundaries_out && t.n_boundaries > 0) {
+        CK(cudaMemcpyAsync(boundaries_out, c.d_bounds, t.n_boundaries * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    }
+    if (totals_out) *totals_out = t;
+    return YCHG_OK;
+}
+
+extern "C" int ychg_cut_vertex_counts(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                      int32_t strategy_kind, int32_t threads, int32_t* counts_out) {
+    // runscan.cpp:24-26: a parallel strategy needs threads >= 1.  Every valid
+    // strategy then runs the one GPU path (outputs are strategy-independent,
+    // runscan.hpp:24-25).
+    if (strategy_kind != YCHG_STRATEGY_SERIAL && strategy_kind != YCHG_STRATEGY_PARALLEL)
+        return fail(YCHG_ERR_INVALID, "scan: unknown strategy kind %d", strategy_kind);
+    if (strategy_kind == YCHG_STRATEGY_PARALLEL && threads < 1)
+        return fail(YCHG_ERR_INVALID, "scan: parallel strategy needs threads >= 1, got %d", threads);
+    if (width > 0 && !counts_out) return fail(YCHG_ERR_INVALID, "cut_vertex_counts: counts_out is NULL");
+    return ychg_scan_host(bits, width, height, row_stride, 0, counts_out, nullptr, nullptr);
+}
+
+extern "C" int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, int32_t* boundaries_out,
+                                            int64_t* n_out) {
+    if (n < 0) return fail(YCHG_ERR_INVALID, "detect_boundary_columns: negative length");
+    if (n > 0 && (!counts || !boundaries_out)) return fail(YCHG_ERR_INVALID, "detect_boundary_columns: NULL buffer");
+    if (n > INT32_MAX) return fail(YCHG_ERR_INVALID, "detect_boundary_columns: more than 2^31-1 columns");
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+    if (n == 0) {
+        if (n_out) *n_out = 0;
+        return YCHG_OK;
+    }
+    if (const int rc = ensure_columns(c, n)) return rc;
+    CK(cudaMemcpyAsync(c.d_counts, counts, n * 4, cudaMemcpyHostToDevice, c.stream));
+    const int rc = ychg_launch_boundaries(c.d_counts, n, c.d_flags, c.d_bounds,
+                                          reinterpret_cast<long long*>(&c.d_totals->n_boundaries), c.stream);
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "boundary kernels launch");
+    CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    const int64_t nb = c.h_totals->n_boundaries;
+    if (nb > 0) {
+        CK(cudaMemcpyAsync(boundaries_out, c.d_bounds, nb * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    }
+    if (n_out) *n_out = nb;
+    return YCHG_OK;
+}

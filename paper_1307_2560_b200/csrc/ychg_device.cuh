@@ -1,0 +1,184 @@
+// ychg_device.cuh -- sm_100a device building blocks for the yCHG column scan.
+//
+// Bit layout (reference image.hpp:10-22,35-36): row-major, MSB-first bytes, rows
+// of ceil(W/8) bytes.  On the device every 32-column word is byte-swapped once
+// after loading (one PRMT) so that column 32w+j sits at bit 31-j: the right
+// neighbour of every column is then "shift left by one", with the first column
+// of the next word funnelled in.
+//
+// All per-pixel work is bit-sliced: one 32-bit register carries one bit of 32
+// columns (K1) or of 32 adjacent column pairs (K3).
+#pragma once
+
+#include <cstdint>
+
+namespace ychg_dev {
+
+constexpr int kWarps = 8;                        // warps per CTA
+constexpr int kThreads = kWarps * 32;
+constexpr int kStripWords = 32;                  // one warp lane per 32-column word
+constexpr int kStripCols = kStripWords * 32;     // 1024 columns per strip
+constexpr int kStripBytes = kStripWords * 4;     // 128 B of every row
+constexpr int kBoxBytes = kStripBytes + 16;      // + 16 B right halo (next strip's first word)
+constexpr int kBlockRows = 32;                   // rows per TMA stage / per Harley-Seal block
+constexpr int kStages = 4;                       // TMA ring depth per warp
+constexpr int kStageBytes = kBoxBytes * kBlockRows;   // 4608 B
+constexpr int kFlushBlocks = 15;                 // 8-bit bit-sliced counters: <= 15*16+15 = 255
+constexpr int kSumPlanes = 7;                    // K3 band summary planes (see BandSummary)
+constexpr int kMaxSegmentRows = 65504;           // u16 SWAR accumulators: counts <= rows/2 < 2^15
+
+// Shared-memory layout of the scan kernel (bytes).
+constexpr int kSmemStages = kWarps * kStages * kStageBytes;            // 147456
+constexpr int kSmemHalo = kWarps * 2 * 32 * 4;                         // halo-row words
+constexpr int kSmemBar = kWarps * kStages * 8;                         // mbarriers
+constexpr int kSmemAcc = kWarps * 16 * 32 * 4;                         // per-warp u16x2 counts
+constexpr int kSmemSum = kWarps * kSumPlanes * 32 * 4;                 // per-warp K3 summaries
+constexpr int kSmemMisc = kWarps * 16;                                 // links + flags
+constexpr int kSmemTotal = kSmemStages + kSmemHalo + kSmemBar + kSmemAcc + kSmemSum + kSmemMisc;
+
+// ----------------------------------------------------------------------------
+// Launch parameters shared by the three kernels of one scan.
+struct ScanParams {
+    const uint8_t* bits;      // device image base (row-major packed bits)
+    int64_t pitch;            // bytes between rows (multiple of 16 for TMA)
+    int32_t width_img;        // columns present in the buffer (incl. a right halo)
+    int32_t width_cnt;        // columns counted: [0, width_cnt)
+    int32_t height;
+    int32_t row_bytes;        // ceil(width_img / 8)
+    int32_t n_strips;         // ceil(width_cnt / 1024)
+    int32_t n_blocks;         // ceil(height / 32)
+    int32_t seg_per_strip;    // k: row segments per strip
+    int32_t n_segments;       // n_strips * k
+    uint32_t* part;           // [n_segments][1024] per-segment column counts
+    uint32_t* sums;           // [n_segments][7][32] K3 band summaries
+    unsigned long long* seg_links;  // [n_segments] links closed inside each segment
+    long long* totals;        // ychg_totals {total_runs, links, hyperedges, n_boundaries}
+    int32_t* counts;          // [width_cnt] final per-column counts
+    uint32_t* flags;          // [ceil(width_cnt/32)] change flags, bit j = column 32w+j
+    int32_t* boundaries;      // [<= width_cnt] ascending boundary columns
+    int32_t* strip_nb;        // [n_strips] boundary columns per strip
+};
+
+// Segment j of a strip covers row blocks [seg_first(j), seg_first(j+1)).
+__host__ __device__ inline int seg_first_block(int j, int k, int n_blocks) {
+    return static_cast<int>((static_cast<long long>(j) * n_blocks) / k);
+}
+
+// ----------------------------------------------------------------------------
+// Small PTX helpers (mbarrier + TMA).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_addr(dst)), "l"(tmap), "r"(x), "r"(y), "r"(smem_addr(bar)) : "memory");
+}
+
+// ----------------------------------------------------------------------------
+// Bit-sliced arithmetic.
+//
+// Carry-save adder: l = a ^ b ^ c, h = majority(a, b, c); two LOP3 each.
+__device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
+    const uint32_t u = a ^ b;
+    h = (a & b) | (u & c);
+    l = u ^ c;
+}
+
+// 8 bit-planes (x[k] = bit k of 32 per-column counters) -> per-column bytes:
+// after the call, byte L of x[p] is the 8-bit counter of the column at bit 8L+p.
+// Three rounds of block swaps inside every byte lane (4x4, 2x2, 1x1).
+__device__ __forceinline__ void transpose8x8_bytes(uint32_t (&x)[8]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t t = ((x[k] >> 4) ^ x[k + 4]) & 0x0F0F0F0Fu;
+        x[k + 4] ^= t;
+        x[k] ^= t << 4;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (k & 2) continue;
+        const uint32_t t = ((x[k] >> 2) ^ x[k + 2]) & 0x33333333u;
+        x[k + 2] ^= t;
+        x[k] ^= t << 2;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        const uint32_t t = ((x[k] >> 1) ^ x[k + 1]) & 0x55555555u;
+        x[k + 1] ^= t;
+        x[k] ^= t << 1;
+    }
+}
+
+// Column (0..31, left to right inside its word) held by u16 lane `half` of
+// accumulator acc[i] (i = 2p + kind) after flush_counts: see flush_counts.
+__host__ __device__ inline int acc_column(int i, int half) {
+    const int p = i >> 1, kind = i & 1;
+    // kind 0 keeps byte lanes {0,2}, kind 1 keeps {1,3}; half selects the upper lane.
+    const int L = kind + 2 * half;
+    return 31 - (8 * L + p);
+}
+
+// ----------------------------------------------------------------------------
+// K3 band summary.  Per column pair (c, c+1), the strip's
+// 4-connected components are row intervals; a component is a decompose() link
+// iff it contains exactly two runs (hypergraph.cpp:137-143: one run per column,
+// mutually unique).  A band of rows [y0, y1) is summarised per pair by
+//   O   a component is open across the band's top edge (the "head"),
+//   E   the head closed inside the band,
+//   h1,h2  head gained >= 1 / >= 2 new runs inside the band,
+//   OE  a component is open across the bottom edge,
+//   T2,T3  that component holds >= 2 / >= 3 runs (only meaningful when the
+//          bottom component started inside the band).
+// Links of components that start and end inside the band are counted directly.
+struct BandSummary {
+    uint32_t O, E, h1, h2, OE, T2, T3;
+};
+
+// Compose summary A (upper band) with B (the band directly below).  Returns the
+// bit mask of pairs whose component straddling the A/B edge closes inside B as
+// a link; `C` is the summary of the union.
+__device__ __forceinline__ uint32_t compose_summary(const BandSummary& A, const BandSummary& B,
+                                                    BandSummary& C) {
+    const uint32_t Ap = A.O & ~A.E;   // A's head runs through all of A
+    const uint32_t Bp = B.O & ~B.E;   // B's head runs through all of B
+    const uint32_t s1 = A.h1 | B.h1;
+    const uint32_t s2 = A.h2 | B.h2 | (A.h1 & B.h1);
+    const uint32_t J = ~Ap & A.OE;    // A's bottom component is known and enters B
+    // N_in = 1 + T2 + T3 (saturating); a link iff N_in + nf_B == 2.
+    const uint32_t resolved =
+        J & B.E & ((~A.T2 & B.h1 & ~B.h2) | (A.T2 & ~A.T3 & ~B.h1));
+    C.O = A.O;
+    C.E = (Ap & B.E) | (~Ap & A.E);
+    C.h1 = (Ap & s1) | (~Ap & A.h1);
+    C.h2 = (Ap & s2) | (~Ap & A.h2);
+    C.OE = B.OE;
+    C.T2 = (Bp & (A.T2 | B.h1)) | (~Bp & B.T2);
+    C.T3 = (Bp & (A.T3 | (A.T2 & B.h1) | B.h2)) | (~Bp & B.T3);
+    return resolved;
+}
+
+}  // namespace ychg_dev

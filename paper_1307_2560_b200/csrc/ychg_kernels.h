@@ -1,0 +1,22 @@
+// ychg_kernels.h -- internal launcher declarations shared by the .cu units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ychg_dev {
+struct ScanParams;
+}
+
+extern "C" {
+// Enqueue scan + finish + compact on `stream`; records ev_mid (if non-null)
+// between the streaming kernel and the finish kernels.  Returns cudaError_t.
+int ychg_launch_scan(const void* tmap, const ychg_dev::ScanParams* prm, int grid, int with_links,
+                     cudaStream_t stream, cudaEvent_t ev_mid);
+
+int ychg_launch_synth(int pattern, int width, int height, int bands, int cell, double density,
+                      uint64_t seed, uint8_t* d_bits, int64_t pitch, cudaStream_t stream);
+
+int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
+                           int32_t* d_boundaries, long long* d_n, cudaStream_t stream);
+}

@@ -1,0 +1,68 @@
+// ychg_runscan.cpp -- the C++ drop-in: ychg::cut_vertex_counts and
+// ychg::detect_boundary_columns (reference runscan.hpp:59-71) implemented over
+// the C ABI of libychg_b200.so.  Status codes become the reference's exception
+// types (errors.hpp:11-40); there is no CPU fallback.
+#include <string>
+#include <vector>
+
+#include "ychg/errors.hpp"
+#include "ychg/image.hpp"
+#include "ychg/runscan.hpp"
+#include "ychg/scan_b200.hpp"
+#include "ychg_b200.h"
+
+namespace ychg {
+
+namespace {
+
+void check(int rc, const char* what) {
+    if (rc == YCHG_OK) return;
+    const std::string msg = std::string(what) + ": " + ychg_last_error();
+    if (rc == YCHG_ERR_INVALID) throw ValidationError(msg);
+    throw Error(msg);
+}
+
+}  // namespace
+
+std::int64_t foreground_count(const BinaryImage& image) {
+    std::int64_t n = 0;
+    for (std::uint8_t b : image.bytes()) n += __builtin_popcount(b);
+    return n;
+}
+
+std::vector<int> cut_vertex_counts(const BinaryImage& image, ScanStrategy strategy) {
+    std::vector<int> counts(static_cast<std::size_t>(image.width()), 0);
+    const int kind = strategy.kind == ScanStrategy::Kind::serial ? YCHG_STRATEGY_SERIAL
+                                                                  : YCHG_STRATEGY_PARALLEL;
+    check(ychg_cut_vertex_counts(image.bytes().data(), image.width(), image.height(),
+                                 image.row_stride(), kind, strategy.threads, counts.data()),
+          "cut_vertex_counts");
+    return counts;
+}
+
+std::vector<int> detect_boundary_columns(std::span<const int> counts) {
+    std::vector<int> out(counts.size());
+    std::int64_t n = 0;
+    check(ychg_detect_boundary_columns(counts.data(), static_cast<std::int64_t>(counts.size()),
+                                       out.data(), &n),
+          "detect_boundary_columns");
+    out.resize(static_cast<std::size_t>(n));
+    return out;
+}
+
+ScanResult scan(const BinaryImage& image) {
+    ScanResult r;
+    r.counts.assign(static_cast<std::size_t>(image.width()), 0);
+    r.boundaries.assign(static_cast<std::size_t>(image.width()), 0);
+    ychg_totals t{};
+    check(ychg_scan_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), 1,
+                         r.counts.data(), r.boundaries.data(), &t),
+          "scan");
+    r.boundaries.resize(static_cast<std::size_t>(t.n_boundaries));
+    r.total_runs = t.total_runs;
+    r.links = t.links;
+    r.hyperedges = t.hyperedges;
+    return r;
+}
+
+}  // namespace ychg

@@ -1,0 +1,109 @@
+// dropin_test.cpp -- the reference's runscan known-answer tests, compiled
+// against OUR ychg headers and linked against libychg.so (the C++ drop-in).
+// Vectors from proj/tests/test_runscan.cpp:35-49,66-85,129-143 and
+// acceptance.cpp:101-121.  Exit code = number of failed checks.
+#include <cstdio>
+#include <vector>
+
+#include "ychg/errors.hpp"
+#include "ychg/image.hpp"
+#include "ychg/runscan.hpp"
+#include "ychg/scan_b200.hpp"
+
+using namespace ychg;
+
+static int failures = 0;
+#define CHECK(cond)                                                   \
+    do {                                                              \
+        if (!(cond)) {                                                \
+            std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond); \
+            ++failures;                                               \
+        }                                                             \
+    } while (0)
+
+static BinaryImage full(int w, int h) {
+    BinaryImage img(w, h);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) img.set(x, y, true);
+    return img;
+}
+static BinaryImage frame(int w, int h) {
+    BinaryImage img(w, h);
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+            if (x == 0 || y == 0 || x == w - 1 || y == h - 1) img.set(x, y, true);
+    return img;
+}
+static BinaryImage hbands(int w, int h, int k) {
+    BinaryImage img(w, h);
+    const int bh = (h - (k - 1)) / k;
+    for (int b = 0; b < k; ++b)
+        for (int y = b * (bh + 1); y < b * (bh + 1) + bh; ++y)
+            for (int x = 0; x < w; ++x) img.set(x, y, true);
+    return img;
+}
+static BinaryImage branch() {
+    BinaryImage img(2, 7);
+    for (int y : {0, 1, 3, 4, 5, 6}) img.set(0, y, true);
+    for (int y : {0, 1, 2, 3, 4, 6}) img.set(1, y, true);
+    return img;
+}
+
+int main() {
+    const auto serial = ScanStrategy::serial();
+    CHECK(cut_vertex_counts(full(4, 4), serial) == (std::vector<int>{1, 1, 1, 1}));
+    CHECK(cut_vertex_counts(frame(5, 5), serial) == (std::vector<int>{1, 2, 2, 2, 1}));
+    CHECK(cut_vertex_counts(BinaryImage(3, 3), serial) == (std::vector<int>{0, 0, 0}));
+    CHECK(cut_vertex_counts(branch(), serial) == (std::vector<int>{2, 2}));
+    CHECK(cut_vertex_counts(BinaryImage(0, 0), serial).empty());
+    CHECK(cut_vertex_counts(hbands(8, 11, 3), serial) == std::vector<int>(8, 3));
+    for (int t : {1, 2, 4, 8, 16})
+        CHECK(cut_vertex_counts(frame(5, 5), ScanStrategy::parallel(t)) ==
+              (std::vector<int>{1, 2, 2, 2, 1}));
+
+    bool threw = false;
+    try {
+        cut_vertex_counts(full(3, 50), ScanStrategy::parallel(0));
+    } catch (const ValidationError&) {
+        threw = true;
+    }
+    CHECK(threw);
+    threw = false;
+    try {
+        cut_vertex_counts(full(3, 50), ScanStrategy::parallel(-2));
+    } catch (const ValidationError&) {
+        threw = true;
+    }
+    CHECK(threw);
+
+    CHECK(detect_boundary_columns(std::vector<int>{1, 2, 2, 2, 1}) == (std::vector<int>{0, 1, 4}));
+    CHECK(detect_boundary_columns(std::vector<int>{0, 0, 0}).empty());
+    CHECK(detect_boundary_columns(std::vector<int>{}).empty());
+    CHECK(detect_boundary_columns(std::vector<int>{0, 1}) == (std::vector<int>{1}));
+    CHECK(detect_boundary_columns(std::vector<int>{3}) == (std::vector<int>{0}));
+    CHECK(detect_boundary_columns(std::vector<int>{2, 2}) == (std::vector<int>{0}));
+    CHECK(detect_boundary_columns(cut_vertex_counts(branch(), serial)) == (std::vector<int>{0}));
+
+    // acceptance.cpp:101-121 -- branch: counts [2,2], boundaries [0], 4 hyperedges.
+    const ScanResult br = scan(branch());
+    CHECK(br.counts == (std::vector<int>{2, 2}));
+    CHECK(br.boundaries == (std::vector<int>{0}));
+    CHECK(br.hyperedges == 4);
+    const ScanResult fr = scan(frame(5, 5));
+    CHECK(fr.boundaries == (std::vector<int>{0, 1, 4}));
+    CHECK(fr.hyperedges == 4);
+    CHECK(fr.total_runs == 8);
+    // test_hypergraph.cpp:75-88
+    for (int k : {1, 3, 7}) CHECK(scan(hbands(20, 20, k)).hyperedges == k);
+    BinaryImage chk(8, 8);
+    for (int y = 0; y < 8; ++y)
+        for (int x = 0; x < 8; ++x)
+            if ((x + y) % 2 == 0) chk.set(x, y, true);
+    CHECK(scan(chk).hyperedges == 32);
+    CHECK(scan(BinaryImage(3, 3)).hyperedges == 0);
+    CHECK(scan(BinaryImage(0, 0)).hyperedges == 0);
+    CHECK(foreground_count(frame(5, 5)) == 16);
+
+    std::printf("dropin_test: %d failure(s)\n", failures);
+    return failures;
+}

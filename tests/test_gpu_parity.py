@@ -1,0 +1,206 @@
+"""GPU parity: the sm_100a path, called through the C ABI, against the oracle and
+the reference golden fixtures.  Bit-exact for everything (integer work)."""
+import hashlib
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from golden_io import acceptance2, corpus, large, spec_of
+from oracle import Spec, branch_example
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PAT = {0: "full", 1: "empty", 2: "frame", 3: "hbands", 4: "checker", 5: "random"}
+
+
+def sha(a):
+    return hashlib.sha256(np.asarray(a, dtype="<i4").tobytes()).hexdigest()
+
+
+def image(y, orc, sp):
+    return y.BinaryImage(sp.width, sp.height, orc.synth(sp))
+
+
+def test_known_answers(gpu):
+    y = gpu
+    assert y.cut_vertex_counts(y.synth("full", 4, 4)).tolist() == [1, 1, 1, 1]
+    assert y.cut_vertex_counts(y.synth("frame", 5, 5)).tolist() == [1, 2, 2, 2, 1]
+    assert y.cut_vertex_counts(y.BinaryImage(3, 3)).tolist() == [0, 0, 0]
+    br = y.BinaryImage(2, 7, branch_example())
+    assert y.cut_vertex_counts(br).tolist() == [2, 2]
+    assert y.cut_vertex_counts(y.BinaryImage(0, 0)).tolist() == []
+    assert y.cut_vertex_counts(y.synth("hbands", 8, 11, bands=3)).tolist() == [3] * 8
+    for counts, want in [([1, 2, 2, 2, 1], [0, 1, 4]), ([0, 0, 0], []), ([], []), ([0, 1], [1]), ([3], [0]),
+                         ([2, 2], [0])]:
+        assert y.detect_boundary_columns(counts).tolist() == want
+    r = y.scan(br)
+    assert (r.counts.tolist(), r.boundaries.tolist(), r.hyperedges) == ([2, 2], [0], 4)
+    f = y.scan(y.synth("frame", 5, 5))
+    assert (f.boundaries.tolist(), f.hyperedges, f.total_runs) == ([0, 1, 4], 4, 8)
+
+
+def test_strategies_identical_and_validated(gpu, orc):
+    y = gpu
+    img = image(y, orc, Spec.random(3, 50, 0.5, 8))
+    base = y.cut_vertex_counts(img, y.ScanStrategy.serial())
+    for t in (1, 2, 4, 8, 16):
+        assert np.array_equal(y.cut_vertex_counts(img, y.ScanStrategy.parallel(t)), base)
+    with pytest.raises(y.ValidationError):
+        y.cut_vertex_counts(img, y.ScanStrategy.parallel(0))
+
+
+def test_golden_corpus(gpu, orc):
+    y = gpu
+    for row in corpus():
+        sp = spec_of(row["spec"])
+        r = y.scan(image(y, orc, sp))
+        assert r.counts.tolist() == row["counts"], row["name"]
+        assert r.boundaries.tolist() == row["boundaries"], row["name"]
+        assert r.hyperedges == row["hyperedges"], row["name"]
+        assert r.total_runs == sum(row["counts"]), row["name"]
+
+
+def test_counts_only_path_matches(gpu, orc):
+    y = gpu
+    for row in corpus()[::11]:
+        sp = spec_of(row["spec"])
+        assert y.cut_vertex_counts(image(y, orc, sp)).tolist() == row["counts"], row["name"]
+
+
+def test_byte_boundary_widths(gpu, orc):
+    # test_runscan.cpp:51-64 widths, plus word/strip edges of the GPU layout
+    y = gpu
+    for w in (1, 7, 8, 9, 16, 17, 31, 32, 33, 63, 64, 65, 70, 1023, 1024, 1025, 1031, 2047, 2049):
+        for seed in (5, 6):
+            sp = Spec.random(w, 33, 0.5, seed)
+            bits = orc.synth(sp)
+            r = y.scan(y.BinaryImage(w, 33, bits))
+            c = orc.counts(bits, w)
+            assert np.array_equal(r.counts, c), w
+            assert np.array_equal(r.boundaries, orc.boundaries(c)), w
+            assert r.hyperedges == orc.hyperedges(bits, w)[0], w
+
+
+def test_acceptance2_512(gpu, orc):
+    y = gpu
+    for row in acceptance2():
+        sp = spec_of(row["spec"])
+        r = y.scan(image(y, orc, sp))
+        assert sha(r.counts) == row["counts_sha256"]
+        assert r.boundaries.size == row["n_boundaries"]
+        assert r.hyperedges == row["hyperedges"]
+
+
+@pytest.mark.parametrize("idx", range(10))
+def test_large_golden(gpu, orc, idx):
+    y = gpu
+    row = large()[idx]
+    sp = spec_of(row["spec"])
+    dev = y.synth(PAT[sp.pattern], sp.width, sp.height, bands=sp.bands, cell=sp.cell, density=sp.density,
+                  seed=sp.seed)
+    r = y.scan(dev)
+    assert sha(r.counts) == row["counts_sha256"]
+    assert sha(r.boundaries) == row["boundaries_sha256"]
+    assert r.n_boundaries == row["n_boundaries"]
+    assert r.hyperedges == row["hyperedges"]
+    assert r.total_runs == row["total_runs"]
+
+
+def test_random_geometries_vs_oracle(gpu, orc):
+    y = gpu
+    rng = np.random.default_rng(2024)
+    for _ in range(60):
+        w, h = int(rng.integers(1, 5000)), int(rng.integers(1, 700))
+        sp = Spec.random(w, h, float(rng.choice([0.05, 0.3, 0.5, 0.8, 0.97])), int(rng.integers(0, 1 << 62)))
+        bits = orc.synth(sp)
+        r = y.scan(y.BinaryImage(w, h, bits))
+        c = orc.counts(bits, w)
+        assert np.array_equal(r.counts, c), sp
+        assert np.array_equal(r.boundaries, orc.boundaries(c)), sp
+        assert r.hyperedges == orc.hyperedges(bits, w)[0], sp
+
+
+def test_device_synth_bit_exact(gpu, orc):
+    y = gpu
+    for sp in [Spec.random(1001, 77, 0.37, 123456789), Spec.random(64, 64, 1.0, 3), Spec.random(64, 64, 0.0, 3),
+               Spec.hbands(333, 100, 7), Spec.checker(129, 65, 3), Spec.frame(17, 9), Spec.full(9, 3),
+               Spec.empty(40, 4)]:
+        d = y.synth(PAT[sp.pattern], sp.width, sp.height, bands=sp.bands, cell=sp.cell, density=sp.density,
+                    seed=sp.seed)
+        assert np.array_equal(d.bytes(), orc.synth(sp)), sp
+    with pytest.raises(y.ValidationError):
+        y.synth("hbands", 10, 10, bands=6)
+
+
+def test_garbage_padding_bits_ignored(gpu, orc):
+    # counts never look at columns >= W (runscan.cpp:41-74); neither may the pair step
+    y = gpu
+    sp = Spec.random(37, 64, 0.5, 77)
+    bits = orc.synth(sp)
+    dirty = bits.copy()
+    dirty[:, -1] |= 0x07  # the 3 padding bits of the last byte
+    r = y.scan(y.BinaryImage(37, 64, dirty))
+    c = orc.counts(bits, 37)
+    assert np.array_equal(r.counts, c)
+    assert r.hyperedges == orc.hyperedges(bits, 37)[0]
+
+
+def test_device_api_and_halo_strips(gpu, orc):
+    """Column strips with a right halo (multi-GPU layout) computed through ychg_scan_device."""
+    y = gpu
+    W, H = 5000, 900
+    bits = orc.synth(Spec.random(W, H, 0.5, 4242))
+    counts = orc.counts(bits, W)
+    pair = orc.pair_links(bits, W)
+    bounds = [0, 2048, 3072, W]
+    total_links = 0
+    for i in range(3):
+        c0, c1 = bounds[i], bounds[i + 1]
+        halo = 8 if c1 < W else 0
+        wimg = (c1 - c0) + halo
+        sub = np.unpackbits(bits, axis=1)[:, c0:c0 + wimg]
+        sub = np.packbits(sub, axis=1)
+        pitch = y.pitch_for(wimg)
+        dev = np.zeros((H, pitch), np.uint8)
+        dev[:, : sub.shape[1]] = sub
+        dbits = y.DeviceBuffer(dev.nbytes)
+        dbits.from_host(dev)
+        n = c1 - c0
+        dc, df, db = y.DeviceBuffer(4 * n), y.DeviceBuffer(4 * ((n + 31) // 32 + 32)), y.DeviceBuffer(4 * n)
+        dt = y.DeviceBuffer(32)
+        plan = y.Plan(wimg, H, width_cnt=n)
+        plan.scan_device(dbits.ptr, pitch, dc.ptr, df.ptr, db.ptr, dt.ptr)
+        got = dc.to_host(np.zeros(n, np.int32))
+        tot = dt.to_host(np.zeros(4, np.int64))
+        assert np.array_equal(got, counts[c0:c1])
+        assert tot[0] == counts[c0:c1].sum()
+        assert tot[1] == pair[c0:c1].sum()
+        total_links += int(tot[1])
+        plan.close()
+    assert counts.sum() - total_links == orc.hyperedges(bits, W)[0]
+
+
+def test_timing_hooks(gpu):
+    y = gpu
+    W = H = 2048
+    pitch = y.pitch_for(W)
+    d = y.DeviceBuffer(pitch * H)
+    y.synth_device("random", W, H, d.ptr, pitch, density=0.5, seed=1)
+    dc, df, db, dt = y.DeviceBuffer(4 * W), y.DeviceBuffer(4 * (W // 32 + 64)), y.DeviceBuffer(4 * W), y.DeviceBuffer(32)
+    plan = y.Plan(W, H)
+    plan.set_timing(True)
+    plan.scan_device(d.ptr, pitch, dc.ptr, df.ptr, db.ptr, dt.ptr)
+    a, b = plan.last_ms()
+    assert a > 0 and b > 0
+    info = plan.info()
+    assert info.kernels_per_scan == 3 and info.grid >= 1
+
+
+def test_cxx_dropin_binary(gpu):
+    exe = os.path.join(ROOT, "tests", "cpp", "dropin_test")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr

@@ -1,0 +1,112 @@
+"""CPU: pin the oracle restatement to the reference's own known answers and to
+the golden fixtures generated from the unmodified reference (oracle/_ref)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from golden_io import acceptance2, corpus, large, spec_of
+from oracle import Spec, a7_links, branch_example, full_corpus
+
+
+def test_splitmix64_frozen_vector(orc):
+    # test_imagekit.cpp:81-91
+    assert orc.splitmix64(1234567, 5) == [6457827717110365317, 3203168211198807973, 9817491932198370423,
+                                          4593380528125082431, 16408922859458223821]
+    assert orc.splitmix64(0, 1) == [16294208416658607535]
+
+
+def test_bit_layout_msb_first(orc):
+    # test_imagekit.cpp:49-53: x=0 is 0x80; frame 5x5 P4 payload (test_imagekit.cpp:198-209)
+    assert orc.synth(Spec.frame(5, 5))[:, 0].tolist() == [0xF8, 0x88, 0x88, 0x88, 0xF8]
+
+
+def test_counts_known_answers(orc):
+    # test_runscan.cpp:35-49
+    assert orc.counts(orc.synth(Spec.full(4, 4)), 4).tolist() == [1, 1, 1, 1]
+    assert orc.counts(orc.synth(Spec.frame(5, 5)), 5).tolist() == [1, 2, 2, 2, 1]
+    assert orc.counts(orc.synth(Spec.empty(3, 3)), 3).tolist() == [0, 0, 0]
+    assert orc.counts(branch_example(), 2).tolist() == [2, 2]
+    assert orc.counts(np.zeros((0, 0), np.uint8), 0).tolist() == []
+    assert orc.counts(orc.synth(Spec.hbands(8, 11, 3)), 8).tolist() == [3] * 8
+
+
+def test_boundaries_known_answers(orc):
+    # test_runscan.cpp:129-143
+    cases = [([1, 2, 2, 2, 1], [0, 1, 4]), ([0, 0, 0], []), ([], []), ([0, 1], [1]), ([3], [0]), ([2, 2], [0])]
+    for counts, want in cases:
+        assert orc.boundaries(np.array(counts, np.int32)).tolist() == want
+
+
+def test_hyperedge_known_answers(orc):
+    # acceptance.cpp:101-121, test_hypergraph.cpp:75-88, test_bench.cpp:139-160, test_cli.cpp:176-193
+    assert orc.hyperedges(branch_example(), 2)[0] == 4
+    assert orc.hyperedges(orc.synth(Spec.frame(5, 5)), 5)[0] == 4
+    for k in (1, 3, 7):
+        assert orc.hyperedges(orc.synth(Spec.hbands(20, 20, k)), 20)[0] == k
+    assert orc.hyperedges(orc.synth(Spec.checker(8, 8, 1)), 8)[0] == 32
+    assert orc.hyperedges(orc.synth(Spec.empty(3, 3)), 3)[0] == 0
+    assert orc.hyperedges(np.zeros((0, 0), np.uint8), 0)[0] == 0
+    for k, want in ((1, 1), (2, 2), (4, 4)):
+        assert orc.hyperedges(orc.synth(Spec.hbands(64, 64, k)), 64)[0] == want
+    assert orc.hyperedges(orc.synth(Spec.checker(64, 64, 1)), 64)[0] == 2048
+    assert orc.hyperedges(orc.synth(Spec.checker(16, 16, 1)), 16)[0] == 128
+
+
+def test_oracle_matches_reference_golden_corpus(orc):
+    rows = corpus()
+    assert len(rows) == 1170
+    for row in rows:
+        sp = spec_of(row["spec"])
+        bits = orc.synth(sp)
+        c = orc.counts(bits, sp.width)
+        assert c.tolist() == row["counts"], row["name"]
+        assert orc.boundaries(c).tolist() == row["boundaries"], row["name"]
+        assert orc.hyperedges(bits, sp.width)[0] == row["hyperedges"], row["name"]
+
+
+def test_corpus_generator_matches_golden():
+    names = [n for n, _ in full_corpus()]
+    assert names == [r["name"] for r in corpus()]
+
+
+def test_oracle_matches_reference_acceptance2(orc):
+    for row in acceptance2()[:40]:
+        sp = spec_of(row["spec"])
+        bits = orc.synth(sp)
+        c = orc.counts(bits, sp.width)
+        assert hashlib.sha256(c.astype("<i4").tobytes()).hexdigest() == row["counts_sha256"]
+        assert orc.boundaries(c).size == row["n_boundaries"]
+        assert orc.hyperedges(bits, sp.width)[0] == row["hyperedges"]
+
+
+@pytest.mark.parametrize("idx", [1, 5, 7, 9])
+def test_oracle_matches_reference_large(orc, idx):
+    row = large()[idx]
+    sp = spec_of(row["spec"])
+    bits = orc.synth(sp)
+    c = orc.counts(bits, sp.width)
+    assert hashlib.sha256(c.astype("<i4").tobytes()).hexdigest() == row["counts_sha256"]
+    assert orc.hyperedges(bits, sp.width)[0] == row["hyperedges"]
+
+
+def test_a7_streaming_rule_equals_decompose(orc):
+    # runs - links(strip components with exactly two runs) == decompose count
+    for name, sp in full_corpus()[::7]:
+        bits = orc.synth(sp)
+        he, runs, links = orc.hyperedges(bits, sp.width)
+        assert a7_links(bits, sp.width) == links, name
+
+
+def test_oracle_against_live_reference(orc, ref):
+    # When oracle/_ref is present: random geometries straddling byte/word edges.
+    rng = np.random.default_rng(5)
+    for _ in range(60):
+        w, h = int(rng.integers(1, 200)), int(rng.integers(1, 120))
+        sp = Spec.random(w, h, float(rng.choice([0.1, 0.5, 0.9])), int(rng.integers(0, 1 << 62)))
+        bits = ref.synth(sp)
+        assert np.array_equal(bits, orc.synth(sp))
+        img = ref.image(bits, w)
+        c = img.counts(1, 4)
+        assert np.array_equal(c, orc.counts(bits, w))
+        assert img.hyperedges() == orc.hyperedges(bits, w)[0]
