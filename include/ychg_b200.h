@@ -135,6 +135,14 @@ YCHG_API int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pi
 YCHG_API int ychg_plan_set_timing(ychg_plan* plan, int32_t enabled);
 YCHG_API int ychg_plan_last_ms(ychg_plan* plan, float* scan_ms, float* finish_ms);
 
+/* Diagnostics: per-CTA %globaltimer stamps of the streaming kernel (32 slots
+ * per CTA: 0 entry, 1+w warp w (< 16) done streaming, 20 segment merged,
+ * 21 strip ticket taken, 22 strip finished, 23 exit, 24 finisher loads done,
+ * 25 finisher look-back done).  enable=1 allocates, 0 frees; host_out (may be
+ * NULL) receives min(capacity, grid*32) stamps of the last scan. */
+YCHG_API int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, int32_t capacity,
+                                    int32_t* n_ctas);
+
 /* ---- helpers ---- */
 /* Bit-exact with reference synth() for every pattern (synth.cpp:38-104);
  * writes height rows of `pitch` bytes, padding bytes and bits zeroed. */

@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libychg_b200.so")
+# YCHG_LIB selects an experimental launch-shape build (see _build.build_variant).
+LIB_PATH = os.environ.get("YCHG_LIB") or os.path.join(_PKG, "libychg_b200.so")
 CXX_LIB_PATH = os.path.join(_PKG, "libychg.so")
 
 if not os.path.exists(LIB_PATH):
@@ -63,6 +64,7 @@ _SIGS = {
     "ychg_scan_device": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "ychg_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
     "ychg_plan_last_ms": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
+    "ychg_plan_debug_stamps": (ctypes.c_int, [_vp, _i32, _vp, _i32, ctypes.POINTER(_i32)]),
     "ychg_synth_device": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64, _vp, _i64, _vp]),
     "ychg_device_alloc": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.POINTER(_vp)]),
     "ychg_device_free": (ctypes.c_int, [ctypes.c_int, _vp]),
@@ -231,9 +233,9 @@ class Plan:
         self._h = h
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.ychg_plan_destroy(self._h)
-            self._h = None
+        self._h = None
 
     __del__ = close
 
@@ -249,6 +251,17 @@ class Plan:
         a, b = ctypes.c_float(0), ctypes.c_float(0)
         _check(_lib.ychg_plan_last_ms(self._h, ctypes.byref(a), ctypes.byref(b)), "plan_last_ms")
         return a.value, b.value
+
+    def debug_stamps(self, enable: bool = True):
+        """Per-CTA %globaltimer stamps (ns) of the last scan, shape (grid, 32); see ychg_b200.h."""
+        n = _i32(0)
+        _check(_lib.ychg_plan_debug_stamps(self._h, int(enable), None, 0, ctypes.byref(n)), "debug_stamps")
+        if not enable:
+            return None
+        out = np.zeros((max(n.value, 1), 32), dtype=np.uint64)
+        _check(_lib.ychg_plan_debug_stamps(self._h, 1, out.ctypes.data_as(_vp), out.size, ctypes.byref(n)),
+               "debug_stamps")
+        return out[: n.value]
 
     def scan_device(self, d_bits: int, pitch: int, d_counts: int, d_flags: int, d_boundaries: int,
                     d_totals: int, stream: int = 0, with_hyperedges: bool = True) -> None:
@@ -280,9 +293,9 @@ class DeviceBuffer:
         self.ptr = p.value
 
     def close(self) -> None:
-        if getattr(self, "ptr", None):
+        if getattr(self, "ptr", None) and _lib is not None:
             _lib.ychg_device_free(self.device, self.ptr)
-            self.ptr = None
+        self.ptr = None
 
     __del__ = close
 

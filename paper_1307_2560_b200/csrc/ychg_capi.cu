@@ -85,8 +85,9 @@ struct ychg_plan {
     alignas(64) CUtensorMap map{};
     // timing
     bool timing = false;
-    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_recorded = false;
+    unsigned long long* dbg = nullptr;  // per-CTA %globaltimer stamps of the last scan
 };
 
 namespace {
@@ -100,7 +101,8 @@ int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out) {
     if (kmin < 1) kmin = 1;
     double best = 1e300;
     int best_k = kmin;
-    for (int k = kmin; k <= std::max(kmin, n_blocks); ++k) {
+    const int kmax = std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip));
+    for (int k = kmin; k <= kmax; ++k) {
         const long long segs = static_cast<long long>(n_strips) * k;
         const long long G = std::min<long long>(sms, segs);
         const long long waves = (segs + G - 1) / G;
@@ -162,18 +164,45 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
     if (p.n_strips > 0 && p.n_blocks > 0) {
         p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid);
         p.n_segments = p.n_strips * p.seg_per_strip;
-        const int64_t part = int64_t(p.n_segments) * ychg_dev::kStripCols * 4;
-        const int64_t sums = int64_t(p.n_segments) * ychg_dev::kSumPlanes * 32 * 4;
-        const int64_t links = int64_t(p.n_segments) * 8;
-        const int64_t snb = int64_t(p.n_strips) * 4;
-        plan->ws_bytes = part + sums + links + snb + 256;
+        if (p.seg_per_strip > ychg_dev::kMaxSegPerStrip)
+            return fail(YCHG_ERR_INVALID, "plan_create: height %d needs more than %d row segments per strip",
+                        height, ychg_dev::kMaxSegPerStrip);
+        // Cooperative launch: every CTA must be co-resident (cross-CTA waits).
+        int per_sm = 0;
+        if (const int rc2 = ychg_scan_kernel_prepare())
+            return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ychg_scan_kernel_ptr(1), ychg_dev::kThreads,
+                                                          ychg_dev::kSmemTotal));
+        if (per_sm < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
+        plan->grid = std::min(plan->grid, per_sm * sms);
+        const int64_t S = p.n_strips, G = p.n_segments;
+        const int64_t sz_part = G * 512 * 4, sz_sums = G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = G * 8;
+        if (height >= (1 << 22))
+            return fail(YCHG_ERR_INVALID, "plan_create: height %d >= 2^22 rows is not supported", height);
+        const int64_t sz_ticket = S * 8, sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
+        // order: part | sums | seg_links | strip_ticket | rec
+        plan->ws_bytes = sz_part + sz_sums + sz_seg + sz_ticket + sz_rec + 64;
         cudaError_t e = cudaMalloc(&plan->ws, plan->ws_bytes);
-        if (e != cudaSuccess) return cuda_fail(e, "plan workspace cudaMalloc");
+        if (e != cudaSuccess) {
+            plan->ws = nullptr;
+            return cuda_fail(e, "plan workspace cudaMalloc");
+        }
+        e = cudaMemset(plan->ws, 0, plan->ws_bytes);
+        if (e != cudaSuccess) {
+            cudaFree(plan->ws);
+            plan->ws = nullptr;
+            return cuda_fail(e, "plan workspace cudaMemset");
+        }
         char* w = static_cast<char*>(plan->ws);
         p.part = reinterpret_cast<uint32_t*>(w);
-        p.sums = reinterpret_cast<uint32_t*>(w + part);
-        p.seg_links = reinterpret_cast<unsigned long long*>(w + part + sums);
-        p.strip_nb = reinterpret_cast<int32_t*>(w + part + sums + links);
+        w += sz_part;
+        p.sums = reinterpret_cast<uint32_t*>(w);
+        w += sz_sums;
+        p.seg_links = reinterpret_cast<unsigned long long*>(w);
+        w += sz_seg;
+        p.strip_ticket = reinterpret_cast<unsigned long long*>(w);
+        w += sz_ticket;
+        p.rec = reinterpret_cast<ychg_dev::StripRecord*>(w);
     }
     *out = plan.release();
     return YCHG_OK;
@@ -185,6 +214,7 @@ void ychg_plan_destroy(ychg_plan* plan) {
     cudaGetDevice(&prev);
     cudaSetDevice(plan->device);
     if (plan->ws) cudaFree(plan->ws);
+    if (plan->dbg) cudaFree(plan->dbg);
     for (auto& e : plan->ev)
         if (e) cudaEventDestroy(e);
     cudaSetDevice(prev);
@@ -198,7 +228,7 @@ int ychg_plan_get_info(const ychg_plan* plan, ychg_plan_info* out) {
     out->seg_per_strip = plan->prm.seg_per_strip;
     out->n_segments = plan->prm.n_segments;
     out->grid = plan->grid;
-    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 3 : 0;
+    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 1 : 0;
     out->workspace_bytes = plan->ws_bytes;
     return YCHG_OK;
 }
@@ -215,12 +245,32 @@ int ychg_plan_set_timing(ychg_plan* plan, int32_t enabled) {
 
 int ychg_plan_last_ms(ychg_plan* plan, float* scan_ms, float* finish_ms) {
     if (!plan || !plan->ev_recorded) return fail(YCHG_ERR_INVALID, "plan_last_ms: no timed scan recorded");
-    CK(cudaEventSynchronize(plan->ev[2]));
-    float a = 0, b = 0;
+    CK(cudaEventSynchronize(plan->ev[1]));
+    float a = 0;
     CK(cudaEventElapsedTime(&a, plan->ev[0], plan->ev[1]));
-    CK(cudaEventElapsedTime(&b, plan->ev[1], plan->ev[2]));
     if (scan_ms) *scan_ms = a;
-    if (finish_ms) *finish_ms = b;
+    if (finish_ms) *finish_ms = 0.0f;  // the finish is fused into the streaming kernel
+    return YCHG_OK;
+}
+
+int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, int32_t capacity,
+                           int32_t* n_ctas) {
+    if (!plan) return fail(YCHG_ERR_INVALID, "plan_debug_stamps: NULL plan");
+    CK(cudaSetDevice(plan->device));
+    if (enable && !plan->dbg && plan->grid > 0) {
+        CK(cudaMalloc(&plan->dbg, int64_t(plan->grid) * 32 * 8));
+        CK(cudaMemset(plan->dbg, 0, int64_t(plan->grid) * 32 * 8));
+    }
+    if (!enable && plan->dbg) {
+        CK(cudaFree(plan->dbg));
+        plan->dbg = nullptr;
+    }
+    if (n_ctas) *n_ctas = plan->grid;
+    if (host_out && plan->dbg) {
+        const int64_t n = std::min<int64_t>(capacity, int64_t(plan->grid) * 32);
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(host_out, plan->dbg, n * 8, cudaMemcpyDeviceToHost));
+    }
     return YCHG_OK;
 }
 
@@ -273,13 +323,15 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     p.flags = d_flags;
     p.boundaries = d_boundaries;
     p.totals = reinterpret_cast<long long*>(d_totals);
+    p.dbg = plan->dbg;
+    p.mul2 = 2u;
+    p.mul17 = 1u << 17;
 
     if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
-    const int rc = ychg_launch_scan(&plan->map, &p, plan->grid, with_hyperedges ? 1 : 0, st,
-                                    plan->timing ? plan->ev[1] : nullptr);
-    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "scan kernels launch");
+    const int rc = ychg_launch_scan(&plan->map, &p, plan->grid, with_hyperedges ? 1 : 0, st, nullptr);
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "scan kernel launch");
     if (plan->timing) {
-        CK(cudaEventRecord(plan->ev[2], st));
+        CK(cudaEventRecord(plan->ev[1], st));
         plan->ev_recorded = true;
     }
     return YCHG_OK;

@@ -1,10 +1,10 @@
 // ychg_device.cuh -- sm_100a device building blocks for the yCHG column scan.
 //
 // Bit layout (reference image.hpp:10-22,35-36): row-major, MSB-first bytes, rows
-// of ceil(W/8) bytes.  On the device every 32-column word is byte-swapped once
-// after loading (one PRMT) so that column 32w+j sits at bit 31-j: the right
-// neighbour of every column is then "shift left by one", with the first column
-// of the next word funnelled in.
+// of ceil(W/8) bytes.  Words are used in raw little-endian load order (column
+// 8L+7-p at bit 8L+p): every step is bitwise, so only the right-neighbour word b
+// needs the layout -- inside a byte the neighbour is one bit lower (raw << 1),
+// across bytes it is bit 7 of the next byte (raw >> 15, next word's byte 0).
 //
 // All per-pixel work is bit-sliced: one 32-bit register carries one bit of 32
 // columns (K1) or of 32 adjacent column pairs (K3).
@@ -14,30 +14,51 @@
 
 namespace ychg_dev {
 
-constexpr int kWarps = 8;                        // warps per CTA
+#ifndef YCHG_WARPS
+#define YCHG_WARPS 8
+#endif
+#ifndef YCHG_STAGES
+#define YCHG_STAGES 4
+#endif
+constexpr int kWarps = YCHG_WARPS;               // warps per CTA
 constexpr int kThreads = kWarps * 32;
 constexpr int kStripWords = 32;                  // one warp lane per 32-column word
 constexpr int kStripCols = kStripWords * 32;     // 1024 columns per strip
 constexpr int kStripBytes = kStripWords * 4;     // 128 B of every row
 constexpr int kBoxBytes = kStripBytes + 16;      // + 16 B right halo (next strip's first word)
 constexpr int kBlockRows = 32;                   // rows per TMA stage / per Harley-Seal block
-constexpr int kStages = 4;                       // TMA ring depth per warp
+constexpr int kStages = YCHG_STAGES;             // TMA ring depth per warp
 constexpr int kStageBytes = kBoxBytes * kBlockRows;   // 4608 B
 constexpr int kFlushBlocks = 15;                 // 8-bit bit-sliced counters: <= 15*16+15 = 255
 constexpr int kSumPlanes = 7;                    // K3 band summary planes (see BandSummary)
 constexpr int kMaxSegmentRows = 65504;           // u16 SWAR accumulators: counts <= rows/2 < 2^15
 
+constexpr int kMaxSegPerStrip = 128;            // the finisher keeps k summaries in smem
+
 // Shared-memory layout of the scan kernel (bytes).
 constexpr int kSmemStages = kWarps * kStages * kStageBytes;            // 147456
-constexpr int kSmemHalo = kWarps * 2 * 32 * 4;                         // halo-row words
 constexpr int kSmemBar = kWarps * kStages * 8;                         // mbarriers
 constexpr int kSmemAcc = kWarps * 16 * 32 * 4;                         // per-warp u16x2 counts
 constexpr int kSmemSum = kWarps * kSumPlanes * 32 * 4;                 // per-warp K3 summaries
-constexpr int kSmemMisc = kWarps * 16;                                 // links + flags
-constexpr int kSmemTotal = kSmemStages + kSmemHalo + kSmemBar + kSmemAcc + kSmemSum + kSmemMisc;
+constexpr int kSmemMisc = kWarps * 16 + 16;                            // links + flags
+constexpr int kSmemTotal = kSmemStages + kSmemBar + kSmemAcc + kSmemSum + kSmemMisc;
+
+// What a strip's finisher publishes for the strips to its right: `status`
+// packs the epoch, the number of change flags strictly inside the strip and the
+// counts of its first and last column (counts < 2^21, i.e. height < 2^22);
+// `tstat` releases the strip's run and link totals.
+struct StripRecord {
+    unsigned long long status;  // epoch:12 | inside:10 | first:21 | last:21 (release-published)
+    unsigned long long tstat;   // epoch, release-published after runs/links
+    long long runs;             // sum of the strip's counts
+    long long links;            // K3 links of the strip's column pairs
+};
 
 // ----------------------------------------------------------------------------
-// Launch parameters shared by the three kernels of one scan.
+// Launch parameters of one scan.  Cross-CTA bookkeeping (tickets, strip
+// records) is epoch-tagged -- the epoch is derived on the device from the
+// monotonic strip tickets -- so it never needs resetting between scans and the
+// launch is CUDA-graph replayable.
 struct ScanParams {
     const uint8_t* bits;      // device image base (row-major packed bits)
     int64_t pitch;            // bytes between rows (multiple of 16 for TMA)
@@ -49,14 +70,17 @@ struct ScanParams {
     int32_t n_blocks;         // ceil(height / 32)
     int32_t seg_per_strip;    // k: row segments per strip
     int32_t n_segments;       // n_strips * k
-    uint32_t* part;           // [n_segments][1024] per-segment column counts
+    uint32_t mul2, mul17;     // 2 and 1 << 17 as runtime values: keeps the b-word shifts on IMAD
+    uint32_t* part;           // [n_segments][512] per-segment u16x2 column counts
     uint32_t* sums;           // [n_segments][7][32] K3 band summaries
-    unsigned long long* seg_links;  // [n_segments] links closed inside each segment
+    unsigned long long* seg_links;    // [n_segments] links closed inside each segment
+    unsigned long long* strip_ticket; // [n_strips] segments finished (monotonic)
+    struct StripRecord* rec;  // [n_strips] published by each strip's finisher
     long long* totals;        // ychg_totals {total_runs, links, hyperedges, n_boundaries}
     int32_t* counts;          // [width_cnt] final per-column counts
     uint32_t* flags;          // [ceil(width_cnt/32)] change flags, bit j = column 32w+j
     int32_t* boundaries;      // [<= width_cnt] ascending boundary columns
-    int32_t* strip_nb;        // [n_strips] boundary columns per strip
+    unsigned long long* dbg;  // optional [grid][16] %globaltimer stamps (diagnostics), or null
 };
 
 // Segment j of a strip covers row blocks [seg_first(j), seg_first(j+1)).
@@ -101,11 +125,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
 // ----------------------------------------------------------------------------
 // Bit-sliced arithmetic.
 //
+// lop3<LUT>(a, b, c): one LOP3.LUT with truth table LUT over (a=0xF0, b=0xCC,
+// c=0xAA).  Written explicitly so every boolean step of the hot loop is exactly
+// one ALU instruction (ptxas does not always find the 3-input merges itself).
+template <uint32_t kLut>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(kLut));
+    return d;
+}
+//
 // Carry-save adder: l = a ^ b ^ c, h = majority(a, b, c); two LOP3 each.
 __device__ __forceinline__ void csa(uint32_t& h, uint32_t& l, uint32_t a, uint32_t b, uint32_t c) {
-    const uint32_t u = a ^ b;
-    h = (a & b) | (u & c);
-    l = u ^ c;
+    h = lop3<0xE8>(a, b, c);  // majority
+    l = lop3<0x96>(a, b, c);  // a ^ b ^ c
 }
 
 // 8 bit-planes (x[k] = bit k of 32 per-column counters) -> per-column bytes:
@@ -135,11 +168,13 @@ __device__ __forceinline__ void transpose8x8_bytes(uint32_t (&x)[8]) {
 
 // Column (0..31, left to right inside its word) held by u16 lane `half` of
 // accumulator acc[i] (i = 2p + kind) after flush_counts: see flush_counts.
+// Words are processed in their raw little-endian load order: bit 8L+p of a word
+// is bit p of byte L, i.e. column 8L + 7 - p of the word (MSB-first bytes).
 __host__ __device__ inline int acc_column(int i, int half) {
     const int p = i >> 1, kind = i & 1;
     // kind 0 keeps byte lanes {0,2}, kind 1 keeps {1,3}; half selects the upper lane.
     const int L = kind + 2 * half;
-    return 31 - (8 * L + p);
+    return 8 * L + 7 - p;
 }
 
 // ----------------------------------------------------------------------------

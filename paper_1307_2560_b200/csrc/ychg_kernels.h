@@ -9,10 +9,15 @@ struct ScanParams;
 }
 
 extern "C" {
-// Enqueue scan + finish + compact on `stream`; records ev_mid (if non-null)
-// between the streaming kernel and the finish kernels.  Returns cudaError_t.
+// Enqueue the fused scan kernel (cooperative launch) on `stream`.  Returns cudaError_t.
 int ychg_launch_scan(const void* tmap, const ychg_dev::ScanParams* prm, int grid, int with_links,
                      cudaStream_t stream, cudaEvent_t ev_mid);
+
+// Set the kernels' dynamic shared-memory opt-in on the current device.
+int ychg_scan_kernel_prepare(void);
+
+// The streaming kernel entry (for occupancy queries).
+const void* ychg_scan_kernel_ptr(int with_links);
 
 int ychg_launch_synth(int pattern, int width, int height, int bands, int cell, double density,
                       uint64_t seed, uint8_t* d_bits, int64_t pitch, cudaStream_t stream);

@@ -1,20 +1,26 @@
-// ychg_scan.cu -- the yCHG hot path on sm_100a.
+// ychg_scan.cu -- the yCHG hot path on sm_100a: ONE persistent, cooperative
+// kernel per scan.
 //
 //   K1  per-column cut-vertex counts      (reference runscan.cpp:41-74,122-128)
 //   K2  change flags + ascending boundary  (runscan.cpp:145-153)
 //   K3  hyperedge total = runs - links     (hypergraph.cpp:94-170,192)
 //
-// Three launches per scan, stream-ordered:
-//   ychg_scan_kernel    streams the packed mask once (TMA, per-warp 4-stage ring),
-//                       bit-sliced K1 + K3 per 32-row block, one partial per
-//                       (strip, row-segment)  -- the HBM-bound kernel.
-//   ychg_finish_kernel  one CTA per 1024-column strip: sums the segment partials,
-//                       writes counts, change-flag words, per-strip boundary
-//                       count; stitches the K3 band summaries top to bottom.
-//   ychg_compact_kernel one CTA per strip: ordered boundary compaction
-//                       (ballot/popc), final totals.
+// Work split: the mask is cut into 1024-column strips (one 32-bit word per
+// lane) and every strip into k row segments; CTA g owns segments g, g+G, ...
+// A segment is split into 8 consecutive warp bands.  Each warp streams its band
+// through its own 4-stage TMA ring (cp.async.bulk.tensor, 32 rows x 144 B per
+// stage: 128 B of the strip + a 16 B right halo) and runs K1 + K3 bit-sliced
+// in registers; the CTA then merges its 8 warps in shared memory and writes one
+// partial per segment (coalesced).  The LAST CTA to finish a strip (ticket
+// counter) finishes it: sums the k partials, writes the counts, stitches the K3
+// summaries top to bottom, computes the change flags (waiting on the left
+// neighbour strip's last count) and compacts the boundary list with a
+// decoupled look-back over strips.  The last strip finisher writes the totals.
+// Cross-CTA waits are safe because the launch is cooperative (all CTAs resident).
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "ychg_device.cuh"
 #include "ychg_kernels.h"
@@ -28,11 +34,11 @@ struct LaneState {
     uint32_t ones, twos, fours, eights, u16, u32, u64, u128;
     uint32_t acc[16];          // u16x2 per-column totals (see acc_column)
     uint32_t pa, pb;           // previous row: column c and column c+1 bits
-    uint32_t mk1, mk3;         // valid counted columns / valid pairs of this word
+    uint32_t mk3;              // valid column pairs of this word
     // K3
     uint32_t G2, G3;           // open component holds >= 2 / >= 3 runs
-    uint32_t Hd, h1, h2, E;    // head tracking (see BandSummary)
-    uint32_t links;            // links closed inside this lane's band (<= rows/2 * 32)
+    uint32_t Hd, h1, h2;       // head still open / head gained >= 1 / >= 2 runs
+    uint32_t links;            // links closed inside this lane's band
 };
 
 __device__ __forceinline__ void flush_counts(LaneState& s) {
@@ -46,60 +52,71 @@ __device__ __forceinline__ void flush_counts(LaneState& s) {
     s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
 }
 
-// One row: returns the rises (background->foreground, runscan.cpp:57) of the
-// lane's 32 columns and, when kLinks, advances the pair state machine and
-// returns the pairs whose component closed at this row as a link.
-template <bool kLinks, bool kHead>
-__device__ __forceinline__ uint32_t row_step(uint32_t raw, uint32_t nbyte, LaneState& s,
-                                             uint32_t& link) {
-    const uint32_t a = __byte_perm(raw, 0u, 0x0123u);   // column j at bit 31-j
-    const uint32_t na = a & ~s.pa & s.mk1;
-    if (kLinks) {
-        const uint32_t b = (a << 1) | (nbyte >> 7);      // column c+1 at column c's bit
-        const uint32_t ab = a & b & s.mk3;
-        const uint32_t f = ab & (s.pa ^ s.pb);           // a new run joins an open component
-        const uint32_t cont = (a & s.pa) | (b & s.pb);   // the component continues into this row
-        uint32_t lk = ~cont & s.G2 & ~s.G3;              // it closed holding exactly two runs
-        if (kHead) {
-            lk &= ~s.Hd;
-            const uint32_t hf = s.Hd & f;
-            s.h2 |= s.h1 & hf;
-            s.h1 |= hf;
-            s.E |= s.Hd & ~cont;
-            s.Hd &= cont;
-        }
-        const uint32_t g3 = (cont & s.G3) | (s.G2 & f);
-        s.G2 = ab | (cont & s.G2);
-        s.G3 = g3;
-        s.pb = b;
-        link = lk;
+// K3 pair step for one row (a = columns c, b = columns c+1 of this word).
+// Components of the 2-column strip are row intervals; one continues into this
+// row iff (a & pa) | (b & pb).  A new run can only join an open component on a
+// row where both columns are set and exactly one of them was set above:
+// f = a & b & (pa ^ pb).  N >= 2 <=> ab | (cont & G2); N >= 3 <=> (cont & G3) | (G2 & f).
+// A component that closes with exactly two runs is a decompose() link
+// (hypergraph.cpp:137-143).  Head pairs (open across the band's top edge) start
+// "poisoned" at N >= 3 so their unknown-prefix component never counts here;
+// kHead additionally tracks their new runs (h1, h2) until they close.
+template <bool kHead>
+__device__ __forceinline__ uint32_t k3_step(uint32_t a, uint32_t b, LaneState& s) {
+    const uint32_t ab = a & b;
+    const uint32_t f = lop3<0x60>(ab, s.pa, s.pb);            // ab & (pa ^ pb)
+    const uint32_t cont = lop3<0xF8>(a & s.pa, b, s.pb);       // (a & pa) | (b & pb)
+    const uint32_t lk = lop3<0x04>(cont, s.G2, s.G3);          // ~cont & G2 & ~G3
+    if (kHead) {
+        s.Hd &= cont;
+        const uint32_t t = s.Hd & f;
+        s.h2 = lop3<0xF8>(s.h2, s.h1, t);                      // h2 | (h1 & t)
+        s.h1 |= t;
     }
+    const uint32_t g3 = lop3<0xEA>(cont, s.G3, s.G2 & f);     // (cont & G3) | (G2 & f)
+    s.G2 = lop3<0xF8>(ab, cont, s.G2);                         // ab | (cont & G2)
+    s.G3 = g3;
     s.pa = a;
-    return na;
+    s.pb = b;
+    return lk;
 }
 
 // 32 rows from one TMA stage: 16 row pairs -> Harley-Seal tree -> ripple planes.
-// Rises of one column never occur in two consecutive rows, so a pair of rows
-// contributes rises0 | rises1 exactly.  Links of one pair are likewise never in
-// consecutive rows, so they are popcounted per row pair.
+// Rises of one column are never in consecutive rows, so a row pair contributes
+// (a0 & ~pa) | (a1 & ~a0) -- one LOP3.  Links of one pair are likewise never in
+// consecutive rows and are popcounted per row pair.
+// Right neighbour (column c+1 at column c's bit) of a raw little-endian word:
+// inside a byte it is one bit lower (raw << 1); bit 0 of byte L takes bit 7 of
+// byte L+1 (raw >> 15), byte 3 takes bit 7 of the next word's byte 0 (nb << 17).
+// The shifts run as IMAD / IMAD.HI on the FMA pipe (runtime multipliers keep
+// ptxas from turning them into ALU shifts); one LOP3 merges them.
+__device__ __forceinline__ uint32_t right_neighbour(uint32_t raw, uint32_t nb, uint32_t mul2, uint32_t mul17) {
+    const uint32_t t1 = raw * mul2;
+    const uint32_t t3 = nb * mul17 + __umulhi(raw, mul17);
+    return lop3<0xE2>(t1, 0xFEFEFEFEu, t3);  // (t1 & M) | (t3 & ~M): bit select, one LOP3
+}
+
 template <bool kLinks, bool kHead>
 __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage, int lane,
-                                              LaneState& s) {
+                                              LaneState& s, uint32_t mul2, uint32_t mul17) {
     const uint8_t* p = stage + 4 * lane;
     uint32_t Pprev = 0, tA = 0, fA = 0, eA = 0;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         const uint8_t* r0 = p + (2 * q) * kBoxBytes;
         const uint8_t* r1 = r0 + kBoxBytes;
-        const uint32_t raw0 = *reinterpret_cast<const uint32_t*>(r0);
-        const uint32_t raw1 = *reinterpret_cast<const uint32_t*>(r1);
-        const uint32_t nb0 = kLinks ? static_cast<uint32_t>(r0[4]) : 0u;
-        const uint32_t nb1 = kLinks ? static_cast<uint32_t>(r1[4]) : 0u;
-        uint32_t l0 = 0, l1 = 0;
-        const uint32_t x0 = row_step<kLinks, kHead>(raw0, nb0, s, l0);
-        const uint32_t x1 = row_step<kLinks, kHead>(raw1, nb1, s, l1);
-        if (kLinks) s.links += __popc(l0 | l1);
-        const uint32_t P = x0 | x1;
+        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0);
+        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(r1);
+        const uint32_t P = lop3<0x3A>(a0, s.pa, a1);  // (a0 & ~pa) | (a1 & ~a0)
+        if (kLinks) {
+            const uint32_t b0 = right_neighbour(a0, r0[4], mul2, mul17);
+            const uint32_t b1 = right_neighbour(a1, r1[4], mul2, mul17);
+            const uint32_t l0 = k3_step<kHead>(a0, b0, s);
+            const uint32_t l1 = k3_step<kHead>(a1, b1, s);
+            s.links += __popc(lop3<0xA8>(l0, l1, s.mk3));  // (l0 | l1) & mk3
+        } else {
+            s.pa = a1;
+        }
         if ((q & 1) == 0) {
             Pprev = P;
             continue;
@@ -144,31 +161,289 @@ __device__ __forceinline__ uint32_t word_mask(int gw, int limit) {
     return ~(0xFFFFFFFFu >> n);
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+#define YCHG_STAMP(slot)                                                             \
+    do {                                                                             \
+        if (prm.dbg) prm.dbg[static_cast<int64_t>(blockIdx.x) * 32 + (slot)] = globaltimer(); \
+    } while (0)
+
+__device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Shared-memory scratch of the strip finisher (lives in the idle TMA stage area).
+struct FinishSmem {
+    int32_t sc[kStripCols];       // counts of the strip's columns
+    uint32_t fw[kStripWords];     // change-flag words of the strip (inside flags only)
+    int wpre[kStripWords];        // exclusive prefix of popc(fw)
+    long long red[kWarps];
+    long long base;
+    uint32_t edge;                // flag of the strip's first column
+};
+
+__device__ __forceinline__ unsigned long long pack_strip_status(uint32_t epoch, uint32_t inside, int32_t first,
+                                                                int32_t last) {
+    return (static_cast<unsigned long long>(epoch & 0xFFFu) << 52) |
+           (static_cast<unsigned long long>(inside & 0x3FFu) << 42) |
+           (static_cast<unsigned long long>(static_cast<uint32_t>(first) & 0x1FFFFFu) << 21) |
+           (static_cast<unsigned long long>(static_cast<uint32_t>(last) & 0x1FFFFFu));
+}
+
+// Warp-uniform wait until word p (per active lane) carries `epoch` in its top 12 bits.
+__device__ __forceinline__ unsigned long long warp_wait_epoch12(const unsigned long long* p, bool active,
+                                                               uint32_t epoch) {
+    unsigned long long v = 0;
+    bool ok = !active;
+    while (true) {
+        if (!ok) {
+            v = ld_acquire(p);
+            ok = static_cast<uint32_t>(v >> 52) == (epoch & 0xFFFu);
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+    }
+    return v;
+}
+
+// Finish strip s: counts, K3 stitch, flags, boundary compaction, totals.
+// This runs on the kernel's tail, so it is built around global round trips:
+// one batch of loads, one release of the strip record (flags strictly inside
+// the strip + counts of its first and last column), one warp-parallel acquire
+// of every record to the left -- from which the boundary offset AND this
+// strip's first-column flag (counts[c0] vs counts[c0-1], runscan.cpp:147)
+// follow -- then fire-and-forget writes.
+template <bool kLinks>
+__device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8_t* scratch) {
+    FinishSmem& fs = *reinterpret_cast<FinishSmem*>(scratch);
+    uint32_t* ssum = reinterpret_cast<uint32_t*>(scratch + ((sizeof(FinishSmem) + 127) / 128) * 128);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int k = prm.seg_per_strip;
+    const int g0 = s * k;
+    constexpr int kSumWords = kSumPlanes * 32;
+
+    // (1) one batch of loads per 8 segments: partial counts (512 u16x2 words per
+    //     segment over the CTA) and the K3 summaries (8 x 224 words).
+    constexpr int kR = (512 + kThreads - 1) / kThreads;
+    constexpr int kY = (8 * kSumWords + kThreads - 1) / kThreads;
+    uint32_t v[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) v[r] = 0;
+    for (int g = 0; g < k; g += 8) {
+        const int n = k - g < 8 ? k - g : 8;
+        uint32_t x[kR][8], y[kY];
+        const uint32_t* src = prm.part + static_cast<int64_t>(g0 + g) * 512;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            const int idx = tid + r * kThreads;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[r][u] = (u < n && idx < 512) ? __ldcg(src + u * 512 + idx) : 0u;
+        }
+        const uint32_t* ss = prm.sums + static_cast<int64_t>(g0 + g) * kSumWords;
+        if (kLinks) {
+#pragma unroll
+            for (int u = 0; u < kY; ++u) {
+                const int i = tid + u * kThreads;
+                y[u] = i < n * kSumWords ? __ldcg(ss + i) : 0u;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kR; ++r)
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[r] += x[r][u];
+        if (kLinks) {
+#pragma unroll
+            for (int u = 0; u < kY; ++u) {
+                const int i = tid + u * kThreads;
+                if (i < n * kSumWords) ssum[g * kSumWords + i] = y[u];
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+        const int idx = tid + r * kThreads;
+        if (idx < 512) {
+            const int i = idx >> 5, ln = idx & 31;
+            fs.sc[32 * ln + acc_column(i, 0)] = static_cast<int32_t>(v[r] & 0xFFFFu);
+            fs.sc[32 * ln + acc_column(i, 1)] = static_cast<int32_t>(v[r] >> 16);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) YCHG_STAMP(24);
+
+    // (2) flags strictly inside the strip (columns 1..1023), counts out, run total
+    const int nwords = (prm.width_cnt + 31) >> 5;
+    long long local_sum = 0;
+    for (int wi = warp; wi < kStripWords; wi += kWarps) {
+        const int col = wi * 32 + lane;
+        const int gc = s * kStripCols + col;
+        const bool valid = gc < prm.width_cnt;
+        const int32_t c = fs.sc[col];
+        const bool f = valid && col > 0 && c != fs.sc[col - 1];
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+        if (lane == 0) fs.fw[wi] = m;
+        if (valid) local_sum += c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local_sum += __shfl_xor_sync(0xFFFFFFFFu, local_sum, o);
+    if (lane == 0) fs.red[warp] = local_sum;
+    __syncthreads();
+
+    const bool last_strip = (s == prm.n_strips - 1);
+    StripRecord* rec = prm.rec + s;
+    if (warp == 0) {
+        // (3) publish this strip's record, then acquire every record to the left
+        const int c = __popc(fs.fw[lane]);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        fs.wpre[lane] = incl - c;
+        const int inside = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const int32_t first = fs.sc[0];
+        if (lane == 0) st_release(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
+        long long off = 0;
+        int32_t carry_last = 0;  // last(j-1) entering each chunk; last(-1) := 0
+        for (int jb = 0; jb < s; jb += 32) {
+            const int j = jb + lane;
+            const bool act = j < s;
+            const unsigned long long st = warp_wait_epoch12(&prm.rec[act ? j : 0].status, act, epoch);
+            const int32_t fj = static_cast<int32_t>((st >> 21) & 0x1FFFFFu);
+            const int32_t lj = static_cast<int32_t>(st & 0x1FFFFFu);
+            int32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, lj, 1);
+            if (lane == 0) prev_last = carry_last;
+            if (act) off += static_cast<long long>((st >> 42) & 0x3FFu) + (fj != prev_last ? 1 : 0);
+            carry_last = __shfl_sync(0xFFFFFFFFu, lj, (s - 1 - jb) < 31 ? (s - 1 - jb) : 31);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
+        if (lane == 0) {
+            fs.edge = (first != carry_last) ? 1u : 0u;
+            fs.base = off;
+            if (last_strip) prm.totals[3] = off + fs.edge + inside;
+        }
+    } else if (warp == 1) {
+        // (4) K3: stitch the strip's segment summaries top to bottom, close at row H,
+        //     then release (runs, links) for the totals.
+        unsigned long long links = 0;
+        if (kLinks) {
+            BandSummary C;
+            for (int g = 0; g < k; ++g) {
+                const uint32_t* gs = ssum + g * kSumWords;
+                BandSummary B{gs[lane], gs[32 + lane], gs[64 + lane], gs[96 + lane], gs[128 + lane],
+                              gs[160 + lane], gs[192 + lane]};
+                if (g == 0) {
+                    C = B;
+                } else {
+                    BandSummary D;
+                    links += __popc(compose_summary(C, B, D));
+                    C = D;
+                }
+            }
+            links += __popc(C.OE & C.T2 & ~C.T3);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
+        }
+        if (lane == 0) {
+            long long runs = 0;
+            for (int w = 0; w < kWarps; ++w) runs += fs.red[w];
+            unsigned long long sl = 0;  // links closed inside the strip's segments
+            if (kLinks)
+                for (int g = 0; g < k; ++g) sl += __ldcg(prm.seg_links + g0 + g);
+            rec->runs = runs;
+            rec->links = static_cast<long long>(links + sl);
+            st_release(&rec->tstat, static_cast<unsigned long long>(epoch));
+        }
+    } else {
+        // counts out (fire and forget)
+        for (int col = tid - 64; col < kStripCols; col += kThreads - 64) {
+            const int gc = s * kStripCols + col;
+            if (gc < prm.width_cnt) prm.counts[gc] = fs.sc[col];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) YCHG_STAMP(25);
+
+    // (5) flags out + ordered compaction (the first-column flag, if set, comes first)
+    const uint32_t e = fs.edge;
+    if (tid == 0 && e) prm.boundaries[fs.base] = s * kStripCols;
+    for (int wi = warp; wi < kStripWords; wi += kWarps) {
+        const int w = s * kStripWords + wi;
+        const uint32_t m = fs.fw[wi];
+        if (lane == 0 && w < nwords) prm.flags[w] = m | (wi == 0 ? e : 0u);
+        if ((m >> lane) & 1u)
+            prm.boundaries[fs.base + e + fs.wpre[wi] + __popc(m & ((1u << lane) - 1u))] = w * 32 + lane;
+    }
+
+    // (6) the right-most strip also writes run/link totals once every strip released them
+    if (last_strip && warp == 0) {
+        long long runs = 0, links = 0;
+        for (int jb = 0; jb < prm.n_strips; jb += 32) {
+            const int j = jb + lane;
+            const bool act = j < prm.n_strips;
+            unsigned long long v = 0;
+            bool ok = !act;
+            while (true) {
+                if (!ok) {
+                    v = ld_acquire(&prm.rec[j].tstat);
+                    ok = static_cast<uint32_t>(v) == epoch;
+                }
+                if (__all_sync(0xFFFFFFFFu, ok)) break;
+            }
+            if (act) {
+                runs += __ldcg(&prm.rec[j].runs);
+                links += __ldcg(&prm.rec[j].links);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            runs += __shfl_xor_sync(0xFFFFFFFFu, runs, o);
+            links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
+        }
+        if (lane == 0) {
+            prm.totals[0] = runs;
+            prm.totals[1] = kLinks ? links : 0;
+            prm.totals[2] = kLinks ? runs - links : -1;
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------
-// K1 + K3 streaming kernel.  Persistent: CTA g processes segments g, g+G, ...
-// Every segment (strip s, row blocks [b0, b1)) is split into 8 consecutive warp
-// bands; each warp streams its band through its own 4-stage TMA ring (no
-// CTA-wide barrier in the main loop), then the CTA merges the 8 warp results.
 template <bool kLinks>
 __global__ void __launch_bounds__(kThreads, 1)
 ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stages = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemStages + kSmemHalo);
-    uint32_t* accs = reinterpret_cast<uint32_t*>(smem + kSmemStages + kSmemHalo + kSmemBar);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemStages);
+    uint32_t* accs = reinterpret_cast<uint32_t*>(smem + kSmemStages + kSmemBar);
     uint32_t* sums = accs + kWarps * 16 * 32;
     unsigned long long* wlinks = reinterpret_cast<unsigned long long*>(sums + kWarps * kSumPlanes * 32);
-    int* wempty = reinterpret_cast<int*>(wlinks + kWarps);
+    int* misc = reinterpret_cast<int*>(wlinks + kWarps);  // [0..W) warp empty, [W] finisher, [W+1] epoch
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
 
     if (tid == 0) {
+        YCHG_STAMP(0);
         for (int i = 0; i < kWarps * kStages; ++i) mbar_init(&bars[i], 1);
-        if (blockIdx.x == 0) {
-            for (int i = 0; i < 4; ++i) prm.totals[i] = 0;
-        }
     }
     fence_proxy_async();
     __syncthreads();
@@ -194,11 +469,11 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) s.acc[i] = 0;
-        s.mk1 = word_mask(gw, prm.width_cnt);
-        s.mk3 = word_mask(gw, min(prm.width_cnt, prm.width_img - 1));
-        s.G2 = s.G3 = s.h1 = s.h2 = s.E = 0;
+        s.mk3 = __byte_perm(word_mask(gw, min(prm.width_cnt, prm.width_img - 1)), 0u, 0x0123u);
+        s.h1 = s.h2 = 0;
         s.links = 0;
         s.pa = s.pb = 0;
+        uint32_t O = 0;
 
         if (nb > 0) {
             // Kick off the ring first so the halo-row load overlaps it.
@@ -219,23 +494,24 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                 const int c = x0 + 4 * lane;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (c + q < prm.row_bytes) raw |= static_cast<uint32_t>(row[c + q]) << (8 * q);
-                if (c + 4 < prm.row_bytes) nbyte = row[c + 4];
+                    if (c + q < prm.row_bytes) raw |= static_cast<uint32_t>(__ldg(row + c + q)) << (8 * q);
+                if (c + 4 < prm.row_bytes) nbyte = __ldg(row + c + 4);
             }
-            s.pa = __byte_perm(raw, 0u, 0x0123u);
-            s.pb = (s.pa << 1) | (nbyte >> 7);
-            s.Hd = kLinks ? ((s.pa | s.pb) & s.mk3) : 0u;
-            const uint32_t O = s.Hd;
+            s.pa = raw;
+            s.pb = right_neighbour(raw, nbyte, prm.mul2, prm.mul17);
+            O = kLinks ? (s.pa | s.pb) : 0u;
+            s.Hd = O;
+            s.G2 = s.G3 = O;  // poisoned: the head's own closing is never a local link
 
             int since_flush = 0;
             for (int bi = 0; bi < nb; ++bi) {
                 const int st = it % kStages;
                 mbar_wait(&my_bars[st], (it / kStages) & 1u);
                 const uint8_t* sp = my_stages + st * kStageBytes;
-                if (kLinks && __any_sync(0xFFFFFFFFu, s.Hd != 0u))
-                    process_block<kLinks, true>(sp, lane, s);
+                if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u))
+                    process_block<kLinks, true>(sp, lane, s, prm.mul2, prm.mul17);
                 else
-                    process_block<kLinks, false>(sp, lane, s);
+                    process_block<kLinks, false>(sp, lane, s, prm.mul2, prm.mul17);
                 __syncwarp();
                 if (lane == 0 && bi + kStages < nb) {
                     fence_proxy_async();
@@ -252,14 +528,15 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             flush_counts(s);
 
             if (kLinks) {
+                const uint32_t m = s.mk3;
                 uint32_t* ws = sums + warp * kSumPlanes * 32;
-                ws[0 * 32 + lane] = O;
-                ws[1 * 32 + lane] = s.E;
-                ws[2 * 32 + lane] = s.h1;
-                ws[3 * 32 + lane] = s.h2;
-                ws[4 * 32 + lane] = (s.pa | s.pb) & s.mk3;
-                ws[5 * 32 + lane] = s.G2;
-                ws[6 * 32 + lane] = s.G3;
+                ws[0 * 32 + lane] = O & m;
+                ws[1 * 32 + lane] = O & ~s.Hd & m;
+                ws[2 * 32 + lane] = s.h1 & m;
+                ws[3 * 32 + lane] = s.h2 & m;
+                ws[4 * 32 + lane] = (s.pa | s.pb) & m;
+                ws[5 * 32 + lane] = s.G2 & m;
+                ws[6 * 32 + lane] = s.G3 & m;
                 unsigned long long l = s.links;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xFFFFFFFFu, l, o);
@@ -269,25 +546,25 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         uint32_t* wa = accs + warp * 16 * 32;
 #pragma unroll
         for (int i = 0; i < 16; ++i) wa[i * 32 + lane] = s.acc[i];
-        if (lane == 0) wempty[warp] = (nb == 0);
+        if (lane == 0) {
+            misc[warp] = (nb == 0);
+            if (warp < 16) YCHG_STAMP(1 + warp);
+        }
         __syncthreads();
 
-        // ---- CTA merge: counts (sum over warps), K3 summaries (compose in row order).
+        // ---- CTA merge: counts (sum over warps, coalesced u16x2 words), K3 (compose in row order).
         for (int idx = tid; idx < 16 * 32; idx += kThreads) {
-            const int i = idx >> 5, ln = idx & 31;
             uint32_t v = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) v += accs[w * 16 * 32 + idx];
-            uint32_t* out = prm.part + static_cast<int64_t>(seg) * kStripCols + 32 * ln;
-            out[acc_column(i, 0)] = v & 0xFFFFu;
-            out[acc_column(i, 1)] = v >> 16;
+            prm.part[static_cast<int64_t>(seg) * 512 + idx] = v;
         }
         if (kLinks && warp == 0) {
             BandSummary C;
             unsigned long long links = 0;
             bool have = false;
             for (int w = 0; w < kWarps; ++w) {
-                if (wempty[w]) continue;
+                if (misc[w]) continue;
                 const uint32_t* ws = sums + w * kSumPlanes * 32;
                 BandSummary B{ws[lane], ws[32 + lane], ws[64 + lane], ws[96 + lane],
                               ws[128 + lane], ws[160 + lane], ws[192 + lane]};
@@ -297,8 +574,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                     have = true;
                 } else {
                     BandSummary D;
-                    const uint32_t r = compose_summary(C, B, D);
-                    links += __popc(r);
+                    links += __popc(compose_summary(C, B, D));
                     C = D;
                 }
             }
@@ -314,184 +590,78 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             gs[6 * 32 + lane] = C.T3;
             if (lane == 0) prm.seg_links[seg] = links;
         }
+        // ---- last CTA of the strip finishes it.  The barrier orders every
+        // thread's partial writes before tid 0's release; its acquire orders the
+        // finisher's reads of the other CTAs' partials after their releases.
+        __syncthreads();
+        if (tid == 0) {
+            YCHG_STAMP(20);
+            const unsigned long long t = atom_add_acq_rel(prm.strip_ticket + strip, 1ull);
+            const unsigned long long kk = static_cast<unsigned long long>(k);
+            misc[kWarps] = (t % kk) == kk - 1;
+            // Every scan adds exactly k to every strip's ticket, so t / k numbers the
+            // scan identically in all finishers: records are tagged with it (12 bits).
+            misc[kWarps + 1] = static_cast<int>((t / kk) % 4095ull) + 1;
+        }
+        __syncthreads();
+        if (tid == 0) YCHG_STAMP(21);
+        if (misc[kWarps]) {
+            finish_strip<kLinks>(prm, strip, static_cast<uint32_t>(misc[kWarps + 1]), stages);
+            if (tid == 0) YCHG_STAMP(22);
+        }
         __syncthreads();
     }
-}
-
-// ----------------------------------------------------------------------------
-// Finish: one CTA per strip.  counts, flags, per-strip boundary count, K3 stitch.
-template <bool kLinks>
-__global__ void __launch_bounds__(kThreads)
-ychg_finish_kernel(const ScanParams prm) {
-    __shared__ int32_t sc[kStripCols + 1];
-    __shared__ long long red_sum[kWarps];
-    __shared__ int red_nb[kWarps];
-    const int s = blockIdx.x;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int k = prm.seg_per_strip;
-    const int g0 = s * k;
-
-    long long local_sum = 0;
-    for (int col = tid; col < kStripCols; col += kThreads) {
-        uint32_t v = 0;
-        for (int g = g0; g < g0 + k; ++g) v += prm.part[static_cast<int64_t>(g) * kStripCols + col];
-        sc[col + 1] = static_cast<int32_t>(v);
-        const int gc = s * kStripCols + col;
-        if (gc < prm.width_cnt) {
-            prm.counts[gc] = static_cast<int32_t>(v);
-            local_sum += v;
-        }
-    }
-    if (tid == 0) {
-        // counts[c0 - 1] (counts[-1] := 0, runscan.cpp:147): last column of the previous strip.
-        uint32_t prev = 0;
-        if (s > 0)
-            for (int g = g0 - k; g < g0; ++g)
-                prev += prm.part[static_cast<int64_t>(g) * kStripCols + kStripCols - 1];
-        sc[0] = static_cast<int32_t>(prev);
-    }
-    __syncthreads();
-
-    const int nwords = (prm.width_cnt + 31) >> 5;
-    int nb = 0;
-    for (int wi = warp; wi < kStripWords; wi += kWarps) {
-        const int col = wi * 32 + lane;
-        const int gc = s * kStripCols + col;
-        const bool f = gc < prm.width_cnt && sc[col + 1] != sc[col];
-        const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
-        if (lane == 0 && s * kStripWords + wi < nwords) prm.flags[s * kStripWords + wi] = m;
-        nb += __popc(m);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) local_sum += __shfl_xor_sync(0xFFFFFFFFu, local_sum, o);
-    if (lane == 0) {
-        red_sum[warp] = local_sum;
-        red_nb[warp] = nb;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        long long t = 0;
-        int n = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            t += red_sum[w];
-            n += red_nb[w];
-        }
-        prm.strip_nb[s] = n;
-        atomicAdd(reinterpret_cast<unsigned long long*>(&prm.totals[0]),
-                  static_cast<unsigned long long>(t));
-    }
-
-    if (kLinks && warp == 0) {
-        // Stitch the strip's segment summaries top to bottom; row -1 and row H
-        // are background (runscan.cpp:45, hypergraph.cpp walks whole columns).
-        BandSummary C{};
-        unsigned long long links = 0;
-        for (int g = g0; g < g0 + k; ++g) {
-            const uint32_t* gs = prm.sums + static_cast<int64_t>(g) * kSumPlanes * 32;
-            BandSummary B{gs[lane], gs[32 + lane], gs[64 + lane], gs[96 + lane],
-                          gs[128 + lane], gs[160 + lane], gs[192 + lane]};
-            if (lane == 0) links += prm.seg_links[g];
-            if (g == g0) {
-                C = B;
-            } else {
-                BandSummary D;
-                links += __popc(compose_summary(C, B, D));
-                C = D;
-            }
-        }
-        // close whatever is open at the bottom edge
-        links += __popc(C.OE & C.T2 & ~C.T3);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
-        if (lane == 0)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&prm.totals[1]), links);
-    }
-}
-
-// ----------------------------------------------------------------------------
-// Ordered compaction of the change flags into the ascending boundary list.
-template <bool kLinks>
-__global__ void __launch_bounds__(kThreads)
-ychg_compact_kernel(const ScanParams prm) {
-    __shared__ long long red[kWarps];
-    __shared__ int wpre[kStripWords + 1];
-    const int s = blockIdx.x;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-    long long off = 0;
-    for (int t = tid; t < s; t += kThreads) off += prm.strip_nb[t];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
-    if (lane == 0) red[warp] = off;
-
-    const int nwords = (prm.width_cnt + 31) >> 5;
-    if (warp == 0) {
-        const int w = s * kStripWords + lane;
-        const uint32_t m = w < nwords ? prm.flags[w] : 0u;
-        int c = __popc(m);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        wpre[lane] = incl - c;
-    }
-    __syncthreads();
-    long long base = 0;
-    for (int w = 0; w < kWarps; ++w) base += red[w];
-
-    for (int wi = warp; wi < kStripWords; wi += kWarps) {
-        const int w = s * kStripWords + wi;
-        if (w >= nwords) break;
-        const uint32_t m = prm.flags[w];
-        if ((m >> lane) & 1u) {
-            const int r = __popc(m & ((1u << lane) - 1u));
-            prm.boundaries[base + wpre[wi] + r] = w * 32 + lane;
-        }
-    }
-
-    if (s == gridDim.x - 1 && tid == 0) {
-        prm.totals[3] = base + prm.strip_nb[s];
-        prm.totals[2] = kLinks ? prm.totals[0] - prm.totals[1] : -1;
-    }
+    if (tid == 0) YCHG_STAMP(23);
 }
 
 }  // namespace ychg_dev
 
 // ----------------------------------------------------------------------------
-// Host-side launchers (C linkage, called from ychg_capi.cu).
+// Host-side launcher (C linkage, called from ychg_capi.cu).
 using namespace ychg_dev;
+
+extern "C" const void* ychg_scan_kernel_ptr(int with_links) {
+    return with_links ? reinterpret_cast<const void*>(&ychg_scan_kernel<true>)
+                      : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
+}
+
+// Opt-in to >48 KB dynamic shared memory (per device, both variants).
+extern "C" int ychg_scan_kernel_prepare(void) {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return 0;
+    cudaError_t e = cudaFuncSetAttribute(&ychg_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kSmemTotal);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(&ychg_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemTotal);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    if (dev < 64) done[dev] = true;
+    return 0;
+}
 
 extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int grid, int with_links,
                                 cudaStream_t stream, cudaEvent_t ev_mid) {
-    // Opt-in to >48 KB dynamic shared memory once per device and variant.
-    static bool attr_done[2][64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const CUtensorMap* map = static_cast<const CUtensorMap*>(tmap);
+    (void)ev_mid;
+    if (const int rc = ychg_scan_kernel_prepare()) return rc;
+    const void* fn = with_links ? reinterpret_cast<const void*>(&ychg_scan_kernel<true>)
+                                : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
+    CUtensorMap map = *static_cast<const CUtensorMap*>(tmap);
+    ScanParams p = *prm;
+    void* args[2] = {&map, &p};
+    // Cross-CTA waits need every CTA resident: the grid never exceeds the
+    // occupancy-checked SM count (ychg_plan_create).  A cooperative launch makes
+    // that a driver-checked guarantee (YCHG_COOPERATIVE=1); the default regular
+    // launch is cheaper and pipelines with the previous kernel on the stream.
+    static const bool coop = [] {
+        const char* v = getenv("YCHG_COOPERATIVE");
+        return v && v[0] == '1';
+    }();
     cudaError_t e;
-    if (with_links) {
-        if (dev >= 64 || !attr_done[1][dev]) {
-            cudaFuncSetAttribute(ychg_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemTotal);
-            if (dev < 64) attr_done[1][dev] = true;
-        }
-        ychg_scan_kernel<true><<<grid, kThreads, kSmemTotal, stream>>>(*map, *prm);
-        if (ev_mid) cudaEventRecord(ev_mid, stream);
-        ychg_finish_kernel<true><<<prm->n_strips, kThreads, 0, stream>>>(*prm);
-        ychg_compact_kernel<true><<<prm->n_strips, kThreads, 0, stream>>>(*prm);
-    } else {
-        if (dev >= 64 || !attr_done[0][dev]) {
-            cudaFuncSetAttribute(ychg_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemTotal);
-            if (dev < 64) attr_done[0][dev] = true;
-        }
-        ychg_scan_kernel<false><<<grid, kThreads, kSmemTotal, stream>>>(*map, *prm);
-        if (ev_mid) cudaEventRecord(ev_mid, stream);
-        ychg_finish_kernel<false><<<prm->n_strips, kThreads, 0, stream>>>(*prm);
-        ychg_compact_kernel<false><<<prm->n_strips, kThreads, 0, stream>>>(*prm);
-    }
-    e = cudaGetLastError();
+    if (coop)
+        e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kSmemTotal, stream);
+    else
+        e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, kSmemTotal, stream);
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }

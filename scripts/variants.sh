@@ -1,0 +1,17 @@
+# Launch-shape sweep (benchmark only).  Prints step ms and roofline fraction per variant/pattern.
+for lib in paper_1307_2560_b200/libychg_b200.so paper_1307_2560_b200/libychg_b200_w12s3.so paper_1307_2560_b200/libychg_b200_w16s2.so; do
+  for pat in hbands random; do
+    for extra in "" "--counts-only"; do
+      r=$(YCHG_LIB=$lib timeout 120 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --pattern $pat $extra 2>&1 | tail -1)
+      python - "$lib" "$pat" "$extra" "$r" <<'PY'
+import json, sys
+lib, pat, extra, r = sys.argv[1:]
+try:
+    d = json.loads(r)
+    print(f"{lib.split('/')[-1]:28s} {pat:7s} {extra or 'full':13s} step {d['ms_per_step']*1000:7.2f} us  kernel {d['roofline']['kernel_ms']*1000:7.2f} us  frac {d['roofline']['frac']:.3f}  HE {d['totals']['hyperedges']}")
+except Exception as e:
+    print(lib, pat, extra, "FAILED", r[-300:])
+PY
+    done
+  done
+done

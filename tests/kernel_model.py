@@ -67,33 +67,36 @@ def compose(A: Summary, B: Summary) -> tuple[Summary, int]:
 
 
 def band(a_rows, b_rows, halo_a, halo_b, mk3, block_rows):
-    """Run one lane over a band; returns (Summary, links)."""
+    """Run one lane over a band; returns (Summary, links).  Head pairs start
+    poisoned at N >= 3 (G2 = G3 = 1) so their closing never counts locally."""
     n = lambda x: (~x) & M32  # noqa: E731
     pa, pb = halo_a, halo_b
-    Hd = (pa | pb) & mk3
-    O = Hd
-    G2 = G3 = h1 = h2 = E = 0
+    O = pa | pb
+    Hd = O
+    G2 = G3 = O
+    h1 = h2 = 0
     links = 0
     for start in range(0, len(a_rows), block_rows):
-        head = Hd != 0  # per lane; the kernel decides per warp, results are identical
+        head = (Hd & mk3) != 0  # per lane; the kernel decides per warp, results are identical
+        lks = []
         for a, b in zip(a_rows[start:start + block_rows], b_rows[start:start + block_rows]):
-            ab = a & b & mk3
+            ab = a & b
             f = ab & (pa ^ pb)
             cont = (a & pa) | (b & pb)
             lk = n(cont) & G2 & n(G3)
             if head:
-                lk &= n(Hd)
-                hf = Hd & f
-                h2 |= h1 & hf
-                h1 |= hf
-                E |= Hd & n(cont)
                 Hd &= cont
+                t = Hd & f
+                h2 |= h1 & t
+                h1 |= t
             g3 = (cont & G3) | (G2 & f)
             G2 = ab | (cont & G2)
             G3 = g3
             pa, pb = a, b
-            links += popc(lk)
-    return Summary(O, E, h1, h2, (pa | pb) & mk3, G2, G3), links
+            lks.append(lk)
+        links += sum(popc(x & mk3) for x in lks)
+    m = mk3
+    return Summary(O & m, O & n(Hd) & m, h1 & m, h2 & m, (pa | pb) & m, G2 & m, G3 & m), links
 
 
 def model_hyperedges(bits: np.ndarray, width: int, *, block_rows: int = 32, seg_per_strip: int = 1,

@@ -193,9 +193,9 @@ def test_timing_hooks(gpu):
     plan.set_timing(True)
     plan.scan_device(d.ptr, pitch, dc.ptr, df.ptr, db.ptr, dt.ptr)
     a, b = plan.last_ms()
-    assert a > 0 and b > 0
+    assert a > 0 and b == 0.0  # the finish is fused into the streaming kernel
     info = plan.info()
-    assert info.kernels_per_scan == 3 and info.grid >= 1
+    assert info.kernels_per_scan == 1 and info.grid >= 1
 
 
 def test_cxx_dropin_binary(gpu):
