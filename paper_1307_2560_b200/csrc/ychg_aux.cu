@@ -185,3 +185,42 @@ extern "C" int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }
+
+// ---- dense host layout -> pitched device layout (TMA needs 16 B-aligned row strides).
+// dst row y byte x (x < pitch) = src[y * row_bytes + x] for x < row_bytes, else 0.
+// Each thread assembles 4 destination bytes from two aligned source words.
+namespace {
+__global__ void repitch_kernel(const uint8_t* __restrict__ src, int64_t row_bytes, uint8_t* __restrict__ dst,
+                               int64_t pitch, int y0, int y1) {
+    const int64_t words_per_row = pitch >> 2;
+    const int64_t total = static_cast<int64_t>(y1 - y0) * words_per_row;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t yy = i / words_per_row;
+        const int64_t x = (i - yy * words_per_row) * 4;
+        const int64_t y = y0 + yy;
+        uint32_t out = 0;
+        if (x < row_bytes) {
+            const int64_t s = y * row_bytes + x;
+            const uint32_t* base = reinterpret_cast<const uint32_t*>(src + (s & ~int64_t(3)));
+            const uint32_t sh = static_cast<uint32_t>(s & 3) * 8;
+            out = __funnelshift_r(__ldg(base), __ldg(base + 1), sh);
+            const int64_t valid = row_bytes - x;
+            if (valid < 4) out &= (1u << (8 * valid)) - 1u;
+        }
+        reinterpret_cast<uint32_t*>(dst + y * pitch)[x >> 2] = out;
+    }
+}
+}  // namespace
+
+// src must have >= 8 readable bytes past its last row (the caller over-allocates).
+extern "C" int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint8_t* d_dst, int64_t pitch, int y0,
+                                   int y1, cudaStream_t stream) {
+    const int64_t total = static_cast<int64_t>(y1 - y0) * (pitch >> 2);
+    if (total <= 0) return 0;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    repitch_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_src, row_bytes, d_dst, pitch, y0, y1);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}

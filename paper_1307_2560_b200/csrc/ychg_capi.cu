@@ -426,6 +426,11 @@ struct HostContext {
     int device = 0;
     bool ready = false;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;   // H2D chunks overlap the re-pitch of the previous chunk
+    static constexpr int kChunks = 8;
+    cudaEvent_t chunk_ev[kChunks] = {};
+    uint8_t* d_dense = nullptr;            // dense staging copy of the host rows
+    int64_t dense_cap = 0;
     ychg_plan* plan = nullptr;
     int32_t plan_w = -1, plan_h = -1;
     uint8_t* d_bits = nullptr;
@@ -448,6 +453,8 @@ int ensure_context(HostContext& c) {
     CK(cudaSetDevice(c.device));
     if (!c.ready) {
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+        for (auto& e : c.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CK(cudaMalloc(&c.d_totals, sizeof(ychg_totals)));
         CK(cudaMallocHost(&c.h_totals, sizeof(ychg_totals)));
         c.ready = true;
@@ -529,10 +536,40 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
     }
     if (const int rc = ensure_columns(c, width)) return rc;
 
-    // H2D: pinned sources go straight to the copy engine; pageable ones are staged by the driver.
+    // H2D.  Row strides that are already TMA-legal (multiple of 16 B) copy straight
+    // into place.  Otherwise the rows go over PCIe as one dense 1-D stream (2-D
+    // copies of odd-sized rows run at less than half the link rate) in chunks on
+    // a copy stream, each chunk re-pitched on the device by a kernel while the
+    // next chunk is still in flight.
     (void)is_pinned;
-    CK(cudaMemcpy2DAsync(c.d_bits, pitch, bits, row_stride, row_bytes, height, cudaMemcpyHostToDevice,
-                         c.stream));
+    if (row_stride == pitch) {
+        CK(cudaMemcpyAsync(c.d_bits, bits, pitch * height, cudaMemcpyHostToDevice, c.stream));
+    } else if (row_stride != row_bytes) {
+        CK(cudaMemcpy2DAsync(c.d_bits, pitch, bits, row_stride, row_bytes, height, cudaMemcpyHostToDevice,
+                             c.stream));
+    } else {
+        const int64_t dense = row_bytes * height;
+        if (dense + 16 > c.dense_cap) {
+            cudaFree(c.d_dense);
+            c.d_dense = nullptr;
+            c.dense_cap = 0;
+            CK(cudaMalloc(&c.d_dense, dense + 16));
+            c.dense_cap = dense + 16;
+        }
+        CK(cudaEventRecord(c.chunk_ev[0], c.stream));  // order after earlier work on c.stream
+        CK(cudaStreamWaitEvent(c.copy_stream, c.chunk_ev[0], 0));
+        const int nch = height >= HostContext::kChunks * 64 ? HostContext::kChunks : 1;
+        for (int i = 0; i < nch; ++i) {
+            const int y0 = static_cast<int>((int64_t(height) * i) / nch);
+            const int y1 = static_cast<int>((int64_t(height) * (i + 1)) / nch);
+            CK(cudaMemcpyAsync(c.d_dense + y0 * row_bytes, bits + y0 * row_bytes, (y1 - y0) * row_bytes,
+                               cudaMemcpyHostToDevice, c.copy_stream));
+            CK(cudaEventRecord(c.chunk_ev[i], c.copy_stream));
+            CK(cudaStreamWaitEvent(c.stream, c.chunk_ev[i], 0));
+            const int rc = ychg_launch_repitch(c.d_dense, row_bytes, c.d_bits, pitch, y0, y1, c.stream);
+            if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "repitch kernel launch");
+        }
+    }
     if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, c.d_counts, c.d_flags,
                                         c.d_bounds, c.d_totals, c.stream))
         return rc;

@@ -22,6 +22,9 @@ const void* ychg_scan_kernel_ptr(int with_links);
 int ychg_launch_synth(int pattern, int width, int height, int bands, int cell, double density,
                       uint64_t seed, uint8_t* d_bits, int64_t pitch, cudaStream_t stream);
 
+int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint8_t* d_dst, int64_t pitch, int y0, int y1,
+                        cudaStream_t stream);
+
 int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
                            int32_t* d_boundaries, long long* d_n, cudaStream_t stream);
 }

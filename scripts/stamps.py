@@ -45,3 +45,7 @@ for name, a_, b_ in (("ticket->loads", 21, 24), ("loads->lookback", 24, 25), ("l
     print(f"{name:18s}", q(rel[isf, b_] - rel[isf, a_]))
 order = np.argsort(rel[isf, 21])
 print("finisher ticket->finish (sorted by ticket):", [f"{a:.1f}->{b:.1f}" for a, b in zip(rel[isf, 21][order], rel[isf, 22][order])])
+print("per-warp-index mean done:", " ".join(f"{x:.2f}" for x in wd.mean(0)))
+print("per-CTA mean done, by CTA index deciles:", " ".join(f"{x:.2f}" for x in [wd[i:i+15].mean() for i in range(0, wd.shape[0], 15)]))
+start = rel[:, 0]
+print("CTA entry spread", q(start))
