@@ -62,18 +62,20 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> None:
               "-Wl,-rpath,$ORIGIN"])
 
 
-def build_variant(warps: int, stages: int) -> str:
-    """Experimental launch-shape variants (benchmarking only): libychg_b200_w{W}s{S}.so."""
-    out = os.path.join(PKG, f"libychg_b200_w{warps}s{stages}.so")
+def build_variant(warps: int, stages: int, *defines: str) -> str:
+    """Experimental launch-shape / diagnostics variants (benchmarking only):
+    libychg_b200_w{W}s{S}[_define...].so."""
+    tag = "".join("_" + d.lower().replace("ychg_", "") for d in defines)
+    out = os.path.join(PKG, f"libychg_b200_w{warps}s{stages}{tag}.so")
     _run([_nvcc(), *NVCC_ARCH, "-lineinfo", "-O3", "-std=c++17", "--shared", f"-DYCHG_WARPS={warps}",
-          f"-DYCHG_STAGES={stages}", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I" + INCLUDE, "-o", out,
-          *[os.path.join(CSRC, f) for f in CU_SRCS]])
+          f"-DYCHG_STAGES={stages}", *[f"-D{d}" for d in defines], "-Xcompiler", "-fPIC,-fvisibility=hidden",
+          "-I" + INCLUDE, "-o", out, *[os.path.join(CSRC, f) for f in CU_SRCS]])
     return out
 
 
 if __name__ == "__main__":
     if "--variant" in sys.argv:
         i = sys.argv.index("--variant")
-        build_variant(int(sys.argv[i + 1]), int(sys.argv[i + 2]))
+        build_variant(int(sys.argv[i + 1]), int(sys.argv[i + 2]), *sys.argv[i + 3:])
     else:
         build(verbose_ptxas="-v" in sys.argv, force="-f" in sys.argv)

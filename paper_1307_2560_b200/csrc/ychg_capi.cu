@@ -179,9 +179,9 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
         const int64_t sz_part = G * 512 * 4, sz_sums = G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = G * 8;
         if (height >= (1 << 22))
             return fail(YCHG_ERR_INVALID, "plan_create: height %d >= 2^22 rows is not supported", height);
-        const int64_t sz_ticket = S * 8, sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
-        // order: part | sums | seg_links | strip_ticket | rec
-        plan->ws_bytes = sz_part + sz_sums + sz_seg + sz_ticket + sz_rec + 64;
+        const int64_t sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
+        // order: part | sums | seg_links | seg_ticket | seg_status | fin_ticket | fin_all | rec
+        plan->ws_bytes = sz_part + sz_sums + 3 * sz_seg + 2 * S * 8 + 64 + sz_rec + 64;
         cudaError_t e = cudaMalloc(&plan->ws, plan->ws_bytes);
         if (e != cudaSuccess) {
             plan->ws = nullptr;
@@ -200,8 +200,16 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
         w += sz_sums;
         p.seg_links = reinterpret_cast<unsigned long long*>(w);
         w += sz_seg;
-        p.strip_ticket = reinterpret_cast<unsigned long long*>(w);
-        w += sz_ticket;
+        p.seg_ticket = reinterpret_cast<unsigned long long*>(w);
+        w += sz_seg;
+        p.seg_status = reinterpret_cast<unsigned long long*>(w);
+        w += sz_seg;
+        p.fin_ticket = reinterpret_cast<unsigned long long*>(w);
+        w += S * 8;
+        p.fin_all = reinterpret_cast<unsigned long long*>(w);
+        w += 64;
+        p.fin_loaded = reinterpret_cast<unsigned long long*>(w);
+        w += S * 8;
         p.rec = reinterpret_cast<ychg_dev::StripRecord*>(w);
     }
     *out = plan.release();
@@ -228,7 +236,7 @@ int ychg_plan_get_info(const ychg_plan* plan, ychg_plan_info* out) {
     out->seg_per_strip = plan->prm.seg_per_strip;
     out->n_segments = plan->prm.n_segments;
     out->grid = plan->grid;
-    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 1 : 0;
+    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 2 : 0;
     out->workspace_bytes = plan->ws_bytes;
     return YCHG_OK;
 }

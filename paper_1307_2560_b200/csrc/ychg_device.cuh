@@ -40,7 +40,7 @@ constexpr int kSmemStages = kWarps * kStages * kStageBytes;            // 147456
 constexpr int kSmemBar = kWarps * kStages * 8;                         // mbarriers
 constexpr int kSmemAcc = kWarps * 16 * 32 * 4;                         // per-warp u16x2 counts
 constexpr int kSmemSum = kWarps * kSumPlanes * 32 * 4;                 // per-warp K3 summaries
-constexpr int kSmemMisc = kWarps * 16 + 16;                            // links + flags
+constexpr int kSmemMisc = kWarps * 24 + 48;                            // links, tree scratch, flags
 constexpr int kSmemTotal = kSmemStages + kSmemBar + kSmemAcc + kSmemSum + kSmemMisc;
 
 // What a strip's finisher publishes for the strips to its right: `status`
@@ -55,10 +55,10 @@ struct StripRecord {
 };
 
 // ----------------------------------------------------------------------------
-// Launch parameters of one scan.  Cross-CTA bookkeeping (tickets, strip
-// records) is epoch-tagged -- the epoch is derived on the device from the
-// monotonic strip tickets -- so it never needs resetting between scans and the
-// launch is CUDA-graph replayable.
+// Launch parameters of one scan.  Cross-CTA bookkeeping (segment flags, strip
+// records) is epoch-tagged -- each segment and each strip finisher numbers its
+// scans with its own monotonic ticket, so both sides agree -- it never needs
+// resetting between scans and the launches are CUDA-graph replayable.
 struct ScanParams {
     const uint8_t* bits;      // device image base (row-major packed bits)
     int64_t pitch;            // bytes between rows (multiple of 16 for TMA)
@@ -74,7 +74,11 @@ struct ScanParams {
     uint32_t* part;           // [n_segments][512] per-segment u16x2 column counts
     uint32_t* sums;           // [n_segments][7][32] K3 band summaries
     unsigned long long* seg_links;    // [n_segments] links closed inside each segment
-    unsigned long long* strip_ticket; // [n_strips] segments finished (monotonic)
+    unsigned long long* seg_ticket;   // [n_segments] scans started per segment (monotonic)
+    unsigned long long* seg_status;   // [n_segments] epoch tag of the last merged segment (release)
+    unsigned long long* fin_ticket;   // [n_strips] scans started per strip finisher (monotonic)
+    unsigned long long* fin_all;      // [1] strip finishers completed (monotonic)
+    unsigned long long* fin_loaded;   // [n_strips] scans whose workspace the finisher has loaded
     struct StripRecord* rec;  // [n_strips] published by each strip's finisher
     long long* totals;        // ychg_totals {total_runs, links, hyperedges, n_boundaries}
     int32_t* counts;          // [width_cnt] final per-column counts

@@ -188,12 +188,52 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// In-place, order-preserving tree composition of n band summaries stored in
+// shared memory (slot i = 7 planes x 32 lanes at base + i*224), using every warp
+// of the CTA: level s composes slots (p*2s, p*2s+s) into p*2s.  Returns, in
+// every thread, the number of links resolved at the junctions.  Must be called
+// by the whole CTA (contains __syncthreads).
+__device__ unsigned long long tree_compose(uint32_t* base, int n, unsigned long long* red) {
+    constexpr int kSW = kSumPlanes * 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long mine = 0;
+    for (int st = 1; st < n; st <<= 1) {
+        for (int p = warp; p * 2 * st + st < n; p += kWarps) {
+            uint32_t* a = base + (p * 2 * st) * kSW;
+            const uint32_t* b = base + (p * 2 * st + st) * kSW;
+            const BandSummary A{a[lane], a[32 + lane], a[64 + lane], a[96 + lane], a[128 + lane], a[160 + lane],
+                                a[192 + lane]};
+            const BandSummary B{b[lane], b[32 + lane], b[64 + lane], b[96 + lane], b[128 + lane], b[160 + lane],
+                                b[192 + lane]};
+            BandSummary C;
+            mine += __popc(compose_summary(A, B, C));
+            a[lane] = C.O;
+            a[32 + lane] = C.E;
+            a[64 + lane] = C.h1;
+            a[96 + lane] = C.h2;
+            a[128 + lane] = C.OE;
+            a[160 + lane] = C.T2;
+            a[192 + lane] = C.T3;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+    if (lane == 0) red[warp] = mine;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int w = 0; w < kWarps; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
 // Shared-memory scratch of the strip finisher (lives in the idle TMA stage area).
 struct FinishSmem {
     int32_t sc[kStripCols];       // counts of the strip's columns
     uint32_t fw[kStripWords];     // change-flag words of the strip (inside flags only)
     int wpre[kStripWords];        // exclusive prefix of popc(fw)
     long long red[kWarps];
+    long long red2[kWarps];
     long long base;
     uint32_t edge;                // flag of the strip's first column
 };
@@ -229,13 +269,49 @@ __device__ __forceinline__ unsigned long long warp_wait_epoch12(const unsigned l
 // strip's first-column flag (counts[c0] vs counts[c0-1], runscan.cpp:147)
 // follow -- then fire-and-forget writes.
 template <bool kLinks>
-__device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8_t* scratch) {
+__global__ void __launch_bounds__(kThreads)
+ychg_finish_kernel(const ScanParams prm) {
+    extern __shared__ __align__(128) uint8_t scratch[];
     FinishSmem& fs = *reinterpret_cast<FinishSmem*>(scratch);
     uint32_t* ssum = reinterpret_cast<uint32_t*>(scratch + ((sizeof(FinishSmem) + 127) / 128) * 128);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int s = blockIdx.x;
     const int k = prm.seg_per_strip;
     const int g0 = s * k;
     constexpr int kSumWords = kSumPlanes * 32;
+
+    // Let the next scan's streaming kernel launch right away (it only needs SMs;
+    // it waits on fin_loaded before reusing this scan's workspace).
+    asm volatile("griddepcontrol.launch_dependents;");
+    // (0) this strip's scan number, then wait until all k segments of this scan merged
+    unsigned long long scan_no = 0;
+    if (tid == 0) {
+        scan_no = atomicAdd(prm.fin_ticket + s, 1ull);
+        fs.base = static_cast<long long>(scan_no);
+    }
+    __syncthreads();
+    scan_no = static_cast<unsigned long long>(fs.base);
+    const uint32_t epoch = static_cast<uint32_t>(scan_no % 4095ull) + 1u;
+    if (warp == 0) {
+        for (int jb = 0; jb < k; jb += 32) {
+            const int j = jb + lane;
+            const bool act = j < k;
+            bool ok = !act;
+            while (true) {
+                if (!ok) ok = static_cast<uint32_t>(ld_acquire(prm.seg_status + g0 + (act ? j : 0))) == epoch;
+                if (__all_sync(0xFFFFFFFFu, ok)) break;
+            }
+        }
+    } else if (warp == 1 && lane == 0 && scan_no > 0) {
+        // Strip records and the outputs are shared by consecutive scans: every
+        // finisher of the previous scan must be done before this one publishes or
+        // writes anything (normally long done: this scan's stream just ended).
+        const unsigned long long need = scan_no * static_cast<unsigned long long>(prm.n_strips);
+        while (ld_acquire(prm.fin_all) < need) {
+        }
+    }
+    __syncthreads();
+    if (tid == 0) YCHG_STAMP(21);
 
     // (1) one batch of loads per 8 segments: partial counts (512 u16x2 words per
     //     segment over the CTA) and the K3 summaries (8 x 224 words).
@@ -284,7 +360,12 @@ __device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8
         }
     }
     __syncthreads();
-    if (tid == 0) YCHG_STAMP(24);
+    if (tid == 0) {
+        YCHG_STAMP(24);
+        // this scan's workspace for strip s is in smem: the next scan's stream
+        // kernel may overwrite it (it waits on this before its first partial write)
+        st_release(prm.fin_loaded + s, scan_no + 1);
+    }
 
     // (2) flags strictly inside the strip (columns 1..1023), counts out, run total
     const int nwords = (prm.width_cnt + 31) >> 5;
@@ -306,8 +387,10 @@ __device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8
 
     const bool last_strip = (s == prm.n_strips - 1);
     StripRecord* rec = prm.rec + s;
+    int inside = 0;
+    const int32_t first = fs.sc[0];
     if (warp == 0) {
-        // (3) publish this strip's record, then acquire every record to the left
+        // (3) publish this strip's record early: the strips to the right wait on it
         const int c = __popc(fs.fw[lane]);
         int incl = c;
 #pragma unroll
@@ -316,9 +399,25 @@ __device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8
             if (lane >= o) incl += t;
         }
         fs.wpre[lane] = incl - c;
-        const int inside = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const int32_t first = fs.sc[0];
+        inside = __shfl_sync(0xFFFFFFFFu, incl, 31);
         if (lane == 0) st_release(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
+    }
+    // (2b) K3: stitch the strip's segment summaries top to bottom (tree, all warps)
+    unsigned long long strip_links = 0;
+    if (kLinks) {
+        strip_links = tree_compose(ssum, k, reinterpret_cast<unsigned long long*>(fs.red2));
+        if (tid == 0) YCHG_STAMP(26);
+        if (warp == 1) {
+            // close whatever is still open at row H (virtual background row)
+            unsigned long long c = __popc(ssum[4 * 32 + lane] & ssum[5 * 32 + lane] & ~ssum[6 * 32 + lane]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+            strip_links += c;
+        }
+    }
+
+    if (warp == 0) {
+        // (4) acquire every record to the left: boundary offset + this strip's first-column flag
         long long off = 0;
         int32_t carry_last = 0;  // last(j-1) entering each chunk; last(-1) := 0
         for (int jb = 0; jb < s; jb += 32) {
@@ -335,38 +434,22 @@ __device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
         if (lane == 0) {
+            YCHG_STAMP(27);
             fs.edge = (first != carry_last) ? 1u : 0u;
             fs.base = off;
             if (last_strip) prm.totals[3] = off + fs.edge + inside;
         }
     } else if (warp == 1) {
-        // (4) K3: stitch the strip's segment summaries top to bottom, close at row H,
-        //     then release (runs, links) for the totals.
-        unsigned long long links = 0;
-        if (kLinks) {
-            BandSummary C;
-            for (int g = 0; g < k; ++g) {
-                const uint32_t* gs = ssum + g * kSumWords;
-                BandSummary B{gs[lane], gs[32 + lane], gs[64 + lane], gs[96 + lane], gs[128 + lane],
-                              gs[160 + lane], gs[192 + lane]};
-                if (g == 0) {
-                    C = B;
-                } else {
-                    BandSummary D;
-                    links += __popc(compose_summary(C, B, D));
-                    C = D;
-                }
-            }
-            links += __popc(C.OE & C.T2 & ~C.T3);
+        // (4) release (runs, links) for the totals
+        const unsigned long long links = strip_links;
+        unsigned long long sl = 0;  // links closed inside the strip's segments (lane-parallel loads)
+        if (kLinks)
+            for (int g = lane; g < k; g += 32) sl += __ldcg(prm.seg_links + g0 + g);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
-        }
+        for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xFFFFFFFFu, sl, o);
         if (lane == 0) {
             long long runs = 0;
             for (int w = 0; w < kWarps; ++w) runs += fs.red[w];
-            unsigned long long sl = 0;  // links closed inside the strip's segments
-            if (kLinks)
-                for (int g = 0; g < k; ++g) sl += __ldcg(prm.seg_links + g0 + g);
             rec->runs = runs;
             rec->links = static_cast<long long>(links + sl);
             st_release(&rec->tstat, static_cast<unsigned long long>(epoch));
@@ -423,6 +506,12 @@ __device__ void finish_strip(const ScanParams& prm, int s, uint32_t epoch, uint8
             prm.totals[2] = kLinks ? runs - links : -1;
         }
     }
+    __syncthreads();
+    if (tid == 0) {
+        YCHG_STAMP(22);
+        __threadfence();
+        atomicAdd(prm.fin_all, 1ull);
+    }
 }
 
 // ----------------------------------------------------------------------------
@@ -435,12 +524,15 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     uint32_t* accs = reinterpret_cast<uint32_t*>(smem + kSmemStages + kSmemBar);
     uint32_t* sums = accs + kWarps * 16 * 32;
     unsigned long long* wlinks = reinterpret_cast<unsigned long long*>(sums + kWarps * kSumPlanes * 32);
-    int* misc = reinterpret_cast<int*>(wlinks + kWarps);  // [0..W) warp empty, [W] finisher, [W+1] epoch
+    int* misc = reinterpret_cast<int*>(wlinks + 2 * kWarps);  // [0..W) warp empty, [W+1] epoch, [W+2] scan index
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
 
+    // Let this scan's finisher kernel launch now: its CTAs are small, co-reside
+    // with ours and wait on the per-segment flags (programmatic dependent launch).
+    asm volatile("griddepcontrol.launch_dependents;");
     if (tid == 0) {
         YCHG_STAMP(0);
         for (int i = 0; i < kWarps * kStages; ++i) mbar_init(&bars[i], 1);
@@ -465,6 +557,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         const int x0 = strip * kStripBytes;
         const int gw = strip * kStripWords + lane;
 
+        // this segment's scan number (agrees with the finisher's strip ticket)
+        if (tid == 0) {
+            const unsigned long long t = atomicAdd(prm.seg_ticket + seg, 1ull);
+            misc[kWarps + 1] = static_cast<int>(t % 4095ull) + 1;
+            misc[kWarps + 2] = static_cast<int>(t);  // scans before this one (< 2^31 per plan)
+        }
         LaneState s;
         s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
 #pragma unroll
@@ -506,14 +604,26 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             int since_flush = 0;
             for (int bi = 0; bi < nb; ++bi) {
                 const int st = it % kStages;
+#ifdef YCHG_COMPUTE_ONLY  // diagnostics build: reuse the first kStages blocks, no TMA after the fill
+                if (bi < kStages) mbar_wait(&my_bars[st], (it / kStages) & 1u);
+#else
                 mbar_wait(&my_bars[st], (it / kStages) & 1u);
+#endif
                 const uint8_t* sp = my_stages + st * kStageBytes;
+#ifdef YCHG_NO_HEAD  // diagnostics build: never take the head-mode block (wrong results, timing only)
+                if (false)
+#else
                 if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u))
+#endif
                     process_block<kLinks, true>(sp, lane, s, prm.mul2, prm.mul17);
                 else
                     process_block<kLinks, false>(sp, lane, s, prm.mul2, prm.mul17);
                 __syncwarp();
+#ifdef YCHG_COMPUTE_ONLY
+                if (false) {
+#else
                 if (lane == 0 && bi + kStages < nb) {
+#endif
                     fence_proxy_async();
                     mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
                     tma_load_2d(my_stages + st * kStageBytes, &tmap, &my_bars[st], x0,
@@ -529,7 +639,9 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 
             if (kLinks) {
                 const uint32_t m = s.mk3;
-                uint32_t* ws = sums + warp * kSumPlanes * 32;
+                int slot = 0;
+                for (int w = 0; w < warp; ++w) slot += ((w + 1) * nseg) / kWarps > (w * nseg) / kWarps;
+                uint32_t* ws = sums + slot * kSumPlanes * 32;
                 ws[0 * 32 + lane] = O & m;
                 ws[1 * 32 + lane] = O & ~s.Hd & m;
                 ws[2 * 32 + lane] = s.h1 & m;
@@ -542,6 +654,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                 for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xFFFFFFFFu, l, o);
                 if (lane == 0) wlinks[warp] = l;
             }
+        } else if (lane == 0) {
+            wlinks[warp] = 0;
         }
         uint32_t* wa = accs + warp * 16 * 32;
 #pragma unroll
@@ -552,6 +666,13 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         }
         __syncthreads();
 
+        // ---- the previous scan's finisher of this strip must hold its workspace first
+        if (tid == 0) {
+            const unsigned long long scan_idx = static_cast<unsigned long long>(misc[kWarps + 2]);
+            while (ld_acquire(prm.fin_loaded + strip) < scan_idx) {
+            }
+        }
+        __syncthreads();
         // ---- CTA merge: counts (sum over warps, coalesced u16x2 words), K3 (compose in row order).
         for (int idx = tid; idx < 16 * 32; idx += kThreads) {
             uint32_t v = 0;
@@ -559,55 +680,27 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             for (int w = 0; w < kWarps; ++w) v += accs[w * 16 * 32 + idx];
             prm.part[static_cast<int64_t>(seg) * 512 + idx] = v;
         }
-        if (kLinks && warp == 0) {
-            BandSummary C;
-            unsigned long long links = 0;
-            bool have = false;
-            for (int w = 0; w < kWarps; ++w) {
-                if (misc[w]) continue;
-                const uint32_t* ws = sums + w * kSumPlanes * 32;
-                BandSummary B{ws[lane], ws[32 + lane], ws[64 + lane], ws[96 + lane],
-                              ws[128 + lane], ws[160 + lane], ws[192 + lane]};
-                if (lane == 0) links += wlinks[w];
-                if (!have) {
-                    C = B;
-                    have = true;
-                } else {
-                    BandSummary D;
-                    links += __popc(compose_summary(C, B, D));
-                    C = D;
-                }
-            }
+        if (kLinks) {
+            // non-empty warp bands were written to consecutive slots (row order)
+            int nfull = 0;
+            for (int w = 0; w < kWarps; ++w) nfull += ((w + 1) * nseg) / kWarps > (w * nseg) / kWarps;
+            const unsigned long long jl = tree_compose(sums, nfull, wlinks + kWarps);
+            if (warp == 0) {
+                unsigned long long links = lane < kWarps ? wlinks[lane] : 0ull;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
-            uint32_t* gs = prm.sums + static_cast<int64_t>(seg) * kSumPlanes * 32;
-            gs[0 * 32 + lane] = C.O;
-            gs[1 * 32 + lane] = C.E;
-            gs[2 * 32 + lane] = C.h1;
-            gs[3 * 32 + lane] = C.h2;
-            gs[4 * 32 + lane] = C.OE;
-            gs[5 * 32 + lane] = C.T2;
-            gs[6 * 32 + lane] = C.T3;
-            if (lane == 0) prm.seg_links[seg] = links;
+                for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
+                uint32_t* gs = prm.sums + static_cast<int64_t>(seg) * kSumPlanes * 32;
+#pragma unroll
+                for (int q = 0; q < kSumPlanes; ++q) gs[q * 32 + lane] = sums[q * 32 + lane];
+                if (lane == 0) prm.seg_links[seg] = links + jl;
+            }
         }
-        // ---- last CTA of the strip finishes it.  The barrier orders every
-        // thread's partial writes before tid 0's release; its acquire orders the
-        // finisher's reads of the other CTAs' partials after their releases.
+        // ---- publish the segment: the barrier orders every thread's partial
+        // writes before tid 0's release store of the epoch-tagged flag.
         __syncthreads();
         if (tid == 0) {
             YCHG_STAMP(20);
-            const unsigned long long t = atom_add_acq_rel(prm.strip_ticket + strip, 1ull);
-            const unsigned long long kk = static_cast<unsigned long long>(k);
-            misc[kWarps] = (t % kk) == kk - 1;
-            // Every scan adds exactly k to every strip's ticket, so t / k numbers the
-            // scan identically in all finishers: records are tagged with it (12 bits).
-            misc[kWarps + 1] = static_cast<int>((t / kk) % 4095ull) + 1;
-        }
-        __syncthreads();
-        if (tid == 0) YCHG_STAMP(21);
-        if (misc[kWarps]) {
-            finish_strip<kLinks>(prm, strip, static_cast<uint32_t>(misc[kWarps + 1]), stages);
-            if (tid == 0) YCHG_STAMP(22);
+            st_release(prm.seg_status + seg, static_cast<unsigned long long>(misc[kWarps + 1]));
         }
         __syncthreads();
     }
@@ -625,7 +718,9 @@ extern "C" const void* ychg_scan_kernel_ptr(int with_links) {
                       : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
 }
 
-// Opt-in to >48 KB dynamic shared memory (per device, both variants).
+constexpr int kFinishSmemMax = 160 * 1024;
+
+// Opt-in to >48 KB dynamic shared memory (per device, all kernels and variants).
 extern "C" int ychg_scan_kernel_prepare(void) {
     static bool done[64] = {};
     int dev = 0;
@@ -636,32 +731,64 @@ extern "C" int ychg_scan_kernel_prepare(void) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemTotal);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(&ychg_finish_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kFinishSmemMax);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(&ychg_finish_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kFinishSmemMax);
     if (e != cudaSuccess) return static_cast<int>(e);
     if (dev < 64) done[dev] = true;
     return 0;
 }
 
+// Two launches per scan, both programmatic dependent launches: the streaming
+// kernel triggers its finisher at entry (the finisher CTAs are small and wait on
+// per-segment flags while the stream runs), and the finisher triggers the NEXT
+// scan's streaming kernel as soon as it holds this scan's workspace in smem, so
+// back-to-back scans (e.g. one CUDA graph) overlap each finish with the next
+// stream.  Every CTA of the finisher grid waits only on work that is already
+// launched; the streaming kernel never waits.
 extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int grid, int with_links,
                                 cudaStream_t stream, cudaEvent_t ev_mid) {
     (void)ev_mid;
     if (const int rc = ychg_scan_kernel_prepare()) return rc;
-    const void* fn = with_links ? reinterpret_cast<const void*>(&ychg_scan_kernel<true>)
+    const void* fa = with_links ? reinterpret_cast<const void*>(&ychg_scan_kernel<true>)
                                 : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
-    CUtensorMap map = *static_cast<const CUtensorMap*>(tmap);
-    ScanParams p = *prm;
-    void* args[2] = {&map, &p};
-    // Cross-CTA waits need every CTA resident: the grid never exceeds the
-    // occupancy-checked SM count (ychg_plan_create).  A cooperative launch makes
-    // that a driver-checked guarantee (YCHG_COOPERATIVE=1); the default regular
-    // launch is cheaper and pipelines with the previous kernel on the stream.
-    static const bool coop = [] {
-        const char* v = getenv("YCHG_COOPERATIVE");
+    const void* fb = with_links ? reinterpret_cast<const void*>(&ychg_finish_kernel<true>)
+                                : reinterpret_cast<const void*>(&ychg_finish_kernel<false>);
+    static const bool no_pdl = [] {
+        const char* v = getenv("YCHG_NO_PDL");
         return v && v[0] == '1';
     }();
-    cudaError_t e;
-    if (coop)
-        e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, kSmemTotal, stream);
-    else
-        e = cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, kSmemTotal, stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+
+    CUtensorMap map = *static_cast<const CUtensorMap*>(tmap);
+    ScanParams p = *prm;
+    void* args_a[2] = {&map, &p};
+    cudaLaunchConfig_t ca{};
+    ca.gridDim = dim3(grid);
+    ca.blockDim = dim3(kThreads);
+    ca.dynamicSmemBytes = kSmemTotal;
+    ca.stream = stream;
+    ca.attrs = attr;
+    ca.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelExC(&ca, fa, args_a);
+    if (e != cudaSuccess) return static_cast<int>(e);
+
+    const size_t fsm = ((sizeof(FinishSmem) + 127) / 128) * 128 +
+                       static_cast<size_t>(prm->seg_per_strip) * kSumPlanes * 32 * 4;
+    if (fsm > static_cast<size_t>(kFinishSmemMax)) return static_cast<int>(cudaErrorInvalidValue);
+    void* args_b[1] = {&p};
+    cudaLaunchConfig_t cb{};
+    cb.gridDim = dim3(prm->n_strips);
+    cb.blockDim = dim3(kThreads);
+    cb.dynamicSmemBytes = fsm;
+    cb.stream = stream;
+    cb.attrs = attr;
+    cb.numAttrs = 1;
+    e = cudaLaunchKernelExC(&cb, fb, args_b);
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }

@@ -35,13 +35,13 @@ wd = rel[:, 1:1 + min(nw, 16)]
 print("warp done    ", q(wd))
 print("warp spread per CTA (max-min)", q(wd.max(1) - wd.min(1)))
 print("merged (9)   ", q(rel[:, 20]))
-print("ticket (10)  ", q(rel[:, 21]))
+print("fin start(21)", q(rel[:21, 21]))
 isf = st[:, 22] > 0
 fin = rel[isf, 22]
 print("finish (11)  ", q(fin) if fin.size else "-", "finishers", fin.size)
 print("finish dur   ", q(rel[isf, 22] - rel[isf, 21]))
 print("exit (12)    ", q(rel[:, 23]))
-for name, a_, b_ in (("ticket->loads", 21, 24), ("loads->lookback", 24, 25), ("lookback->done", 25, 22)):
+for name, a_, b_ in (("segs->loads", 21, 24), ("loads->tree", 24, 26), ("tree->wait", 26, 27), ("wait->sync", 27, 25), ("sync->done", 25, 22)):
     print(f"{name:18s}", q(rel[isf, b_] - rel[isf, a_]))
 order = np.argsort(rel[isf, 21])
 print("finisher ticket->finish (sorted by ticket):", [f"{a:.1f}->{b:.1f}" for a, b in zip(rel[isf, 21][order], rel[isf, 22][order])])
