@@ -135,11 +135,12 @@ YCHG_API int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pi
 YCHG_API int ychg_plan_set_timing(ychg_plan* plan, int32_t enabled);
 YCHG_API int ychg_plan_last_ms(ychg_plan* plan, float* scan_ms, float* finish_ms);
 
-/* Diagnostics: per-CTA %globaltimer stamps of the streaming kernel (32 slots
- * per CTA: 0 entry, 1+w warp w (< 16) done streaming, 20 segment merged,
- * 21 strip ticket taken, 22 strip finished, 23 exit, 24 finisher loads done,
- * 25 finisher look-back done).  enable=1 allocates, 0 frees; host_out (may be
- * NULL) receives min(capacity, grid*32) stamps of the last scan. */
+/* Diagnostics: per-CTA %globaltimer stamps, layout [scan % 4][CTA][32 slots].
+ * Streaming kernel: 0 entry, 1+w warp w (< 16) done streaming, 20 segment
+ * published, 23 exit.  Finisher kernel (CTA = strip): 21 all segments seen,
+ * 24 loads done, 26 K3 tree done, 27 look-back done, 25 outputs ready, 22 done.
+ * enable=1 allocates, 0 frees; host_out (may be NULL) receives
+ * min(capacity, 4*grid*32) stamps. */
 YCHG_API int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, int32_t capacity,
                                     int32_t* n_ctas);
 

@@ -253,15 +253,16 @@ class Plan:
         return a.value, b.value
 
     def debug_stamps(self, enable: bool = True):
-        """Per-CTA %globaltimer stamps (ns) of the last scan, shape (grid, 32); see ychg_b200.h."""
+        """Per-CTA %globaltimer stamps (ns) of the last 4 scans, shape (4, grid, 32), indexed by
+        scan number % 4; see ychg_b200.h."""
         n = _i32(0)
         _check(_lib.ychg_plan_debug_stamps(self._h, int(enable), None, 0, ctypes.byref(n)), "debug_stamps")
         if not enable:
             return None
-        out = np.zeros((max(n.value, 1), 32), dtype=np.uint64)
+        out = np.zeros((4, max(n.value, 1), 32), dtype=np.uint64)
         _check(_lib.ychg_plan_debug_stamps(self._h, 1, out.ctypes.data_as(_vp), out.size, ctypes.byref(n)),
                "debug_stamps")
-        return out[: n.value]
+        return out[:, : n.value]
 
     def scan_device(self, d_bits: int, pitch: int, d_counts: int, d_flags: int, d_boundaries: int,
                     d_totals: int, stream: int = 0, with_hyperedges: bool = True) -> None:

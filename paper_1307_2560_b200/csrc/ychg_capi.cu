@@ -176,7 +176,8 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
         if (per_sm < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
         plan->grid = std::min(plan->grid, per_sm * sms);
         const int64_t S = p.n_strips, G = p.n_segments;
-        const int64_t sz_part = G * 512 * 4, sz_sums = G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = G * 8;
+        // part / sums / seg_links / seg_status are double-buffered by scan parity
+        const int64_t sz_part = 2 * G * 512 * 4, sz_sums = 2 * G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = 2 * G * 8;
         if (height >= (1 << 22))
             return fail(YCHG_ERR_INVALID, "plan_create: height %d >= 2^22 rows is not supported", height);
         const int64_t sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
@@ -266,8 +267,8 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
     if (!plan) return fail(YCHG_ERR_INVALID, "plan_debug_stamps: NULL plan");
     CK(cudaSetDevice(plan->device));
     if (enable && !plan->dbg && plan->grid > 0) {
-        CK(cudaMalloc(&plan->dbg, int64_t(plan->grid) * 32 * 8));
-        CK(cudaMemset(plan->dbg, 0, int64_t(plan->grid) * 32 * 8));
+        CK(cudaMalloc(&plan->dbg, int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4));
+        CK(cudaMemset(plan->dbg, 0, int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4));
     }
     if (!enable && plan->dbg) {
         CK(cudaFree(plan->dbg));
@@ -275,7 +276,7 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
     }
     if (n_ctas) *n_ctas = plan->grid;
     if (host_out && plan->dbg) {
-        const int64_t n = std::min<int64_t>(capacity, int64_t(plan->grid) * 32);
+        const int64_t n = std::min<int64_t>(capacity, int64_t(plan->grid) * 32 * 4);
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(host_out, plan->dbg, n * 8, cudaMemcpyDeviceToHost));
     }
@@ -332,6 +333,7 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     p.boundaries = d_boundaries;
     p.totals = reinterpret_cast<long long*>(d_totals);
     p.dbg = plan->dbg;
+    p.dbg_rows = std::max(plan->grid, p.n_strips);
     p.mul2 = 2u;
     p.mul17 = 1u << 17;
 

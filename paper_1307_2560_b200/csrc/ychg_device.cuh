@@ -84,7 +84,8 @@ struct ScanParams {
     int32_t* counts;          // [width_cnt] final per-column counts
     uint32_t* flags;          // [ceil(width_cnt/32)] change flags, bit j = column 32w+j
     int32_t* boundaries;      // [<= width_cnt] ascending boundary columns
-    unsigned long long* dbg;  // optional [grid][16] %globaltimer stamps (diagnostics), or null
+    unsigned long long* dbg;  // optional [4][dbg_rows][32] %globaltimer stamps (diagnostics), or null
+    int32_t dbg_rows;
 };
 
 // Segment j of a strip covers row blocks [seg_first(j), seg_first(j+1)).

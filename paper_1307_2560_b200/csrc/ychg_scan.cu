@@ -167,10 +167,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-#define YCHG_STAMP(slot)                                                             \
-    do {                                                                             \
-        if (prm.dbg) prm.dbg[static_cast<int64_t>(blockIdx.x) * 32 + (slot)] = globaltimer(); \
+// dbg layout: [scan index % 4][CTA][32 slots]; `ring` must be in scope.
+#define YCHG_STAMP_AT(slot, value)                                                                       \
+    do {                                                                                                 \
+        if (prm.dbg)                                                                                     \
+            prm.dbg[(static_cast<int64_t>(ring) * prm.dbg_rows + blockIdx.x) * 32 + (slot)] = (value);      \
     } while (0)
+#define YCHG_STAMP(slot) YCHG_STAMP_AT(slot, globaltimer())
 
 __device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
     unsigned long long old;
@@ -292,22 +295,24 @@ ychg_finish_kernel(const ScanParams prm) {
     __syncthreads();
     scan_no = static_cast<unsigned long long>(fs.base);
     const uint32_t epoch = static_cast<uint32_t>(scan_no % 4095ull) + 1u;
+    const int ring = static_cast<int>(scan_no & 3ull);
+    // Segment partials are double-buffered by scan parity (the next scan's
+    // stream kernel writes the other half while this finisher reads).
+    const int64_t par = static_cast<int64_t>(scan_no & 1ull);
+    const int64_t G = prm.n_segments;
+    const uint32_t* part_p = prm.part + par * G * 512;
+    const uint32_t* sums_p = prm.sums + par * G * kSumWords;
+    const unsigned long long* seglinks_p = prm.seg_links + par * G;
+    const unsigned long long* segstat_p = prm.seg_status + par * G;
     if (warp == 0) {
         for (int jb = 0; jb < k; jb += 32) {
             const int j = jb + lane;
             const bool act = j < k;
             bool ok = !act;
             while (true) {
-                if (!ok) ok = static_cast<uint32_t>(ld_acquire(prm.seg_status + g0 + (act ? j : 0))) == epoch;
+                if (!ok) ok = static_cast<uint32_t>(ld_acquire(segstat_p + g0 + (act ? j : 0))) == epoch;
                 if (__all_sync(0xFFFFFFFFu, ok)) break;
             }
-        }
-    } else if (warp == 1 && lane == 0 && scan_no > 0) {
-        // Strip records and the outputs are shared by consecutive scans: every
-        // finisher of the previous scan must be done before this one publishes or
-        // writes anything (normally long done: this scan's stream just ended).
-        const unsigned long long need = scan_no * static_cast<unsigned long long>(prm.n_strips);
-        while (ld_acquire(prm.fin_all) < need) {
         }
     }
     __syncthreads();
@@ -323,14 +328,14 @@ ychg_finish_kernel(const ScanParams prm) {
     for (int g = 0; g < k; g += 8) {
         const int n = k - g < 8 ? k - g : 8;
         uint32_t x[kR][8], y[kY];
-        const uint32_t* src = prm.part + static_cast<int64_t>(g0 + g) * 512;
+        const uint32_t* src = part_p + static_cast<int64_t>(g0 + g) * 512;
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
             const int idx = tid + r * kThreads;
 #pragma unroll
             for (int u = 0; u < 8; ++u) x[r][u] = (u < n && idx < 512) ? __ldcg(src + u * 512 + idx) : 0u;
         }
-        const uint32_t* ss = prm.sums + static_cast<int64_t>(g0 + g) * kSumWords;
+        const uint32_t* ss = sums_p + static_cast<int64_t>(g0 + g) * kSumWords;
         if (kLinks) {
 #pragma unroll
             for (int u = 0; u < kY; ++u) {
@@ -385,6 +390,15 @@ ychg_finish_kernel(const ScanParams prm) {
     if (lane == 0) fs.red[warp] = local_sum;
     __syncthreads();
 
+    // Strip records and the outputs are shared by consecutive scans: every
+    // finisher of the previous scan must be done before this one publishes or
+    // writes anything (normally long done by now).
+    if (tid == 0 && scan_no > 0) {
+        const unsigned long long need = scan_no * static_cast<unsigned long long>(prm.n_strips);
+        while (ld_acquire(prm.fin_all) < need) {
+        }
+    }
+    __syncthreads();
     const bool last_strip = (s == prm.n_strips - 1);
     StripRecord* rec = prm.rec + s;
     int inside = 0;
@@ -444,7 +458,7 @@ ychg_finish_kernel(const ScanParams prm) {
         const unsigned long long links = strip_links;
         unsigned long long sl = 0;  // links closed inside the strip's segments (lane-parallel loads)
         if (kLinks)
-            for (int g = lane; g < k; g += 32) sl += __ldcg(prm.seg_links + g0 + g);
+            for (int g = lane; g < k; g += 32) sl += __ldcg(seglinks_p + g0 + g);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xFFFFFFFFu, sl, o);
         if (lane == 0) {
@@ -533,8 +547,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     // Let this scan's finisher kernel launch now: its CTAs are small, co-reside
     // with ours and wait on the per-segment flags (programmatic dependent launch).
     asm volatile("griddepcontrol.launch_dependents;");
+    const unsigned long long t_entry = globaltimer();
     if (tid == 0) {
-        YCHG_STAMP(0);
         for (int i = 0; i < kWarps * kStages; ++i) mbar_init(&bars[i], 1);
     }
     fence_proxy_async();
@@ -562,6 +576,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             const unsigned long long t = atomicAdd(prm.seg_ticket + seg, 1ull);
             misc[kWarps + 1] = static_cast<int>(t % 4095ull) + 1;
             misc[kWarps + 2] = static_cast<int>(t);  // scans before this one (< 2^31 per plan)
+            const int ring = static_cast<int>(t & 3ull);
+            YCHG_STAMP_AT(0, t_entry);
         }
         LaneState s;
         s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
@@ -662,14 +678,17 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         for (int i = 0; i < 16; ++i) wa[i * 32 + lane] = s.acc[i];
         if (lane == 0) {
             misc[warp] = (nb == 0);
+            const int ring = misc[kWarps + 2] & 3;
             if (warp < 16) YCHG_STAMP(1 + warp);
         }
         __syncthreads();
 
-        // ---- the previous scan's finisher of this strip must hold its workspace first
-        if (tid == 0) {
-            const unsigned long long scan_idx = static_cast<unsigned long long>(misc[kWarps + 2]);
-            while (ld_acquire(prm.fin_loaded + strip) < scan_idx) {
+        // ---- partials are double-buffered by scan parity: the finisher of the scan
+        // two back (same half) must have loaded this strip before we overwrite it
+        const unsigned long long scan_idx = static_cast<unsigned long long>(misc[kWarps + 2]);
+        const int64_t par = static_cast<int64_t>(scan_idx & 1ull);
+        if (tid == 0 && scan_idx >= 2) {
+            while (ld_acquire(prm.fin_loaded + strip) < scan_idx - 1) {
             }
         }
         __syncthreads();
@@ -678,7 +697,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             uint32_t v = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) v += accs[w * 16 * 32 + idx];
-            prm.part[static_cast<int64_t>(seg) * 512 + idx] = v;
+            prm.part[(par * prm.n_segments + seg) * 512 + idx] = v;
         }
         if (kLinks) {
             // non-empty warp bands were written to consecutive slots (row order)
@@ -689,22 +708,26 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                 unsigned long long links = lane < kWarps ? wlinks[lane] : 0ull;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
-                uint32_t* gs = prm.sums + static_cast<int64_t>(seg) * kSumPlanes * 32;
+                uint32_t* gs = prm.sums + (par * prm.n_segments + seg) * kSumPlanes * 32;
 #pragma unroll
                 for (int q = 0; q < kSumPlanes; ++q) gs[q * 32 + lane] = sums[q * 32 + lane];
-                if (lane == 0) prm.seg_links[seg] = links + jl;
+                if (lane == 0) prm.seg_links[par * prm.n_segments + seg] = links + jl;
             }
         }
         // ---- publish the segment: the barrier orders every thread's partial
         // writes before tid 0's release store of the epoch-tagged flag.
         __syncthreads();
         if (tid == 0) {
+            const int ring = misc[kWarps + 2] & 3;
             YCHG_STAMP(20);
-            st_release(prm.seg_status + seg, static_cast<unsigned long long>(misc[kWarps + 1]));
+            st_release(prm.seg_status + par * prm.n_segments + seg, static_cast<unsigned long long>(misc[kWarps + 1]));
         }
         __syncthreads();
     }
-    if (tid == 0) YCHG_STAMP(23);
+    if (tid == 0 && prm.n_segments > 0) {
+        const int ring = misc[kWarps + 2] & 3;
+        YCHG_STAMP(23);
+    }
 }
 
 }  // namespace ychg_dev
@@ -737,6 +760,17 @@ extern "C" int ychg_scan_kernel_prepare(void) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_finish_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kFinishSmemMax);
+    // Same (maximum) shared-memory carveout for every kernel of a scan: an SM only
+    // co-schedules CTAs whose carveout matches, and the finisher must co-reside
+    // with the streaming CTAs it waits on.
+    const void* fns[4] = {reinterpret_cast<const void*>(&ychg_scan_kernel<true>),
+                          reinterpret_cast<const void*>(&ychg_scan_kernel<false>),
+                          reinterpret_cast<const void*>(&ychg_finish_kernel<true>),
+                          reinterpret_cast<const void*>(&ychg_finish_kernel<false>)};
+    for (const void* f : fns)
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     static_cast<int>(cudaSharedmemCarveoutMaxShared));
     if (e != cudaSuccess) return static_cast<int>(e);
     if (dev < 64) done[dev] = true;
     return 0;
