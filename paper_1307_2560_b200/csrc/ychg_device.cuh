@@ -18,7 +18,7 @@ namespace ychg_dev {
 #define YCHG_WARPS 8
 #endif
 #ifndef YCHG_STAGES
-#define YCHG_STAGES 4
+#define YCHG_STAGES 2
 #endif
 constexpr int kWarps = YCHG_WARPS;               // warps per CTA
 constexpr int kThreads = kWarps * 32;
