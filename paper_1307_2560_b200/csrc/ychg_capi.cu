@@ -437,7 +437,7 @@ struct HostContext {
     bool ready = false;
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;   // H2D chunks overlap the re-pitch of the previous chunk
-    static constexpr int kChunks = 8;
+    static constexpr int kChunks = 4;
     cudaEvent_t chunk_ev[kChunks] = {};
     uint8_t* d_dense = nullptr;            // dense staging copy of the host rows
     int64_t dense_cap = 0;
@@ -451,6 +451,10 @@ struct HostContext {
     int64_t cols_cap = 0;
     ychg_totals* d_totals = nullptr;
     ychg_totals* h_totals = nullptr;  // pinned
+    int32_t* h_out = nullptr;         // pinned staging: counts | boundaries (capacity cols_cap each)
+    bool h2d_timing = false;
+    cudaEvent_t h2d_ev[3] = {nullptr, nullptr, nullptr};
+    int64_t h_out_cap = 0;
 };
 
 HostContext& host_context(int device) {
@@ -465,6 +469,10 @@ int ensure_context(HostContext& c) {
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
         for (auto& e : c.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        const char* ht = getenv("YCHG_HOST_TIMING");
+        c.h2d_timing = ht && ht[0] == '1';
+        if (c.h2d_timing)
+            for (auto& e : c.h2d_ev) CK(cudaEventCreate(&e));
         CK(cudaMalloc(&c.d_totals, sizeof(ychg_totals)));
         CK(cudaMallocHost(&c.h_totals, sizeof(ychg_totals)));
         c.ready = true;
@@ -568,6 +576,7 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
         }
         CK(cudaEventRecord(c.chunk_ev[0], c.stream));  // order after earlier work on c.stream
         CK(cudaStreamWaitEvent(c.copy_stream, c.chunk_ev[0], 0));
+        if (c.h2d_timing) cudaEventRecord(c.h2d_ev[0], c.copy_stream);
         const int nch = height >= HostContext::kChunks * 64 ? HostContext::kChunks : 1;
         for (int i = 0; i < nch; ++i) {
             const int y0 = static_cast<int>((int64_t(height) * i) / nch);
@@ -579,19 +588,56 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
             const int rc = ychg_launch_repitch(c.d_dense, row_bytes, c.d_bits, pitch, y0, y1, c.stream);
             if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "repitch kernel launch");
         }
+        if (c.h2d_timing) {
+            cudaEventRecord(c.h2d_ev[1], c.copy_stream);
+            cudaEventRecord(c.h2d_ev[2], c.stream);
+        }
+    }
+    static const bool host_timing = [] {
+        const char* v = getenv("YCHG_HOST_TIMING");
+        return v && v[0] == '1';
+    }();
+    cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+    if (host_timing) {
+        for (auto& e : tev) cudaEventCreate(&e);
+        cudaEventRecord(tev[0], c.stream);
     }
     if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, c.d_counts, c.d_flags,
                                         c.d_bounds, c.d_totals, c.stream))
         return rc;
+    if (host_timing) cudaEventRecord(tev[1], c.stream);
+    // D2H in one round trip: totals + counts + the whole boundary buffer into pinned
+    // staging (W ints cost microseconds; a second synchronisation costs more), then
+    // host copies of exactly what the caller asked for.
+    if (c.h_out_cap < 2 * int64_t(width)) {
+        cudaFreeHost(c.h_out);
+        c.h_out = nullptr;
+        c.h_out_cap = 0;
+        CK(cudaMallocHost(&c.h_out, 2 * int64_t(width) * 4));
+        c.h_out_cap = 2 * int64_t(width);
+    }
     CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
     if (counts_out)
-        CK(cudaMemcpyAsync(counts_out, c.d_counts, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(c.h_out, c.d_counts, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (boundaries_out)
+        CK(cudaMemcpyAsync(c.h_out + width, c.d_bounds, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (host_timing) cudaEventRecord(tev[2], c.stream);
     CK(cudaStreamSynchronize(c.stream));
-    const ychg_totals t = *c.h_totals;
-    if (boundaries_out && t.n_boundaries > 0) {
-        CK(cudaMemcpyAsync(boundaries_out, c.d_bounds, t.n_boundaries * 4, cudaMemcpyDeviceToHost, c.stream));
-        CK(cudaStreamSynchronize(c.stream));
+    if (host_timing) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, tev[0], tev[1]);
+        cudaEventElapsedTime(&b, tev[1], tev[2]);
+        float h1 = 0, h2 = 0;
+        cudaEventElapsedTime(&h1, c.h2d_ev[0], c.h2d_ev[1]);
+        cudaEventElapsedTime(&h2, c.h2d_ev[0], c.h2d_ev[2]);
+        std::fprintf(stderr, "[ychg host] h2d copies %.1f us, +repitch %.1f us, scan %.1f us, d2h %.1f us\n",
+                     h1 * 1e3, h2 * 1e3, a * 1e3, b * 1e3);
+        for (auto& e : tev) cudaEventDestroy(e);
     }
+    const ychg_totals t = *c.h_totals;
+    if (counts_out) std::memcpy(counts_out, c.h_out, size_t(width) * 4);
+    if (boundaries_out && t.n_boundaries > 0)
+        std::memcpy(boundaries_out, c.h_out + width, size_t(t.n_boundaries) * 4);
     if (totals_out) *totals_out = t;
     return YCHG_OK;
 }
