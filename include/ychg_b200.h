@@ -110,6 +110,18 @@ YCHG_API int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, 
                    int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
                    ychg_totals* totals_out);
 
+/* Run materialisation (build_profile / column_runs, runscan.cpp:78-143).
+ * Runs are int32 triples {col, y_top, y_bot} (the layout of ychg::Run), column-major
+ * and sorted by y_top inside a column -- ColumnProfile::runs flattened.
+ * *n_runs_out always receives the total; runs are written only when
+ * runs_capacity >= total (call once with runs_out = NULL to size the buffer). */
+YCHG_API int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                     int32_t strategy_kind, int32_t threads, int32_t* counts_out,
+                                     int32_t* runs_out, int64_t runs_capacity, int64_t* n_runs_out);
+/* Runs of one column (runscan.cpp:104-120); YCHG_ERR_INVALID if col is out of range. */
+YCHG_API int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                   int32_t col, int32_t* runs_out, int64_t runs_capacity, int64_t* n_out);
+
 /* ---- device-resident plans ----
  * A plan fixes the geometry and owns its device workspace.  width_img columns
  * are present in the buffer, width_cnt <= width_img are counted; columns

@@ -86,6 +86,8 @@ class Oracle:
         L.yo_hyperedge_count.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i64p, _i64p]
         L.yo_pair_link_counts.restype = ctypes.c_int
         L.yo_pair_link_counts.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i32p]
+        L.yo_profile.restype = ctypes.c_int64
+        L.yo_profile.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i32p, ctypes.c_int64, _i32p]
         L.yo_foreground_count.restype = ctypes.c_int64
         L.yo_foreground_count.argtypes = [_u8p, ctypes.c_int64]
         self.lib = L
@@ -129,6 +131,17 @@ class Oracle:
             raise MemoryError("oracle hyperedge_count allocation failed")
         return int(he), int(tr.value), int(lk.value)
 
+    def profile(self, bits: np.ndarray, w: int) -> np.ndarray:
+        """(n, 3) int32 runs {col, y_top, y_bot}, column-major (build_profile flattened)."""
+        h = bits.shape[0]
+        if w == 0 or h == 0:
+            return np.zeros((0, 3), dtype=np.int32)
+        bits = np.ascontiguousarray(bits)
+        n = self.lib.yo_profile(_ptr(bits, _u8p), w, h, bits.shape[1], None, 0, None)
+        out = np.zeros((max(n, 1), 3), dtype=np.int32)
+        self.lib.yo_profile(_ptr(bits, _u8p), w, h, bits.shape[1], _ptr(out, _i32p), n, None)
+        return out[:n]
+
     def pair_links(self, bits: np.ndarray, w: int) -> np.ndarray:
         h = bits.shape[0]
         out = np.zeros(max(w - 1, 0), dtype=np.int32)
@@ -165,6 +178,8 @@ class Reference:
         L.yr_boundaries.argtypes = [_i32p, ctypes.c_int64, _i32p]
         L.yr_hyperedges.restype = ctypes.c_int64
         L.yr_hyperedges.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        L.yr_profile.restype = ctypes.c_int64
+        L.yr_profile.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _i32p, ctypes.c_int64]
         L.yr_time_path.restype = ctypes.c_int
         L.yr_time_path.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, _i64p, _i32p, _i64p, _i64p]
@@ -230,6 +245,14 @@ class RefImage:
         if rc != 0:
             raise RuntimeError(self.ref.last_error())
         return out[: self.width].copy()
+
+    def profile(self, kind: int = 0, threads: int = 1) -> np.ndarray:
+        n = self.ref.lib.yr_profile(self.handle, kind, threads, None, 0)
+        if n < 0:
+            raise RuntimeError(self.ref.last_error())
+        out = np.zeros((max(n, 1), 3), dtype=np.int32)
+        self.ref.lib.yr_profile(self.handle, kind, threads, _ptr(out, _i32p), n)
+        return out[:n]
 
     def hyperedges(self, kind: int = 0, threads: int = 1) -> int:
         v = self.ref.lib.yr_hyperedges(self.handle, kind, threads)

@@ -126,6 +126,26 @@ YR_EXPORT int64_t yr_hyperedges(void* img, int kind, int threads) {
     }
 }
 
+// build_profile (runscan.hpp:64-66) flattened column-major into int32 triples.
+YR_EXPORT int64_t yr_profile(void* img, int kind, int threads, int32_t* runs, int64_t capacity) {
+    try {
+        const auto prof = ychg::build_profile(*static_cast<ychg::BinaryImage*>(img), strategy_of(kind, threads));
+        int64_t n = 0;
+        for (const auto& col : prof.runs)
+            for (const auto& r : col) {
+                if (runs && n < capacity) {
+                    runs[3 * n] = r.col;
+                    runs[3 * n + 1] = r.y_top;
+                    runs[3 * n + 2] = r.y_bot;
+                }
+                ++n;
+            }
+        return n;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 // The reference's full hot path (counts + boundaries + hyperedge total), timed
 // with the reference protocol (bench.cpp:37-57: warmup untimed, reps timed with
 // steady_clock).  with_hyperedges=0 times counts + boundaries only.

@@ -243,3 +243,32 @@ YO_EXPORT int64_t yo_foreground_count(const uint8_t* bits, int64_t nbytes) {
     for (int64_t i = 0; i < nbytes; ++i) n += __builtin_popcount(bits[i]);
     return n;
 }
+
+/* ---------------------------------------------------------------- run materialisation
+ * collect_runs_in_columns / build_profile (runscan.cpp:78-100,130-143), restated per
+ * column: flat column-major int32 triples {col, y_top, y_bot}.  Returns the number
+ * of runs; writes at most `capacity` triples (runs may be NULL to only count). */
+YO_EXPORT int64_t yo_profile(const uint8_t* bits, int w, int h, int64_t stride, int32_t* runs, int64_t capacity,
+                             int32_t* counts) {
+    int64_t n = 0;
+    for (int c = 0; c < w; ++c) {
+        int start = -1, k = 0;
+        for (int y = 0; y <= h; ++y) {
+            const int bit = y < h ? yo_get(bits, stride, c, y) : 0;
+            if (bit) {
+                if (start < 0) start = y;
+            } else if (start >= 0) {
+                if (runs && n < capacity) {
+                    runs[3 * n + 0] = c;
+                    runs[3 * n + 1] = start;
+                    runs[3 * n + 2] = y - 1;
+                }
+                ++n;
+                ++k;
+                start = -1;
+            }
+        }
+        if (counts) counts[c] = k;
+    }
+    return n;
+}

@@ -58,6 +58,8 @@ _SIGS = {
     "ychg_cut_vertex_counts": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp]),
     "ychg_detect_boundary_columns": (ctypes.c_int, [_vp, _i64, _vp, ctypes.POINTER(_i64)]),
     "ychg_scan_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, ctypes.POINTER(Totals)]),
+    "ychg_build_profile_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64)]),
+    "ychg_column_runs_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
     "ychg_plan_create": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "ychg_plan_destroy": (None, [_vp]),
     "ychg_plan_get_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
@@ -219,6 +221,54 @@ def hyperedge_count(image: BinaryImage) -> int:
     return scan(image).hyperedges
 
 
+@dataclass
+class ColumnProfile:
+    """runscan.hpp:40-50: per-column runs + counts.  `runs_flat` is the (n, 3) int32
+    array {col, y_top, y_bot}, column-major, sorted by y_top inside a column."""
+    width: int
+    height: int
+    counts: np.ndarray
+    runs_flat: np.ndarray
+
+    @property
+    def col_off(self) -> np.ndarray:
+        return np.concatenate([[0], np.cumsum(self.counts, dtype=np.int64)])
+
+    def runs(self, col: int) -> np.ndarray:
+        o = self.col_off
+        return self.runs_flat[o[col]:o[col + 1]]
+
+    def total_runs(self) -> int:
+        return int(self.counts.sum())
+
+
+def build_profile(image: BinaryImage, strategy: ScanStrategy = ScanStrategy.serial()) -> ColumnProfile:
+    """build_profile (runscan.cpp:130-143) on the GPU: count -> scan -> fill."""
+    counts = np.zeros(max(image.width, 1), dtype=np.int32)
+    n = _i64(0)
+    _check(_lib.ychg_build_profile_host(image._ptr(), image.width, image.height, image.row_stride, strategy.kind,
+                                        strategy.threads, counts.ctypes.data_as(_vp), None, 0, ctypes.byref(n)),
+           "build_profile")
+    runs = np.zeros((max(n.value, 1), 3), dtype=np.int32)
+    if n.value > 0:
+        _check(_lib.ychg_build_profile_host(image._ptr(), image.width, image.height, image.row_stride,
+                                            strategy.kind, strategy.threads, counts.ctypes.data_as(_vp),
+                                            runs.ctypes.data_as(_vp), n.value, ctypes.byref(n)), "build_profile")
+    return ColumnProfile(image.width, image.height, counts[: image.width].copy(), runs[: n.value].copy())
+
+
+def column_runs(image: BinaryImage, col: int) -> np.ndarray:
+    """column_runs (runscan.cpp:104-120): (n, 3) int32 {col, y_top, y_bot}."""
+    n = _i64(0)
+    _check(_lib.ychg_column_runs_host(image._ptr(), image.width, image.height, image.row_stride, int(col), None, 0,
+                                      ctypes.byref(n)), "column_runs")
+    out = np.zeros((max(n.value, 1), 3), dtype=np.int32)
+    if n.value > 0:
+        _check(_lib.ychg_column_runs_host(image._ptr(), image.width, image.height, image.row_stride, int(col),
+                                          out.ctypes.data_as(_vp), n.value, ctypes.byref(n)), "column_runs")
+    return out[: n.value].copy()
+
+
 # ---------------------------------------------------------------- device-resident plumbing
 class Plan:
     """Geometry-specific launch plan + workspace on one device (ychg_plan_*)."""
@@ -332,7 +382,8 @@ def synth(pattern: str, width: int, height: int, *, bands: int = 0, cell: int = 
 
 
 __all__ = [
-    "BinaryImage", "ScanStrategy", "ScanResult", "Error", "ValidationError", "cut_vertex_counts",
+    "BinaryImage", "ScanStrategy", "ScanResult", "ColumnProfile", "build_profile", "column_runs", "Error",
+    "ValidationError", "cut_vertex_counts",
     "detect_boundary_columns", "scan", "hyperedge_count", "Plan", "DeviceBuffer", "synth", "synth_device",
     "pitch_for", "device_count", "Totals", "PlanInfo", "LIB_PATH", "CXX_LIB_PATH", "EXPORTED_SYMBOLS",
 ]

@@ -451,6 +451,13 @@ struct HostContext {
     int64_t cols_cap = 0;
     ychg_totals* d_totals = nullptr;
     ychg_totals* h_totals = nullptr;  // pinned
+    // run materialisation (build_profile / column_runs)
+    uint32_t* d_band = nullptr;
+    int64_t band_cap = 0;
+    int64_t* d_col_off = nullptr;
+    int64_t col_off_cap = 0;
+    int32_t* d_runs = nullptr;
+    int64_t runs_cap = 0;
     int32_t* h_out = nullptr;         // pinned staging: counts | boundaries (capacity cols_cap each)
     bool h2d_timing = false;
     cudaEvent_t h2d_ev[3] = {nullptr, nullptr, nullptr};
@@ -516,33 +523,14 @@ bool is_pinned(const void* p) {
 
 }  // namespace
 
-extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
-                              int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
-                              ychg_totals* totals_out) {
-    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan: negative geometry %dx%d", width, height);
+// H2D of the caller's rows into the context's pitched device image.  Row strides
+// that are already TMA-legal (multiple of 16 B) copy straight into place.
+// Otherwise the rows go over PCIe as one dense 1-D stream (2-D copies of
+// odd-sized rows run at less than half the link rate) in chunks on a copy
+// stream, each chunk re-pitched on the device by a kernel while the next chunk
+// is still in flight.
+int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride) {
     const int64_t row_bytes = (int64_t(width) + 7) / 8;
-    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
-        return fail(YCHG_ERR_INVALID, "scan: row_stride %lld < %lld", static_cast<long long>(row_stride),
-                    static_cast<long long>(row_bytes));
-    const int device = pick_device();
-    if (const int rc = require_device(device)) return rc;
-    HostContext& c = host_context(device);
-    std::lock_guard<std::mutex> lock(c.mu);
-    if (const int rc = ensure_context(c)) return rc;
-
-    if (width == 0 || height == 0) {
-        if (counts_out && width > 0) std::memset(counts_out, 0, size_t(width) * 4);
-        if (totals_out) *totals_out = ychg_totals{0, 0, with_hyperedges ? 0 : -1, 0};
-        return YCHG_OK;
-    }
-    if (c.plan_w != width || c.plan_h != height) {
-        ychg_plan_destroy(c.plan);
-        c.plan = nullptr;
-        c.plan_w = c.plan_h = -1;
-        if (const int rc = ychg_plan_create(device, width, width, height, &c.plan)) return rc;
-        c.plan_w = width;
-        c.plan_h = height;
-    }
     const int64_t pitch = (row_bytes + 15) / 16 * 16;
     const int64_t need = pitch * height;
     if (need > c.bits_cap) {
@@ -552,13 +540,7 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
         CK(cudaMalloc(&c.d_bits, need));
         c.bits_cap = need;
     }
-    if (const int rc = ensure_columns(c, width)) return rc;
 
-    // H2D.  Row strides that are already TMA-legal (multiple of 16 B) copy straight
-    // into place.  Otherwise the rows go over PCIe as one dense 1-D stream (2-D
-    // copies of odd-sized rows run at less than half the link rate) in chunks on
-    // a copy stream, each chunk re-pitched on the device by a kernel while the
-    // next chunk is still in flight.
     (void)is_pinned;
     if (row_stride == pitch) {
         CK(cudaMemcpyAsync(c.d_bits, bits, pitch * height, cudaMemcpyHostToDevice, c.stream));
@@ -593,6 +575,39 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
             cudaEventRecord(c.h2d_ev[2], c.stream);
         }
     }
+    return YCHG_OK;
+}
+
+extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                              int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
+                              ychg_totals* totals_out) {
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan: negative geometry %dx%d", width, height);
+    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
+        return fail(YCHG_ERR_INVALID, "scan: row_stride %lld < %lld", static_cast<long long>(row_stride),
+                    static_cast<long long>(row_bytes));
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+
+    if (width == 0 || height == 0) {
+        if (counts_out && width > 0) std::memset(counts_out, 0, size_t(width) * 4);
+        if (totals_out) *totals_out = ychg_totals{0, 0, with_hyperedges ? 0 : -1, 0};
+        return YCHG_OK;
+    }
+    if (c.plan_w != width || c.plan_h != height) {
+        ychg_plan_destroy(c.plan);
+        c.plan = nullptr;
+        c.plan_w = c.plan_h = -1;
+        if (const int rc = ychg_plan_create(device, width, width, height, &c.plan)) return rc;
+        c.plan_w = width;
+        c.plan_h = height;
+    }
+    const int64_t pitch = (row_bytes + 15) / 16 * 16;
+    if (const int rc = upload_image(c, bits, width, height, row_stride)) return rc;
+    if (const int rc = ensure_columns(c, width)) return rc;
     static const bool host_timing = [] {
         const char* v = getenv("YCHG_HOST_TIMING");
         return v && v[0] == '1';
@@ -682,5 +697,126 @@ extern "C" int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, in
         CK(cudaStreamSynchronize(c.stream));
     }
     if (n_out) *n_out = nb;
+    return YCHG_OK;
+}
+
+// ---------------------------------------------------------------------------- run materialisation
+namespace {
+
+// Uploads the image and runs profile phase 0 (counts, column offsets, run total).
+int profile_phase0(HostContext& c, const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                   int64_t* n_runs) {
+    if (const int rc = upload_image(c, bits, width, height, row_stride)) return rc;
+    if (const int rc = ensure_columns(c, width)) return rc;
+    const int64_t pitch = ((int64_t(width) + 7) / 8 + 15) / 16 * 16;
+    const int64_t bw = ychg_profile_band_words(width, height);
+    if (bw > c.band_cap) {
+        cudaFree(c.d_band);
+        c.d_band = nullptr;
+        c.band_cap = 0;
+        CK(cudaMalloc(&c.d_band, bw * 4));
+        c.band_cap = bw;
+    }
+    if (width > c.col_off_cap) {
+        cudaFree(c.d_col_off);
+        c.d_col_off = nullptr;
+        c.col_off_cap = 0;
+        CK(cudaMalloc(&c.d_col_off, int64_t(width) * 8));
+        c.col_off_cap = width;
+    }
+    const int rc = ychg_launch_profile(c.d_bits, pitch, width, height, c.d_band, c.d_counts, c.d_col_off,
+                                       &c.d_totals->total_runs, nullptr, 0, c.stream);
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "profile count kernels launch");
+    CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    *n_runs = c.h_totals->total_runs;
+    return YCHG_OK;
+}
+
+int profile_fill(HostContext& c, int32_t width, int32_t height, int64_t n_runs) {
+    if (n_runs > c.runs_cap) {
+        cudaFree(c.d_runs);
+        c.d_runs = nullptr;
+        c.runs_cap = 0;
+        CK(cudaMalloc(&c.d_runs, std::max<int64_t>(n_runs, 1) * 12));
+        c.runs_cap = n_runs;
+    }
+    const int64_t pitch = ((int64_t(width) + 7) / 8 + 15) / 16 * 16;
+    const int rc = ychg_launch_profile(c.d_bits, pitch, width, height, c.d_band, c.d_counts, c.d_col_off, nullptr,
+                                       c.d_runs, 1, c.stream);
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "profile fill kernel launch");
+    return YCHG_OK;
+}
+
+int check_profile_args(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride) {
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "profile: negative geometry %dx%d", width, height);
+    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
+        return fail(YCHG_ERR_INVALID, "profile: row_stride %lld < %lld", static_cast<long long>(row_stride),
+                    static_cast<long long>(row_bytes));
+    return YCHG_OK;
+}
+
+}  // namespace
+
+extern "C" int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                       int32_t strategy_kind, int32_t threads, int32_t* counts_out,
+                                       int32_t* runs_out, int64_t runs_capacity, int64_t* n_runs_out) {
+    // Same strategy validation as the scan (runscan.cpp:24-26); build_profile is strategy-independent.
+    if (strategy_kind != YCHG_STRATEGY_SERIAL && strategy_kind != YCHG_STRATEGY_PARALLEL)
+        return fail(YCHG_ERR_INVALID, "scan: unknown strategy kind %d", strategy_kind);
+    if (strategy_kind == YCHG_STRATEGY_PARALLEL && threads < 1)
+        return fail(YCHG_ERR_INVALID, "scan: parallel strategy needs threads >= 1, got %d", threads);
+    if (const int rc = check_profile_args(bits, width, height, row_stride)) return rc;
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+    if (width == 0 || height == 0) {
+        if (counts_out && width > 0) std::memset(counts_out, 0, size_t(width) * 4);
+        if (n_runs_out) *n_runs_out = 0;
+        return YCHG_OK;
+    }
+    int64_t n_runs = 0;
+    if (const int rc = profile_phase0(c, bits, width, height, row_stride, &n_runs)) return rc;
+    if (n_runs_out) *n_runs_out = n_runs;
+    if (counts_out) CK(cudaMemcpyAsync(counts_out, c.d_counts, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (runs_out && runs_capacity >= n_runs && n_runs > 0) {
+        if (const int rc = profile_fill(c, width, height, n_runs)) return rc;
+        CK(cudaMemcpyAsync(runs_out, c.d_runs, n_runs * 12, cudaMemcpyDeviceToHost, c.stream));
+    }
+    CK(cudaStreamSynchronize(c.stream));
+    return YCHG_OK;
+}
+
+extern "C" int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                     int32_t col, int32_t* runs_out, int64_t runs_capacity, int64_t* n_out) {
+    // runscan.cpp:105-107
+    if (col < 0 || col >= width)
+        return fail(YCHG_ERR_INVALID, "column_runs: column %d out of range [0, %d)", col, width);
+    if (const int rc = check_profile_args(bits, width, height, row_stride)) return rc;
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+    if (height == 0) {
+        if (n_out) *n_out = 0;
+        return YCHG_OK;
+    }
+    int64_t n_runs = 0;
+    if (const int rc = profile_phase0(c, bits, width, height, row_stride, &n_runs)) return rc;
+    int64_t off = 0;
+    int32_t cnt = 0;
+    CK(cudaMemcpyAsync(&off, c.d_col_off + col, 8, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&cnt, c.d_counts + col, 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (n_out) *n_out = cnt;
+    if (runs_out && runs_capacity >= cnt && cnt > 0) {
+        if (const int rc = profile_fill(c, width, height, n_runs)) return rc;
+        CK(cudaMemcpyAsync(runs_out, c.d_runs + 3 * off, int64_t(cnt) * 12, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+    }
     return YCHG_OK;
 }

@@ -25,6 +25,13 @@ int ychg_launch_synth(int pattern, int width, int height, int bands, int cell, d
 int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint8_t* d_dst, int64_t pitch, int y0, int y1,
                         cudaStream_t stream);
 
+// Run materialisation (ychg_profile.cu): phase 0 = band counts + column totals +
+// column offsets (+ run total); phase 1 = fill the flat [n][3] int32 run array.
+int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t width, int32_t height, uint32_t* d_band_counts,
+                        int32_t* d_counts, int64_t* d_col_off, int64_t* d_n_runs, int32_t* d_runs, int phase,
+                        cudaStream_t stream);
+int64_t ychg_profile_band_words(int32_t width, int32_t height);
+
 int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
                            int32_t* d_boundaries, long long* d_n, cudaStream_t stream);
 }

@@ -40,6 +40,47 @@ std::vector<int> cut_vertex_counts(const BinaryImage& image, ScanStrategy strate
     return counts;
 }
 
+std::vector<Run> column_runs(const BinaryImage& image, int col) {
+    std::int64_t n = 0;
+    check(ychg_column_runs_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), col,
+                                nullptr, 0, &n),
+          "column_runs");
+    std::vector<Run> runs(static_cast<std::size_t>(n));
+    if (n > 0)
+        check(ychg_column_runs_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), col,
+                                    reinterpret_cast<std::int32_t*>(runs.data()), n, &n),
+              "column_runs");
+    return runs;
+}
+
+ColumnProfile build_profile(const BinaryImage& image, ScanStrategy strategy) {
+    static_assert(sizeof(Run) == 3 * sizeof(std::int32_t), "Run must be three ints (C ABI run triples)");
+    const int kind = strategy.kind == ScanStrategy::Kind::serial ? YCHG_STRATEGY_SERIAL : YCHG_STRATEGY_PARALLEL;
+    ColumnProfile p;
+    p.width = image.width();
+    p.height = image.height();
+    p.counts.assign(static_cast<std::size_t>(image.width()), 0);
+    std::int64_t n = 0;
+    check(ychg_build_profile_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), kind,
+                                  strategy.threads, p.counts.data(), nullptr, 0, &n),
+          "build_profile");
+    std::vector<Run> flat(static_cast<std::size_t>(n));
+    if (n > 0)
+        check(ychg_build_profile_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), kind,
+                                      strategy.threads, p.counts.data(), reinterpret_cast<std::int32_t*>(flat.data()),
+                                      n, &n),
+              "build_profile");
+    p.runs.resize(static_cast<std::size_t>(image.width()));
+    std::size_t at = 0;
+    for (int c = 0; c < image.width(); ++c) {
+        const auto k = static_cast<std::size_t>(p.counts[static_cast<std::size_t>(c)]);
+        p.runs[static_cast<std::size_t>(c)].assign(flat.begin() + static_cast<std::ptrdiff_t>(at),
+                                                   flat.begin() + static_cast<std::ptrdiff_t>(at + k));
+        at += k;
+    }
+    return p;
+}
+
 std::vector<int> detect_boundary_columns(std::span<const int> counts) {
     std::vector<int> out(counts.size());
     std::int64_t n = 0;

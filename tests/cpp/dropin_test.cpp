@@ -104,6 +104,34 @@ int main() {
     CHECK(scan(BinaryImage(0, 0)).hyperedges == 0);
     CHECK(foreground_count(frame(5, 5)) == 16);
 
+    // test_runscan.cpp:17-33 (column_runs) and :116-123 (build_profile worked examples)
+    CHECK(column_runs(full(4, 4), 2) == (std::vector<Run>{{2, 0, 3}}));
+    CHECK(column_runs(frame(5, 5), 0) == (std::vector<Run>{{0, 0, 4}}));
+    CHECK(column_runs(frame(5, 5), 1) == (std::vector<Run>{{1, 0, 0}, {1, 4, 4}}));
+    CHECK(column_runs(frame(5, 5), 4) == (std::vector<Run>{{4, 0, 4}}));
+    CHECK(column_runs(BinaryImage(3, 3), 0).empty());
+    CHECK(column_runs(branch(), 0) == (std::vector<Run>{{0, 0, 1}, {0, 3, 6}}));
+    CHECK(column_runs(branch(), 1) == (std::vector<Run>{{1, 0, 4}, {1, 6, 6}}));
+    for (int bad : {4, -1}) {
+        bool t = false;
+        try {
+            column_runs(full(4, 4), bad);
+        } catch (const ValidationError&) {
+            t = true;
+        }
+        CHECK(t);
+    }
+    const ColumnProfile fp = build_profile(frame(5, 5), serial);
+    CHECK(fp.counts == (std::vector<int>{1, 2, 2, 2, 1}));
+    CHECK(fp.runs[0] == (std::vector<Run>{{0, 0, 4}}));
+    CHECK(fp.runs[2] == (std::vector<Run>{{2, 0, 0}, {2, 4, 4}}));
+    CHECK(fp.total_runs() == 8);
+    const ColumnProfile bp = build_profile(branch(), ScanStrategy::parallel(4));
+    CHECK(bp.counts == (std::vector<int>{2, 2}));
+    CHECK(bp.runs[0] == (std::vector<Run>{{0, 0, 1}, {0, 3, 6}}));
+    CHECK(bp.runs[1] == (std::vector<Run>{{1, 0, 4}, {1, 6, 6}}));
+    CHECK(build_profile(frame(5, 5), ScanStrategy::parallel(16)) == fp);
+
     std::printf("dropin_test: %d failure(s)\n", failures);
     return failures;
 }

@@ -244,3 +244,51 @@ def test_back_to_back_scans_pipelined(gpu, orc):
         assert tt[3] == bounds.size and np.array_equal(b.cpu().numpy()[: bounds.size], bounds), i
         assert tt[2] == he, i
     plan.close()
+
+
+def test_build_profile_known_answers(gpu):
+    y = gpu
+    fr = y.build_profile(y.synth("frame", 5, 5))
+    assert fr.counts.tolist() == [1, 2, 2, 2, 1]
+    assert fr.runs(0).tolist() == [[0, 0, 4]]
+    assert fr.runs(2).tolist() == [[2, 0, 0], [2, 4, 4]]
+    assert fr.total_runs() == 8
+    br = y.BinaryImage(2, 7, branch_example())
+    assert y.build_profile(br, y.ScanStrategy.parallel(4)).runs_flat.tolist() == [[0, 0, 1], [0, 3, 6], [1, 0, 4],
+                                                                                 [1, 6, 6]]
+    assert y.column_runs(br, 1).tolist() == [[1, 0, 4], [1, 6, 6]]
+    assert y.column_runs(y.BinaryImage(3, 3), 0).tolist() == []
+    with pytest.raises(y.ValidationError):
+        y.column_runs(y.synth("full", 4, 4), 4)
+    with pytest.raises(y.ValidationError):
+        y.column_runs(y.synth("full", 4, 4), -1)
+    with pytest.raises(y.ValidationError):
+        y.build_profile(br, y.ScanStrategy.parallel(0))
+
+
+def test_build_profile_golden_corpus(gpu, orc):
+    y = gpu
+    for row in corpus():
+        sp = spec_of(row["spec"])
+        bits = orc.synth(sp)
+        p = y.build_profile(y.BinaryImage(sp.width, sp.height, bits))
+        assert p.counts.tolist() == row["counts"], row["name"]
+        assert np.array_equal(p.runs_flat, orc.profile(bits, sp.width)), row["name"]
+
+
+def test_build_profile_invariants_and_large(gpu, orc):
+    # test_runscan.cpp:93-123: sorted, separated by background, conservation of pixels
+    y = gpu
+    for sp in [Spec.random(4096, 3000, 0.5, 99), Spec.random(1025, 700, 0.9, 3), Spec.hbands(5000, 600, 147),
+               Spec.checker(777, 513, 1), Spec.random(33, 2000, 0.3, 1)]:
+        bits = orc.synth(sp)
+        p = y.build_profile(y.BinaryImage(sp.width, sp.height, bits))
+        want = orc.profile(bits, sp.width)
+        assert np.array_equal(p.runs_flat, want), sp
+        r = p.runs_flat
+        assert (r[:, 1] <= r[:, 2]).all()
+        same = r[1:, 0] == r[:-1, 0]
+        assert (r[1:, 1][same] >= r[:-1, 2][same] + 2).all()
+        assert int((r[:, 2] - r[:, 1] + 1).sum()) == int(np.unpackbits(bits).sum())
+        for c in (0, sp.width // 2, sp.width - 1):
+            assert np.array_equal(y.column_runs(y.BinaryImage(sp.width, sp.height, bits), c), p.runs(c)), (sp, c)

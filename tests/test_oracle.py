@@ -110,3 +110,19 @@ def test_oracle_against_live_reference(orc, ref):
         c = img.counts(1, 4)
         assert np.array_equal(c, orc.counts(bits, w))
         assert img.hyperedges() == orc.hyperedges(bits, w)[0]
+
+
+def test_profile_restatement_matches_reference(orc, ref):
+    # build_profile (runscan.cpp:130-143) via the compiled reference vs the oracle restatement
+    for name, sp in full_corpus()[::5]:
+        bits = orc.synth(sp)
+        img = ref.image(bits, sp.width)
+        assert np.array_equal(orc.profile(bits, sp.width), img.profile(1, 4)), name
+
+
+def test_profile_known_answers(orc):
+    # test_runscan.cpp:17-33, 116-123
+    fr = orc.profile(orc.synth(Spec.frame(5, 5)), 5)
+    assert fr.tolist() == [[0, 0, 4], [1, 0, 0], [1, 4, 4], [2, 0, 0], [2, 4, 4], [3, 0, 0], [3, 4, 4], [4, 0, 4]]
+    br = orc.profile(branch_example(), 2)
+    assert br.tolist() == [[0, 0, 1], [0, 3, 6], [1, 0, 4], [1, 6, 6]]
