@@ -292,3 +292,17 @@ def test_build_profile_invariants_and_large(gpu, orc):
         assert int((r[:, 2] - r[:, 1] + 1).sum()) == int(np.unpackbits(bits).sum())
         for c in (0, sp.width // 2, sp.width - 1):
             assert np.array_equal(y.column_runs(y.BinaryImage(sp.width, sp.height, bits), c), p.runs(c)), (sp, c)
+
+
+def test_reference_acceptance_on_gpu_library(gpu):
+    """The reference's own acceptance suite (tests/acceptance.cpp), compiled from the
+    reference sources and headers with libychg.so linked in place of runscan.cpp
+    (oracle/Makefile `dropin`).  Criteria 4 and 6 assert CPU-thread scaling and are
+    reported, not required."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "acceptance_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/acceptance_dropin not built (needs /root/reference at build time)")
+    for crit in (1, 2, 3, 5, 7):
+        out = subprocess.run([exe, str(crit)], capture_output=True, text=True, timeout=600)
+        line = out.stdout.strip().splitlines()[0] if out.stdout.strip() else out.stderr
+        assert out.returncode == 0 and line.startswith("[PASS]"), line
