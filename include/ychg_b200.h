@@ -122,6 +122,28 @@ YCHG_API int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32_t
 YCHG_API int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
                                    int32_t col, int32_t* runs_out, int64_t runs_capacity, int64_t* n_out);
 
+/* Hyperedge decomposition (decompose, hypergraph.cpp:94-170) on the device.
+ * The result handle holds the reference Hypergraph's members as flat arrays:
+ *   edge_runs     n_runs int32 triples {col, y_top, y_bot}, grouped by hyperedge
+ *                 in canonical order, columns ascending inside an edge (all_runs());
+ *   edge_offsets  n_edges + 1 uint32 (edge i owns edge_runs[off[i] .. off[i+1]));
+ *   run_to_edge   n_runs uint32, hyperedge id of each run in profile order.
+ * ychg_decompose_image runs build_profile + decompose without leaving the GPU;
+ * ychg_decompose_profile takes a flattened ColumnProfile (list_sizes[c] runs of
+ * column list c, column-major) and validates it like validate_profile
+ * (hypergraph.cpp:62-90): YCHG_ERR_INVALID with the reference's message. */
+typedef struct ychg_hypergraph ychg_hypergraph;
+YCHG_API int ychg_decompose_image(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                  int32_t strategy_kind, int32_t threads, ychg_hypergraph** out);
+YCHG_API int ychg_decompose_profile(int32_t width, int32_t height, const int32_t* list_sizes, const int32_t* runs,
+                                    int64_t n_runs, ychg_hypergraph** out);
+/* n_runs, n_edges; device_ms = device time of the decomposition kernels (profile excluded). */
+YCHG_API int ychg_hypergraph_info(const ychg_hypergraph* hg, int64_t* n_runs, int64_t* n_edges, float* device_ms);
+/* Copies out any of the three arrays (NULL skips one). */
+YCHG_API int ychg_hypergraph_copy(const ychg_hypergraph* hg, int32_t* edge_runs, uint32_t* edge_offsets,
+                                  uint32_t* run_to_edge);
+YCHG_API void ychg_hypergraph_destroy(ychg_hypergraph* hg);
+
 /* ---- device-resident plans ----
  * A plan fixes the geometry and owns its device workspace.  width_img columns
  * are present in the buffer, width_cnt <= width_img are counted; columns

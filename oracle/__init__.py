@@ -32,6 +32,28 @@ PATTERN_IDS = {"full": FULL, "empty": EMPTY, "frame": FRAME, "hbands": HBANDS,
 _u8p = ctypes.POINTER(ctypes.c_uint8)
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _i64p = ctypes.POINTER(ctypes.c_int64)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+
+
+class Decomposition(tuple):
+    """decompose() as flat arrays: (edge_runs (n,3) int32 in hyperedge order,
+    edge_offsets (E+1,) uint32, run_to_edge (n,) uint32 in profile order) --
+    the members of the reference Hypergraph (hypergraph.hpp:68-71)."""
+
+    def __new__(cls, edge_runs, edge_offsets, run_to_edge):
+        return super().__new__(cls, (edge_runs, edge_offsets, run_to_edge))
+
+    @property
+    def edge_runs(self): return self[0]
+
+    @property
+    def edge_offsets(self): return self[1]
+
+    @property
+    def run_to_edge(self): return self[2]
+
+    @property
+    def edge_count(self) -> int: return len(self[1]) - 1
 
 
 def _ptr(a: np.ndarray, t):
@@ -89,6 +111,8 @@ class Oracle:
         L.yo_profile.restype = ctypes.c_int64
         L.yo_profile.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i32p, ctypes.c_int64, _i32p]
         L.yo_foreground_count.restype = ctypes.c_int64
+        L.yo_decompose.restype = ctypes.c_int64
+        L.yo_decompose.argtypes = [_i32p, _i32p, ctypes.c_int, _i32p, _u32p, _u32p]
         L.yo_foreground_count.argtypes = [_u8p, ctypes.c_int64]
         self.lib = L
 
@@ -142,6 +166,26 @@ class Oracle:
         self.lib.yo_profile(_ptr(bits, _u8p), w, h, bits.shape[1], _ptr(out, _i32p), n, None)
         return out[:n]
 
+    def decompose_profile(self, runs: np.ndarray, counts: np.ndarray) -> Decomposition:
+        """decompose (hypergraph.cpp:94-170) of a flat column-major profile."""
+        runs = np.ascontiguousarray(runs, dtype=np.int32).reshape(-1, 3)
+        counts = np.ascontiguousarray(counts, dtype=np.int32)
+        n = runs.shape[0]
+        er = np.zeros((max(n, 1), 3), dtype=np.int32)
+        eo = np.zeros(n + 1, dtype=np.uint32)
+        r2e = np.zeros(max(n, 1), dtype=np.uint32)
+        e = self.lib.yo_decompose(_ptr(runs, _i32p) if n else None, _ptr(counts, _i32p), len(counts),
+                                  _ptr(er, _i32p), _ptr(eo, _u32p), _ptr(r2e, _u32p))
+        if e < 0:
+            raise MemoryError("oracle decompose allocation failed")
+        return Decomposition(er[:n], eo[: e + 1], r2e[:n])
+
+    def decompose(self, bits: np.ndarray, w: int) -> Decomposition:
+        h = bits.shape[0]
+        runs = self.profile(bits, w)
+        counts = np.bincount(runs[:, 0], minlength=w).astype(np.int32) if len(runs) else np.zeros(w, np.int32)
+        return self.decompose_profile(runs, counts)
+
     def pair_links(self, bits: np.ndarray, w: int) -> np.ndarray:
         h = bits.shape[0]
         out = np.zeros(max(w - 1, 0), dtype=np.int32)
@@ -180,6 +224,8 @@ class Reference:
         L.yr_hyperedges.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.yr_profile.restype = ctypes.c_int64
         L.yr_profile.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _i32p, ctypes.c_int64]
+        L.yr_decompose.restype = ctypes.c_int64
+        L.yr_decompose.argtypes = [ctypes.c_void_p, _i32p, ctypes.c_int64, _u32p, ctypes.c_int64, _u32p, _i64p]
         L.yr_time_path.restype = ctypes.c_int
         L.yr_time_path.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, _i64p, _i32p, _i64p, _i64p]
@@ -259,6 +305,20 @@ class RefImage:
         if v < 0:
             raise RuntimeError(self.ref.last_error())
         return int(v)
+
+    def decompose(self) -> Decomposition:
+        """decompose(build_profile(img)) by the reference (hypergraph.cpp:94-170)."""
+        n = ctypes.c_int64(0)
+        e = self.ref.lib.yr_decompose(self.handle, None, 0, None, 0, None, ctypes.byref(n))
+        if e < 0:
+            raise RuntimeError(self.ref.last_error())
+        nr = n.value
+        er = np.zeros((max(nr, 1), 3), dtype=np.int32)
+        eo = np.zeros(e + 1, dtype=np.uint32)
+        r2e = np.zeros(max(nr, 1), dtype=np.uint32)
+        self.ref.lib.yr_decompose(self.handle, _ptr(er, _i32p), nr, _ptr(eo, _u32p), e + 1, _ptr(r2e, _u32p),
+                                  ctypes.byref(n))
+        return Decomposition(er[:nr], eo, r2e[:nr])
 
     def time_path(self, kind: int, threads: int, warmup: int, reps: int,
                   with_hyperedges: bool) -> dict:

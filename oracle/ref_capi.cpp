@@ -146,6 +146,40 @@ YR_EXPORT int64_t yr_profile(void* img, int kind, int threads, int32_t* runs, in
     }
 }
 
+// decompose(build_profile(img)) (hypergraph.cpp:94-170) exported as flat arrays:
+// edge_runs = all_runs() triples, edge_offsets[0..E], run_to_edge() (profile
+// order).  Returns E (or a negative error code); *n_runs_out gets the run total.
+// Outputs are written only if the capacities suffice.
+YR_EXPORT int64_t yr_decompose(void* img, int32_t* edge_runs, int64_t runs_cap, uint32_t* edge_offsets,
+                               int64_t edges_cap, uint32_t* run_to_edge, int64_t* n_runs_out) {
+    try {
+        const auto hg = ychg::decompose(ychg::build_profile(*static_cast<ychg::BinaryImage*>(img),
+                                                            ychg::ScanStrategy::serial()));
+        const auto all = hg.all_runs();
+        const int64_t n = static_cast<int64_t>(all.size());
+        const int64_t e = static_cast<int64_t>(hg.edge_count());
+        if (n_runs_out) *n_runs_out = n;
+        if (edge_runs && runs_cap >= n)
+            for (int64_t i = 0; i < n; ++i) {
+                edge_runs[3 * i] = all[i].col;
+                edge_runs[3 * i + 1] = all[i].y_top;
+                edge_runs[3 * i + 2] = all[i].y_bot;
+            }
+        if (edge_offsets && edges_cap >= e + 1) {
+            edge_offsets[0] = 0;
+            for (int64_t i = 0; i < e; ++i)
+                edge_offsets[i + 1] = edge_offsets[i] + static_cast<uint32_t>(hg.edge(i).runs.size());
+        }
+        if (run_to_edge && runs_cap >= n) {
+            const auto r2e = hg.run_to_edge();
+            std::memcpy(run_to_edge, r2e.data(), r2e.size() * 4);
+        }
+        return e;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
 // The reference's full hot path (counts + boundaries + hyperedge total), timed
 // with the reference protocol (bench.cpp:37-57: warmup untimed, reps timed with
 // steady_clock).  with_hyperedges=0 times counts + boundaries only.

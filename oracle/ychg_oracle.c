@@ -272,3 +272,62 @@ YO_EXPORT int64_t yo_profile(const uint8_t* bits, int w, int h, int64_t stride, 
     }
     return n;
 }
+
+/* ---------------------------------------------------------------- decompose
+ * decompose(const ColumnProfile&) (hypergraph.cpp:94-170) restated on the flat
+ * profile (column-major {col, y_top, y_bot} triples, counts[c] runs per column):
+ *   1. per adjacent column pair, the two-pointer overlap sweep (:108-135) marks a
+ *      link r -> s iff each run is the other's only vertical overlap (:136-143);
+ *   2. chains are walked from every run without a left link, in profile order
+ *      (:145-167), which is the canonical hyperedge numbering.
+ * Outputs: edge_runs (triples, hyperedge order, columns ascending inside an edge),
+ * edge_offsets[0..E] and run_to_edge[profile index] (the Hypergraph members,
+ * hypergraph.hpp:68-71; run_to_edge as the constructor derives it, :19-55).
+ * Returns E, or -1 on allocation failure. */
+YO_EXPORT int64_t yo_decompose(const int32_t* runs, const int32_t* counts, int w, int32_t* edge_runs,
+                               uint32_t* edge_offsets, uint32_t* run_to_edge) {
+    int64_t n = 0;
+    for (int c = 0; c < w; ++c) n += counts[c];
+    int64_t* off = malloc(sizeof(int64_t) * ((size_t)w + 1));
+    uint32_t* right = malloc(sizeof(uint32_t) * ((size_t)n + 1));
+    uint8_t* has_left = calloc((size_t)n + 1, 1);
+    size_t cap = 1;
+    for (int c = 0; c < w; ++c) if ((size_t)counts[c] > cap) cap = (size_t)counts[c];
+    uint32_t* scratch = malloc(sizeof(uint32_t) * cap * 4);
+    yo_run* ra = malloc(sizeof(yo_run) * cap);
+    yo_run* rb = malloc(sizeof(yo_run) * cap);
+    if (!off || !right || !has_left || !scratch || !ra || !rb) {
+        free(off); free(right); free(has_left); free(scratch); free(ra); free(rb);
+        return -1;
+    }
+    off[0] = 0;
+    for (int c = 0; c < w; ++c) off[c + 1] = off[c] + counts[c];
+    for (int64_t g = 0; g < n; ++g) right[g] = UINT32_MAX;
+    for (int c = 0; c + 1 < w; ++c) {
+        const int64_t na = counts[c], nb = counts[c + 1];
+        if (na == 0 || nb == 0) continue;
+        for (int64_t i = 0; i < na; ++i) { ra[i].top = runs[3 * (off[c] + i) + 1]; ra[i].bot = runs[3 * (off[c] + i) + 2]; }
+        for (int64_t j = 0; j < nb; ++j) { rb[j].top = runs[3 * (off[c + 1] + j) + 1]; rb[j].bot = runs[3 * (off[c + 1] + j) + 2]; }
+        uint32_t *ov_a = scratch, *pa = scratch + cap, *ov_b = scratch + 2 * cap, *pb = scratch + 3 * cap;
+        yo_pair_links(ra, na, rb, nb, ov_a, pa, ov_b, pb);
+        for (int64_t i = 0; i < na; ++i)
+            if (ov_a[i] == 1 && ov_b[pa[i]] == 1) {
+                right[off[c] + i] = (uint32_t)(off[c + 1] + pa[i]);
+                has_left[off[c + 1] + pa[i]] = 1;
+            }
+    }
+    int64_t e = 0, pos = 0;
+    edge_offsets[0] = 0;
+    for (int64_t g = 0; g < n; ++g) {
+        if (has_left[g]) continue;
+        for (int64_t cur = g;; cur = right[cur]) {
+            memcpy(edge_runs + 3 * pos, runs + 3 * cur, 12);
+            run_to_edge[cur] = (uint32_t)e;
+            ++pos;
+            if (right[cur] == UINT32_MAX) break;
+        }
+        edge_offsets[++e] = (uint32_t)pos;
+    }
+    free(off); free(right); free(has_left); free(scratch); free(ra); free(rb);
+    return e;
+}

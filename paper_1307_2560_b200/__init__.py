@@ -60,6 +60,12 @@ _SIGS = {
     "ychg_scan_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, ctypes.POINTER(Totals)]),
     "ychg_build_profile_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64)]),
     "ychg_column_runs_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
+    "ychg_decompose_image": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_vp)]),
+    "ychg_decompose_profile": (ctypes.c_int, [_i32, _i32, _vp, _vp, _i64, ctypes.POINTER(_vp)]),
+    "ychg_hypergraph_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                            ctypes.POINTER(ctypes.c_float)]),
+    "ychg_hypergraph_copy": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "ychg_hypergraph_destroy": (None, [_vp]),
     "ychg_plan_create": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "ychg_plan_destroy": (None, [_vp]),
     "ychg_plan_get_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
@@ -269,6 +275,69 @@ def column_runs(image: BinaryImage, col: int) -> np.ndarray:
     return out[: n.value].copy()
 
 
+class Hypergraph:
+    """decompose's result (hypergraph.hpp:27-71) as flat arrays: `edge_runs` (n, 3)
+    int32 grouped by hyperedge in canonical order, `edge_offsets` (E+1,) uint32,
+    `run_to_edge` (n,) uint32 in profile order.  `device_ms` is the device time of
+    the decomposition kernels."""
+
+    def __init__(self, width: int, height: int, edge_runs: np.ndarray, edge_offsets: np.ndarray,
+                 run_to_edge: np.ndarray, device_ms: float = 0.0):
+        self.width, self.height = width, height
+        self.edge_runs, self.edge_offsets, self.run_to_edge = edge_runs, edge_offsets, run_to_edge
+        self.device_ms = device_ms
+
+    @property
+    def edge_count(self) -> int:
+        return len(self.edge_offsets) - 1
+
+    def edge(self, i: int) -> np.ndarray:
+        """Runs of hyperedge i (HyperedgeView::runs)."""
+        return self.edge_runs[self.edge_offsets[i]:self.edge_offsets[i + 1]]
+
+    def all_runs(self) -> np.ndarray:
+        return self.edge_runs
+
+    def __eq__(self, other) -> bool:  # Hypergraph::operator== (hypergraph.hpp:62-65)
+        return (self.width == other.width and self.height == other.height
+                and np.array_equal(self.edge_runs, other.edge_runs)
+                and np.array_equal(self.edge_offsets, other.edge_offsets))
+
+
+def _take_hypergraph(h: ctypes.c_void_p, width: int, height: int) -> Hypergraph:
+    try:
+        n, e, ms = _i64(0), _i64(0), ctypes.c_float(0)
+        _check(_lib.ychg_hypergraph_info(h, ctypes.byref(n), ctypes.byref(e), ctypes.byref(ms)), "decompose")
+        er = np.zeros((max(n.value, 1), 3), dtype=np.int32)
+        eo = np.zeros(e.value + 1, dtype=np.uint32)
+        r2e = np.zeros(max(n.value, 1), dtype=np.uint32)
+        _check(_lib.ychg_hypergraph_copy(h, er.ctypes.data_as(_vp), eo.ctypes.data_as(_vp), r2e.ctypes.data_as(_vp)),
+               "decompose")
+        return Hypergraph(width, height, er[: n.value], eo, r2e[: n.value], float(ms.value))
+    finally:
+        _lib.ychg_hypergraph_destroy(h)
+
+
+def decompose(source, strategy: ScanStrategy = ScanStrategy.serial()) -> Hypergraph:
+    """decompose (hypergraph.cpp:94-170) on the GPU.  `source` is a ColumnProfile
+    (validated like validate_profile, :62-90) or a BinaryImage (build_profile +
+    decompose without leaving the device)."""
+    h = _vp()
+    if isinstance(source, BinaryImage):
+        _check(_lib.ychg_decompose_image(source._ptr(), source.width, source.height, source.row_stride,
+                                         strategy.kind, strategy.threads, ctypes.byref(h)), "decompose")
+        return _take_hypergraph(h, source.width, source.height)
+    prof = source
+    runs = np.ascontiguousarray(prof.runs_flat, dtype=np.int32).reshape(-1, 3)
+    sizes = np.ascontiguousarray(prof.counts, dtype=np.int32)
+    if prof.width >= 0 and sizes.shape[0] != prof.width:
+        raise ValidationError(f"decompose: profile arrays do not match width {prof.width}")
+    _check(_lib.ychg_decompose_profile(prof.width, prof.height, sizes.ctypes.data_as(_vp) if sizes.size else None,
+                                       runs.ctypes.data_as(_vp) if runs.size else None, runs.shape[0],
+                                       ctypes.byref(h)), "decompose")
+    return _take_hypergraph(h, prof.width, prof.height)
+
+
 # ---------------------------------------------------------------- device-resident plumbing
 class Plan:
     """Geometry-specific launch plan + workspace on one device (ychg_plan_*)."""
@@ -383,6 +452,7 @@ def synth(pattern: str, width: int, height: int, *, bands: int = 0, cell: int = 
 
 __all__ = [
     "BinaryImage", "ScanStrategy", "ScanResult", "ColumnProfile", "build_profile", "column_runs", "Error",
+    "Hypergraph", "decompose",
     "ValidationError", "cut_vertex_counts",
     "detect_boundary_columns", "scan", "hyperedge_count", "Plan", "DeviceBuffer", "synth", "synth_device",
     "pitch_for", "device_count", "Totals", "PlanInfo", "LIB_PATH", "CXX_LIB_PATH", "EXPORTED_SYMBOLS",

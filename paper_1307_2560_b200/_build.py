@@ -22,7 +22,7 @@ CUDA_SO = os.path.join(PKG, "libychg_b200.so")
 CXX_SO = os.path.join(PKG, "libychg.so")
 
 NVCC_ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SRCS = ["ychg_scan.cu", "ychg_aux.cu", "ychg_profile.cu", "ychg_capi.cu"]
+CU_SRCS = ["ychg_scan.cu", "ychg_aux.cu", "ychg_profile.cu", "ychg_decompose.cu", "ychg_capi.cu"]
 CU_DEPS = CU_SRCS + ["ychg_device.cuh", "ychg_kernels.h"]
 
 

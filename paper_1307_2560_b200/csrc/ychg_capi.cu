@@ -163,6 +163,11 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
     p.n_blocks = (height + ychg_dev::kBlockRows - 1) / ychg_dev::kBlockRows;
     if (p.n_strips > 0 && p.n_blocks > 0) {
         p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid);
+        // experiment hooks (benchmarking only): force the segments per strip / grid
+        if (const char* v = getenv("YCHG_SEGMENTS"); v && *v) {
+            p.seg_per_strip = std::max(1, atoi(v));
+            plan->grid = static_cast<int>(std::min<long long>(2LL * sms, 1LL * p.n_strips * p.seg_per_strip));
+        }
         p.n_segments = p.n_strips * p.seg_per_strip;
         if (p.seg_per_strip > ychg_dev::kMaxSegPerStrip)
             return fail(YCHG_ERR_INVALID, "plan_create: height %d needs more than %d row segments per strip",
@@ -462,6 +467,19 @@ struct HostContext {
     bool h2d_timing = false;
     cudaEvent_t h2d_ev[3] = {nullptr, nullptr, nullptr};
     int64_t h_out_cap = 0;
+    // hyperedge decomposition
+    void* d_dws = nullptr;
+    int64_t dws_cap = 0;
+    int32_t* d_eruns = nullptr;
+    int64_t eruns_cap = 0;
+    uint32_t* d_eoff = nullptr;
+    int64_t eoff_cap = 0;
+    uint32_t* d_r2e = nullptr;
+    int64_t r2e_cap = 0;
+    unsigned long long* d_dscal = nullptr;  // [0] edge/run totals, [1] validation error
+    unsigned long long* h_dscal = nullptr;  // pinned
+    int* h_flag = nullptr;                  // pinned: jump-round change flag
+    cudaEvent_t dec_ev[2] = {nullptr, nullptr};
 };
 
 HostContext& host_context(int device) {
@@ -820,3 +838,192 @@ extern "C" int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t
     }
     return YCHG_OK;
 }
+
+// ---------------------------------------------------------------------------- hyperedge decomposition
+struct ychg_hypergraph {
+    int32_t width = 0, height = 0;
+    int64_t n_runs = 0, n_edges = 0;
+    float device_ms = 0.f;
+    std::vector<int32_t> edge_runs;
+    std::vector<uint32_t> edge_offsets{0};
+    std::vector<uint32_t> run_to_edge;
+};
+
+namespace {
+
+template <typename T>
+int ensure_buf(T** p, int64_t* cap, int64_t elems) {
+    if (elems <= *cap) return YCHG_OK;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<int64_t>(elems, 1) * int64_t(sizeof(T))));
+    *cap = elems;
+    return YCHG_OK;
+}
+
+int ensure_decompose(HostContext& c, int64_t n) {
+    if (!c.h_flag) {
+        CK(cudaMallocHost(&c.h_flag, 16));
+        CK(cudaMallocHost(&c.h_dscal, 16));
+        CK(cudaMalloc(&c.d_dscal, 16));
+        CK(cudaEventCreate(&c.dec_ev[0]));
+        CK(cudaEventCreate(&c.dec_ev[1]));
+    }
+    const int64_t ws = ychg_decompose_ws_bytes(n);
+    if (ws > c.dws_cap) {
+        cudaFree(c.d_dws);
+        c.d_dws = nullptr;
+        c.dws_cap = 0;
+        CK(cudaMalloc(&c.d_dws, ws));
+        c.dws_cap = ws;
+    }
+    if (const int rc = ensure_buf(&c.d_eruns, &c.eruns_cap, 3 * n)) return rc;
+    if (const int rc = ensure_buf(&c.d_eoff, &c.eoff_cap, n + 1)) return rc;
+    return ensure_buf(&c.d_r2e, &c.r2e_cap, n);
+}
+
+// Decompose the n-run profile in c.d_runs / c.d_col_off / c.d_counts into hg.
+int decompose_device_profile(HostContext& c, int32_t width, int64_t n, ychg_hypergraph* hg) {
+    if (n > int64_t(0xFFFFFFFEu))
+        return fail(YCHG_ERR_INVALID, "decompose: %lld runs exceed the 32-bit run index of Hypergraph",
+                    static_cast<long long>(n));
+    if (const int rc = ensure_decompose(c, n)) return rc;
+    CK(cudaEventRecord(c.dec_ev[0], c.stream));
+    const int rounds = ychg_launch_decompose(c.d_runs, c.d_col_off, c.d_counts, width, n, c.d_dws, c.d_eruns,
+                                             c.d_eoff, c.d_r2e, c.d_dscal, c.h_flag, c.stream);
+    if (rounds < 0) return cuda_fail(static_cast<cudaError_t>(-rounds), "decompose kernels");
+    CK(cudaEventRecord(c.dec_ev[1], c.stream));
+    CK(cudaMemcpyAsync(c.h_dscal, c.d_dscal, 8, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    CK(cudaEventElapsedTime(&hg->device_ms, c.dec_ev[0], c.dec_ev[1]));
+    const unsigned long long tot = c.h_dscal[0];
+    hg->n_runs = n;
+    hg->n_edges = static_cast<int64_t>(tot >> 32);
+    if (static_cast<int64_t>(tot & 0xFFFFFFFFull) != n)
+        return fail(YCHG_ERR_INTERNAL, "decompose: chains cover %llu of %lld runs", tot & 0xFFFFFFFFull,
+                    static_cast<long long>(n));
+    hg->edge_runs.resize(size_t(3 * n));
+    hg->edge_offsets.resize(size_t(hg->n_edges + 1));
+    hg->run_to_edge.resize(size_t(n));
+    CK(cudaMemcpyAsync(hg->edge_runs.data(), c.d_eruns, n * 12, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(hg->edge_offsets.data(), c.d_eoff, (hg->n_edges + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(hg->run_to_edge.data(), c.d_r2e, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return YCHG_OK;
+}
+
+}  // namespace
+
+extern "C" int ychg_decompose_image(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                    int32_t strategy_kind, int32_t threads, ychg_hypergraph** out) {
+    if (!out) return fail(YCHG_ERR_INVALID, "decompose: null result pointer");
+    *out = nullptr;
+    if (strategy_kind != YCHG_STRATEGY_SERIAL && strategy_kind != YCHG_STRATEGY_PARALLEL)
+        return fail(YCHG_ERR_INVALID, "scan: unknown strategy kind %d", strategy_kind);
+    if (strategy_kind == YCHG_STRATEGY_PARALLEL && threads < 1)
+        return fail(YCHG_ERR_INVALID, "scan: parallel strategy needs threads >= 1, got %d", threads);
+    if (const int rc = check_profile_args(bits, width, height, row_stride)) return rc;
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    std::unique_ptr<ychg_hypergraph> hg(new ychg_hypergraph);
+    hg->width = width;
+    hg->height = height;
+    if (width > 0 && height > 0) {
+        HostContext& c = host_context(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        if (const int rc = ensure_context(c)) return rc;
+        int64_t n_runs = 0;
+        if (const int rc = profile_phase0(c, bits, width, height, row_stride, &n_runs)) return rc;
+        if (n_runs > 0) {
+            if (const int rc = profile_fill(c, width, height, n_runs)) return rc;
+            if (const int rc = decompose_device_profile(c, width, n_runs, hg.get())) return rc;
+        }
+    }
+    *out = hg.release();
+    return YCHG_OK;
+}
+
+extern "C" int ychg_decompose_profile(int32_t width, int32_t height, const int32_t* list_sizes, const int32_t* runs,
+                                      int64_t n_runs, ychg_hypergraph** out) {
+    if (!out) return fail(YCHG_ERR_INVALID, "decompose: null result pointer");
+    *out = nullptr;
+    // validate_profile (hypergraph.cpp:62-66)
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "decompose: profile has negative geometry");
+    int64_t total = 0;
+    for (int32_t c = 0; c < width; ++c) {
+        if (list_sizes[c] < 0) return fail(YCHG_ERR_INVALID, "decompose: negative run count in column %d", c);
+        total += list_sizes[c];
+    }
+    if (total != n_runs)
+        return fail(YCHG_ERR_INVALID, "decompose: list sizes sum to %lld, not %lld runs",
+                    static_cast<long long>(total), static_cast<long long>(n_runs));
+    if (n_runs > 0 && !runs) return fail(YCHG_ERR_INVALID, "decompose: null runs");
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    std::unique_ptr<ychg_hypergraph> hg(new ychg_hypergraph);
+    hg->width = width;
+    hg->height = height;
+    if (n_runs > 0) {
+        HostContext& c = host_context(device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        if (const int rc = ensure_context(c)) return rc;
+        if (const int rc = ensure_columns(c, width)) return rc;
+        if (const int rc = ensure_buf(&c.d_col_off, &c.col_off_cap, int64_t(width))) return rc;
+        if (n_runs > c.runs_cap) {  // capacity counted in runs (12 B each), as in profile_fill
+            cudaFree(c.d_runs);
+            c.d_runs = nullptr;
+            c.runs_cap = 0;
+            CK(cudaMalloc(&c.d_runs, n_runs * 12));
+            c.runs_cap = n_runs;
+        }
+        std::vector<int64_t> off(size_t(width) + 1, 0);
+        for (int32_t k = 0; k < width; ++k) off[size_t(k) + 1] = off[size_t(k)] + list_sizes[k];
+        CK(cudaMemcpyAsync(c.d_runs, runs, n_runs * 12, cudaMemcpyHostToDevice, c.stream));
+        CK(cudaMemcpyAsync(c.d_counts, list_sizes, int64_t(width) * 4, cudaMemcpyHostToDevice, c.stream));
+        CK(cudaMemcpyAsync(c.d_col_off, off.data(), int64_t(width) * 8, cudaMemcpyHostToDevice, c.stream));
+        if (const int rc = ensure_decompose(c, n_runs)) return rc;
+        const int rv = ychg_launch_decompose_validate(c.d_runs, c.d_col_off, width, height, n_runs, c.d_dscal + 1,
+                                                      c.stream);
+        if (rv != 0) return cuda_fail(static_cast<cudaError_t>(rv), "decompose validation");
+        CK(cudaMemcpyAsync(c.h_dscal + 1, c.d_dscal + 1, 8, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        const unsigned long long err = c.h_dscal[1];
+        if (err != ~0ull) {
+            // the reference's messages (hypergraph.cpp:74-86)
+            const int64_t g = static_cast<int64_t>(err >> 2);
+            const int kind = static_cast<int>(err & 3ull);
+            const int list = static_cast<int>(std::upper_bound(off.begin(), off.end(), g) - off.begin()) - 1;
+            const int32_t* r = runs + 3 * g;
+            if (kind == 1)
+                return fail(YCHG_ERR_INVALID, "decompose: run in column list %d claims column %d", list, r[0]);
+            if (kind == 2)
+                return fail(YCHG_ERR_INVALID, "decompose: run [%d,%d] in column %d outside height %d", r[1], r[2],
+                            list, height);
+            return fail(YCHG_ERR_INVALID, "decompose: runs in column %d must be sorted and separated by background",
+                        list);
+        }
+        if (const int rc = decompose_device_profile(c, width, n_runs, hg.get())) return rc;
+    }
+    *out = hg.release();
+    return YCHG_OK;
+}
+
+extern "C" int ychg_hypergraph_info(const ychg_hypergraph* hg, int64_t* n_runs, int64_t* n_edges, float* device_ms) {
+    if (!hg) return fail(YCHG_ERR_INVALID, "hypergraph: null handle");
+    if (n_runs) *n_runs = hg->n_runs;
+    if (n_edges) *n_edges = hg->n_edges;
+    if (device_ms) *device_ms = hg->device_ms;
+    return YCHG_OK;
+}
+
+extern "C" int ychg_hypergraph_copy(const ychg_hypergraph* hg, int32_t* edge_runs, uint32_t* edge_offsets,
+                                    uint32_t* run_to_edge) {
+    if (!hg) return fail(YCHG_ERR_INVALID, "hypergraph: null handle");
+    if (edge_runs && hg->n_runs) std::memcpy(edge_runs, hg->edge_runs.data(), size_t(hg->n_runs) * 12);
+    if (edge_offsets) std::memcpy(edge_offsets, hg->edge_offsets.data(), size_t(hg->n_edges + 1) * 4);
+    if (run_to_edge && hg->n_runs) std::memcpy(run_to_edge, hg->run_to_edge.data(), size_t(hg->n_runs) * 4);
+    return YCHG_OK;
+}
+
+extern "C" void ychg_hypergraph_destroy(ychg_hypergraph* hg) { delete hg; }

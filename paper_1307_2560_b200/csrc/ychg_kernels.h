@@ -32,6 +32,14 @@ int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t width, int
                         cudaStream_t stream);
 int64_t ychg_profile_band_words(int32_t width, int32_t height);
 
+// Hyperedge decomposition (ychg_decompose.cu).
+int64_t ychg_decompose_ws_bytes(int64_t n);
+int ychg_launch_decompose_validate(const int32_t* d_runs, const int64_t* d_col_off, int32_t width, int32_t height,
+                                   int64_t n, unsigned long long* d_err, cudaStream_t stream);
+int ychg_launch_decompose(const int32_t* d_runs, const int64_t* d_col_off, const int32_t* d_counts, int32_t width,
+                          int64_t n, void* d_ws, int32_t* d_edge_runs, uint32_t* d_edge_offsets,
+                          uint32_t* d_run_to_edge, unsigned long long* d_total, int* h_flag, cudaStream_t stream);
+
 int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
                            int32_t* d_boundaries, long long* d_n, cudaStream_t stream);
 }

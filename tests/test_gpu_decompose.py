@@ -1,0 +1,116 @@
+"""GPU parity of the device decomposition: decompose
+(hypergraph.cpp:94-170) through the C ABI, bit-exact against the reference's own
+known answers (test_hypergraph.cpp), the golden digests of the unmodified
+reference (tests/golden/decompose_ref.json.gz) and the oracle restatement."""
+import numpy as np
+import pytest
+
+from golden_io import decompose as golden_decompose
+from golden_io import decomposition_digest, spec_of
+from oracle import Decomposition, Spec, branch_example
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_decompose(y, orc, sp):
+    return y.decompose(y.BinaryImage(sp.width, sp.height, orc.synth(sp)))
+
+
+def as_tuple(hg):
+    return Decomposition(hg.edge_runs, hg.edge_offsets, hg.run_to_edge)
+
+
+def test_decompose_known_answers(gpu):
+    y = gpu
+    # test_hypergraph.cpp:24-35 full image -> one edge
+    hg = y.decompose(y.synth("full", 4, 4))
+    assert hg.edge_count == 1 and hg.edge(0).tolist() == [[0, 0, 3], [1, 0, 3], [2, 0, 3], [3, 0, 3]]
+    # :37-57 frame
+    hg = y.decompose(y.synth("frame", 5, 5))
+    assert hg.edge_offsets.tolist() == [0, 1, 4, 7, 8]
+    assert hg.edge(1).tolist() == [[1, 0, 0], [2, 0, 0], [3, 0, 0]]
+    assert hg.edge(2).tolist() == [[1, 4, 4], [2, 4, 4], [3, 4, 4]]
+    assert hg.run_to_edge.tolist() == [0, 1, 2, 1, 2, 1, 2, 3]
+    # :59-73 branch example: four single-run edges
+    hg = y.decompose(y.BinaryImage(2, 7, branch_example()))
+    assert hg.edge_runs.tolist() == [[0, 0, 1], [0, 3, 6], [1, 0, 4], [1, 6, 6]]
+    assert hg.edge_offsets.tolist() == [0, 1, 2, 3, 4]
+    # :75-88 pattern counts, empty images
+    for k in (1, 3, 7):
+        assert y.decompose(y.synth("hbands", 20, 20, bands=k)).edge_count == k
+    assert y.decompose(y.synth("checker", 8, 8, cell=1)).edge_count == 32
+    assert y.decompose(y.synth("empty", 3, 3)).edge_count == 0
+    assert y.decompose(y.BinaryImage(0, 0)).edge_count == 0
+
+
+def test_decompose_golden_reference_digests(gpu, orc):
+    # every corpus image and the large images, digests of the reference's own output
+    y = gpu
+    for row in golden_decompose():
+        sp = spec_of(row["spec"])
+        got = decomposition_digest(as_tuple(gpu_decompose(y, orc, sp)))
+        assert got == {k: row[k] for k in got}, (row["name"], row["spec"])
+
+
+def test_decompose_random_geometries_vs_oracle(gpu, orc):
+    y = gpu
+    rng = np.random.default_rng(2024)
+    for _ in range(80):
+        w, h = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        sp = Spec.random(w, h, float(rng.choice([0.05, 0.3, 0.5, 0.7, 0.95])), int(rng.integers(0, 1 << 62)))
+        want = orc.decompose(orc.synth(sp), w)
+        got = gpu_decompose(y, orc, sp)
+        for a, b in zip(as_tuple(got), want):
+            assert np.array_equal(a, b), sp
+
+
+@pytest.mark.parametrize("sp", [Spec.hbands(21000, 600, 147), Spec.checker(3000, 3000, 1),
+                                Spec.random(6000, 5000, 0.5, 1307), Spec.full(70000, 3), Spec.frame(3, 70000)],
+                         ids=["long-chains", "checker1", "random", "one-wide-chain", "tall"])
+def test_decompose_large_vs_oracle(gpu, orc, sp):
+    y = gpu
+    bits = orc.synth(sp)
+    want = orc.decompose(bits, sp.width)
+    got = y.decompose(y.BinaryImage(sp.width, sp.height, bits))
+    for a, b in zip(as_tuple(got), want):
+        assert np.array_equal(a, b)
+    assert got.edge_count == orc.hyperedges(bits, sp.width)[0]
+
+
+def test_decompose_profile_input_and_validation(gpu, orc):
+    y = gpu
+    sp = Spec.random(97, 61, 0.4, 5)
+    img = y.BinaryImage(sp.width, sp.height, orc.synth(sp))
+    prof = y.build_profile(img)
+    assert y.decompose(prof) == y.decompose(img)
+    assert np.array_equal(y.decompose(prof).run_to_edge, y.decompose(img).run_to_edge)
+
+    def bad(mutate, msg):
+        runs = prof.runs_flat.copy()
+        mutate(runs)
+        with pytest.raises(y.ValidationError, match=msg):
+            y.decompose(y.ColumnProfile(prof.width, prof.height, prof.counts.copy(), runs))
+
+    # hypergraph.cpp:74-86 messages; the first failing run in profile order wins
+    c0 = int(np.argmax(prof.counts > 1))
+    o = int(prof.col_off[c0])
+    bad(lambda r: r.__setitem__((o, 0), c0 + 1), f"run in column list {c0} claims column {c0 + 1}")
+    bad(lambda r: r.__setitem__((o, 2), sp.height), f"outside height {sp.height}")
+    bad(lambda r: r.__setitem__((o + 1, 1), int(r[o, 2]) + 1), f"runs in column {c0} must be sorted")
+    with pytest.raises(y.ValidationError):
+        y.decompose(y.ColumnProfile(-1, 3, np.zeros(0, np.int32), np.zeros((0, 3), np.int32)))
+    with pytest.raises(y.ValidationError):
+        y.decompose(y.ColumnProfile(3, 3, np.zeros(2, np.int32), np.zeros((0, 3), np.int32)))
+    # an empty profile is fine
+    assert y.decompose(y.ColumnProfile(4, 4, np.zeros(4, np.int32), np.zeros((0, 3), np.int32))).edge_count == 0
+
+
+def test_decompose_live_reference(gpu, orc, ref):
+    # when oracle/_ref travelled with the repo: the unmodified reference itself
+    y = gpu
+    for sp in [Spec.checker(2049, 1500, 7), Spec.random(1500, 1700, 0.6, 77), Spec.hbands(4000, 4000, 147)]:
+        bits = orc.synth(sp)
+        want = ref.image(bits, sp.width).decompose()
+        got = y.decompose(y.BinaryImage(sp.width, sp.height, bits))
+        for a, b in zip(as_tuple(got), want):
+            assert np.array_equal(a, b)

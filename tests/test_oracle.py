@@ -5,7 +5,7 @@ import hashlib
 import numpy as np
 import pytest
 
-from golden_io import acceptance2, corpus, large, spec_of
+from golden_io import acceptance2, corpus, decompose, decomposition_digest, large, spec_of
 from oracle import Spec, a7_links, branch_example, full_corpus
 
 
@@ -126,3 +126,41 @@ def test_profile_known_answers(orc):
     assert fr.tolist() == [[0, 0, 4], [1, 0, 0], [1, 4, 4], [2, 0, 0], [2, 4, 4], [3, 0, 0], [3, 4, 4], [4, 0, 4]]
     br = orc.profile(branch_example(), 2)
     assert br.tolist() == [[0, 0, 1], [0, 3, 6], [1, 0, 4], [1, 6, 6]]
+
+
+def test_decompose_known_answers(orc):
+    # test_hypergraph.cpp:37-57 (frame) and :59-73 (branch example)
+    d = orc.decompose(orc.synth(Spec.frame(5, 5)), 5)
+    assert d.edge_offsets.tolist() == [0, 1, 4, 7, 8]
+    assert d.edge_runs.tolist() == [[0, 0, 4], [1, 0, 0], [2, 0, 0], [3, 0, 0], [1, 4, 4], [2, 4, 4], [3, 4, 4],
+                                    [4, 0, 4]]
+    assert d.run_to_edge.tolist() == [0, 1, 2, 1, 2, 1, 2, 3]  # edge_of(0,0)=0, (1,0)=1, (1,1)=2, (4,0)=3
+    b = orc.decompose(branch_example(), 2)
+    assert b.edge_offsets.tolist() == [0, 1, 2, 3, 4]
+    assert b.edge_runs.tolist() == [[0, 0, 1], [0, 3, 6], [1, 0, 4], [1, 6, 6]]
+    # test_hypergraph.cpp:75-88: hbands(20,20,k) -> k edges; empty -> 0
+    for k in (1, 3, 7):
+        assert orc.decompose(orc.synth(Spec.hbands(20, 20, k)), 20).edge_count == k
+    assert orc.decompose(orc.synth(Spec.empty(3, 3)), 3).edge_count == 0
+
+
+def test_decompose_matches_reference_golden(orc):
+    # digests of the reference's decompose on the 1170-image corpus + the small large images
+    for row in decompose():
+        sp = spec_of(row["spec"])
+        if sp.width * sp.height > 5_000_000:
+            continue
+        got = decomposition_digest(orc.decompose(orc.synth(sp), sp.width))
+        want = {k: row[k] for k in got}
+        assert got == want, row["name"]
+
+
+def test_decompose_against_live_reference(orc, ref):
+    rng = np.random.default_rng(11)
+    for _ in range(40):
+        w, h = int(rng.integers(1, 150)), int(rng.integers(1, 100))
+        sp = Spec.random(w, h, float(rng.choice([0.2, 0.5, 0.8])), int(rng.integers(0, 1 << 62)))
+        bits = orc.synth(sp)
+        a, b = orc.decompose(bits, w), ref.image(bits, w).decompose()
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
