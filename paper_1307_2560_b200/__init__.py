@@ -308,9 +308,9 @@ def _take_hypergraph(h: ctypes.c_void_p, width: int, height: int) -> Hypergraph:
     try:
         n, e, ms = _i64(0), _i64(0), ctypes.c_float(0)
         _check(_lib.ychg_hypergraph_info(h, ctypes.byref(n), ctypes.byref(e), ctypes.byref(ms)), "decompose")
-        er = np.zeros((max(n.value, 1), 3), dtype=np.int32)
-        eo = np.zeros(e.value + 1, dtype=np.uint32)
-        r2e = np.zeros(max(n.value, 1), dtype=np.uint32)
+        er = np.empty((max(n.value, 1), 3), dtype=np.int32)
+        eo = np.empty(e.value + 1, dtype=np.uint32)
+        r2e = np.empty(max(n.value, 1), dtype=np.uint32)
         _check(_lib.ychg_hypergraph_copy(h, er.ctypes.data_as(_vp), eo.ctypes.data_as(_vp), r2e.ctypes.data_as(_vp)),
                "decompose")
         return Hypergraph(width, height, er[: n.value], eo, r2e[: n.value], float(ms.value))

@@ -470,12 +470,6 @@ struct HostContext {
     // hyperedge decomposition
     void* d_dws = nullptr;
     int64_t dws_cap = 0;
-    int32_t* d_eruns = nullptr;
-    int64_t eruns_cap = 0;
-    uint32_t* d_eoff = nullptr;
-    int64_t eoff_cap = 0;
-    uint32_t* d_r2e = nullptr;
-    int64_t r2e_cap = 0;
     unsigned long long* d_dscal = nullptr;  // [0] edge/run totals, [1] validation error
     unsigned long long* h_dscal = nullptr;  // pinned
     int* h_flag = nullptr;                  // pinned: jump-round change flag
@@ -844,9 +838,11 @@ struct ychg_hypergraph {
     int32_t width = 0, height = 0;
     int64_t n_runs = 0, n_edges = 0;
     float device_ms = 0.f;
-    std::vector<int32_t> edge_runs;
-    std::vector<uint32_t> edge_offsets{0};
-    std::vector<uint32_t> run_to_edge;
+    int device = 0;
+    // device-resident results (stream-ordered allocations, freed by destroy)
+    int32_t* d_eruns = nullptr;
+    uint32_t* d_eoff = nullptr;
+    uint32_t* d_r2e = nullptr;
 };
 
 namespace {
@@ -869,6 +865,11 @@ int ensure_decompose(HostContext& c, int64_t n) {
         CK(cudaMalloc(&c.d_dscal, 16));
         CK(cudaEventCreate(&c.dec_ev[0]));
         CK(cudaEventCreate(&c.dec_ev[1]));
+        // keep freed result buffers cached in the device's default pool
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, c.device));
+        uint64_t keep = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     const int64_t ws = ychg_decompose_ws_bytes(n);
     if (ws > c.dws_cap) {
@@ -878,20 +879,23 @@ int ensure_decompose(HostContext& c, int64_t n) {
         CK(cudaMalloc(&c.d_dws, ws));
         c.dws_cap = ws;
     }
-    if (const int rc = ensure_buf(&c.d_eruns, &c.eruns_cap, 3 * n)) return rc;
-    if (const int rc = ensure_buf(&c.d_eoff, &c.eoff_cap, n + 1)) return rc;
-    return ensure_buf(&c.d_r2e, &c.r2e_cap, n);
+    return YCHG_OK;
 }
 
-// Decompose the n-run profile in c.d_runs / c.d_col_off / c.d_counts into hg.
+// Decompose the n-run profile in c.d_runs / c.d_col_off / c.d_counts into hg's
+// device buffers (kept on the device until ychg_hypergraph_copy).
 int decompose_device_profile(HostContext& c, int32_t width, int64_t n, ychg_hypergraph* hg) {
     if (n > int64_t(0xFFFFFFFEu))
         return fail(YCHG_ERR_INVALID, "decompose: %lld runs exceed the 32-bit run index of Hypergraph",
                     static_cast<long long>(n));
     if (const int rc = ensure_decompose(c, n)) return rc;
+    hg->device = c.device;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&hg->d_eruns), n * 12, c.stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&hg->d_eoff), (n + 1) * 4, c.stream));
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&hg->d_r2e), n * 4, c.stream));
     CK(cudaEventRecord(c.dec_ev[0], c.stream));
-    const int rounds = ychg_launch_decompose(c.d_runs, c.d_col_off, c.d_counts, width, n, c.d_dws, c.d_eruns,
-                                             c.d_eoff, c.d_r2e, c.d_dscal, c.h_flag, c.stream);
+    const int rounds = ychg_launch_decompose(c.d_runs, c.d_col_off, c.d_counts, width, n, c.d_dws, hg->d_eruns,
+                                             hg->d_eoff, hg->d_r2e, c.d_dscal, c.h_flag, c.stream);
     if (rounds < 0) return cuda_fail(static_cast<cudaError_t>(-rounds), "decompose kernels");
     CK(cudaEventRecord(c.dec_ev[1], c.stream));
     CK(cudaMemcpyAsync(c.h_dscal, c.d_dscal, 8, cudaMemcpyDeviceToHost, c.stream));
@@ -903,15 +907,23 @@ int decompose_device_profile(HostContext& c, int32_t width, int64_t n, ychg_hype
     if (static_cast<int64_t>(tot & 0xFFFFFFFFull) != n)
         return fail(YCHG_ERR_INTERNAL, "decompose: chains cover %llu of %lld runs", tot & 0xFFFFFFFFull,
                     static_cast<long long>(n));
-    hg->edge_runs.resize(size_t(3 * n));
-    hg->edge_offsets.resize(size_t(hg->n_edges + 1));
-    hg->run_to_edge.resize(size_t(n));
-    CK(cudaMemcpyAsync(hg->edge_runs.data(), c.d_eruns, n * 12, cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaMemcpyAsync(hg->edge_offsets.data(), c.d_eoff, (hg->n_edges + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaMemcpyAsync(hg->run_to_edge.data(), c.d_r2e, n * 4, cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
     return YCHG_OK;
 }
+
+void release_hypergraph(ychg_hypergraph* hg) {
+    if (!hg) return;
+    if (hg->d_eruns || hg->d_eoff || hg->d_r2e) {
+        HostContext& c = host_context(hg->device);
+        std::lock_guard<std::mutex> lock(c.mu);
+        cudaSetDevice(hg->device);
+        cudaFreeAsync(hg->d_eruns, c.stream);
+        cudaFreeAsync(hg->d_eoff, c.stream);
+        cudaFreeAsync(hg->d_r2e, c.stream);
+    }
+    delete hg;
+}
+
+using HgPtr = std::unique_ptr<ychg_hypergraph, void (*)(ychg_hypergraph*)>;
 
 }  // namespace
 
@@ -926,7 +938,7 @@ extern "C" int ychg_decompose_image(const uint8_t* bits, int32_t width, int32_t 
     if (const int rc = check_profile_args(bits, width, height, row_stride)) return rc;
     const int device = pick_device();
     if (const int rc = require_device(device)) return rc;
-    std::unique_ptr<ychg_hypergraph> hg(new ychg_hypergraph);
+    HgPtr hg(new ychg_hypergraph, release_hypergraph);
     hg->width = width;
     hg->height = height;
     if (width > 0 && height > 0) {
@@ -961,7 +973,7 @@ extern "C" int ychg_decompose_profile(int32_t width, int32_t height, const int32
     if (n_runs > 0 && !runs) return fail(YCHG_ERR_INVALID, "decompose: null runs");
     const int device = pick_device();
     if (const int rc = require_device(device)) return rc;
-    std::unique_ptr<ychg_hypergraph> hg(new ychg_hypergraph);
+    HgPtr hg(new ychg_hypergraph, release_hypergraph);
     hg->width = width;
     hg->height = height;
     if (n_runs > 0) {
@@ -1020,10 +1032,19 @@ extern "C" int ychg_hypergraph_info(const ychg_hypergraph* hg, int64_t* n_runs, 
 extern "C" int ychg_hypergraph_copy(const ychg_hypergraph* hg, int32_t* edge_runs, uint32_t* edge_offsets,
                                     uint32_t* run_to_edge) {
     if (!hg) return fail(YCHG_ERR_INVALID, "hypergraph: null handle");
-    if (edge_runs && hg->n_runs) std::memcpy(edge_runs, hg->edge_runs.data(), size_t(hg->n_runs) * 12);
-    if (edge_offsets) std::memcpy(edge_offsets, hg->edge_offsets.data(), size_t(hg->n_edges + 1) * 4);
-    if (run_to_edge && hg->n_runs) std::memcpy(run_to_edge, hg->run_to_edge.data(), size_t(hg->n_runs) * 4);
+    if (hg->n_runs == 0) {
+        if (edge_offsets) edge_offsets[0] = 0;
+        return YCHG_OK;
+    }
+    HostContext& c = host_context(hg->device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    CK(cudaSetDevice(hg->device));
+    if (edge_runs) CK(cudaMemcpyAsync(edge_runs, hg->d_eruns, hg->n_runs * 12, cudaMemcpyDeviceToHost, c.stream));
+    if (edge_offsets)
+        CK(cudaMemcpyAsync(edge_offsets, hg->d_eoff, (hg->n_edges + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (run_to_edge) CK(cudaMemcpyAsync(run_to_edge, hg->d_r2e, hg->n_runs * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
     return YCHG_OK;
 }
 
-extern "C" void ychg_hypergraph_destroy(ychg_hypergraph* hg) { delete hg; }
+extern "C" void ychg_hypergraph_destroy(ychg_hypergraph* hg) { release_hypergraph(hg); }

@@ -114,3 +114,17 @@ def test_decompose_live_reference(gpu, orc, ref):
         got = y.decompose(y.BinaryImage(sp.width, sp.height, bits))
         for a, b in zip(as_tuple(got), want):
             assert np.array_equal(a, b)
+
+
+def test_decompose_cxx_dropin(gpu):
+    """ychg::b200::decompose returns the reference's own Hypergraph type, equal to
+    ychg::decompose (tests/cpp/decompose_dropin.cpp, built by `make -C oracle dropin`)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "decompose_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/decompose_dropin not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "[PASS]" in out.stdout
