@@ -49,7 +49,8 @@ enum {
     YCHG_ERR_CUDA = -2,      /* CUDA runtime/driver failure: maps to ychg::Error */
     YCHG_ERR_OOM = -3,       /* device or pinned allocation failed */
     YCHG_ERR_NO_DEVICE = -4, /* no CUDA device (no CPU fallback exists) */
-    YCHG_ERR_INTERNAL = -5
+    YCHG_ERR_INTERNAL = -5,
+    YCHG_ERR_PARSE = -6      /* malformed input bytes: maps to ychg::ParseError at ychg_last_error_offset() */
 };
 
 /* ScanStrategy::Kind (runscan.hpp:26-36) */
@@ -87,6 +88,9 @@ typedef struct ychg_plan ychg_plan;
 
 /* ---- diagnostics ---- */
 YCHG_API const char* ychg_last_error(void);
+/* Byte offset of the last YCHG_ERR_PARSE (the reference's ParseError::offset()); -1 otherwise.
+ * ychg_last_error() then holds the message without the " (byte offset N)" suffix. */
+YCHG_API int64_t ychg_last_error_offset(void);
 YCHG_API int ychg_abi_version(void);
 YCHG_API int ychg_device_count(int* n);
 
@@ -143,6 +147,23 @@ YCHG_API int ychg_hypergraph_info(const ychg_hypergraph* hg, int64_t* n_runs, in
 YCHG_API int ychg_hypergraph_copy(const ychg_hypergraph* hg, int32_t* edge_runs, uint32_t* edge_offsets,
                                   uint32_t* run_to_edge);
 YCHG_API void ychg_hypergraph_destroy(ychg_hypergraph* hg);
+
+/* PNM input (load_pnm, pnm.cpp:124-153).  P4 rasters are the
+ * BinaryImage bytes themselves and go to the device as they are; P5 grey rasters
+ * are thresholded and packed on the device (sample < threshold = foreground);
+ * ASCII P1/P2 are parsed on the host.  Errors follow the reference: threshold
+ * outside [0,255], P3/P6/P7 and maxval != 255 -> YCHG_ERR_INVALID; malformed or
+ * truncated bytes -> YCHG_ERR_PARSE with the reference's byte offset. */
+YCHG_API int ychg_pnm_info(const uint8_t* bytes, int64_t n, int32_t* kind, int32_t* width, int32_t* height);
+/* Decode into a host BinaryImage buffer (row_stride >= (width+7)/8, height rows; padding bits zero). */
+YCHG_API int ychg_load_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, uint8_t* bits_out,
+                           int64_t row_stride);
+/* Decode straight into a device bit buffer (pitch >= (width+7)/8) on `cuda_stream`. */
+YCHG_API int ychg_load_pnm_device(const uint8_t* bytes, int64_t n, int32_t threshold, uint8_t* d_bits,
+                                  int64_t pitch, void* cuda_stream);
+/* ychg_scan_host on a PNM file's bytes (counts_out: width ints, boundaries_out: width ints). */
+YCHG_API int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, int32_t with_hyperedges,
+                           int32_t* counts_out, int32_t* boundaries_out, ychg_totals* totals_out);
 
 /* ---- device-resident plans ----
  * A plan fixes the geometry and owns its device workspace.  width_img columns

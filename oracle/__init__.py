@@ -224,6 +224,8 @@ class Reference:
         L.yr_hyperedges.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.yr_profile.restype = ctypes.c_int64
         L.yr_profile.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _i32p, ctypes.c_int64]
+        L.yr_load_pnm.restype = ctypes.c_int
+        L.yr_load_pnm.argtypes = [_u8p, ctypes.c_int64, ctypes.c_int, _u8p, ctypes.c_int64, _i32p, _i32p, _i64p]
         L.yr_decompose.restype = ctypes.c_int64
         L.yr_decompose.argtypes = [ctypes.c_void_p, _i32p, ctypes.c_int64, _u32p, ctypes.c_int64, _u32p, _i64p]
         L.yr_time_path.restype = ctypes.c_int
@@ -241,6 +243,25 @@ class Reference:
         if rc != 0:
             raise ValueError(self.last_error())
         return out
+
+    def load_pnm(self, data: bytes, threshold: int = 128):
+        """load_pnm by the reference: ("ok", bits (h, stride) uint8, w, h) or
+        ("parse", message, offset) / ("invalid", message) / ("error", message)."""
+        buf = np.frombuffer(data, dtype=np.uint8).copy() if len(data) else np.zeros(1, np.uint8)
+        w, h, off = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int64(0)
+        rc = self.lib.yr_load_pnm(_ptr(buf, _u8p), len(data), threshold, None, 0, ctypes.byref(w), ctypes.byref(h),
+                                  ctypes.byref(off))
+        if rc == -4:
+            return ("parse", self.last_error(), off.value)
+        if rc == -1:
+            return ("invalid", self.last_error())
+        if rc != 0:
+            return ("error", self.last_error())
+        stride = (w.value + 7) // 8
+        out = np.zeros((max(h.value, 1), max(stride, 1)), dtype=np.uint8)
+        self.lib.yr_load_pnm(_ptr(buf, _u8p), len(data), threshold, _ptr(out, _u8p), out.size, ctypes.byref(w),
+                             ctypes.byref(h), ctypes.byref(off))
+        return ("ok", out[: h.value, :stride], w.value, h.value)
 
     def image(self, bits: np.ndarray, w: int) -> "RefImage":
         bits = np.ascontiguousarray(bits)

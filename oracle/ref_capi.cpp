@@ -21,6 +21,7 @@
 #include "ychg/errors.hpp"
 #include "ychg/hypergraph.hpp"
 #include "ychg/image.hpp"
+#include "ychg/pnm.hpp"
 #include "ychg/runscan.hpp"
 #include "ychg/synth.hpp"
 
@@ -141,6 +142,26 @@ YR_EXPORT int64_t yr_profile(void* img, int kind, int threads, int32_t* runs, in
                 ++n;
             }
         return n;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// load_pnm (pnm.cpp:124-153).  Returns 0 and fills w/h (+ bits when cap
+// suffices), or -1 ValidationError / -4 ParseError (*offset set) / -2 / -3.
+YR_EXPORT int yr_load_pnm(const uint8_t* bytes, int64_t n, int threshold, uint8_t* bits, int64_t cap,
+                          int32_t* w, int32_t* h, int64_t* offset) {
+    try {
+        const auto img = ychg::load_pnm(std::span<const uint8_t>(bytes, static_cast<size_t>(n)), threshold);
+        *w = img.width();
+        *h = img.height();
+        if (bits && cap >= static_cast<int64_t>(img.bytes().size()))
+            std::memcpy(bits, img.bytes().data(), img.bytes().size());
+        return 0;
+    } catch (const ychg::ParseError& e) {
+        g_err = e.what();
+        *offset = static_cast<int64_t>(e.offset());
+        return -4;
     } catch (const std::exception& e) {
         return code_of(e);
     }

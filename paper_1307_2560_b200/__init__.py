@@ -32,7 +32,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- C ABI
-OK, ERR_INVALID, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL = 0, -1, -2, -3, -4, -5
+OK, ERR_INVALID, ERR_CUDA, ERR_OOM, ERR_NO_DEVICE, ERR_INTERNAL, ERR_PARSE = 0, -1, -2, -3, -4, -5, -6
 STRATEGY_SERIAL, STRATEGY_PARALLEL = 0, 1
 PATTERNS = {"full": 0, "empty": 1, "frame": 2, "hbands": 3, "checker": 4, "random": 5}
 
@@ -53,6 +53,11 @@ _vp, _i32, _i64, _u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.
 _SIGS = {
     "ychg_last_error": (ctypes.c_char_p, []),
     "ychg_abi_version": (ctypes.c_int, []),
+    "ychg_last_error_offset": (ctypes.c_int64, []),
+    "ychg_pnm_info": (ctypes.c_int, [_vp, _i64, ctypes.POINTER(_i32), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "ychg_load_pnm": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i64]),
+    "ychg_load_pnm_device": (ctypes.c_int, [_vp, _i64, _i32, _vp, _i64, _vp]),
+    "ychg_scan_pnm": (ctypes.c_int, [_vp, _i64, _i32, _i32, _vp, _vp, ctypes.POINTER(Totals)]),
     "ychg_device_count": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
     "ychg_set_device": (ctypes.c_int, [ctypes.c_int]),
     "ychg_cut_vertex_counts": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp]),
@@ -102,10 +107,21 @@ class ValidationError(Error):
     """Precondition violation (ychg::ValidationError)."""
 
 
+class ParseError(Error):
+    """Malformed input bytes (ychg::ParseError); `offset` is the byte offset."""
+
+    def __init__(self, msg: str, offset: int = 0):
+        super().__init__(msg)
+        self.offset = offset
+
+
 def _check(rc: int, what: str) -> None:
     if rc == OK:
         return
     msg = f"{what}: {_lib.ychg_last_error().decode(errors='replace')}"
+    if rc == ERR_PARSE:
+        off = int(_lib.ychg_last_error_offset())
+        raise ParseError(f"{msg} (byte offset {off})", off)
     if rc == ERR_INVALID:
         raise ValidationError(msg)
     raise Error(msg)
@@ -220,6 +236,49 @@ def scan(image: BinaryImage, with_hyperedges: bool = True) -> ScanResult:
                                bounds.ctypes.data_as(_vp), ctypes.byref(t)), "scan")
     return ScanResult(counts[: image.width], bounds[: t.n_boundaries].copy(), t.total_runs,
                       t.links, t.hyperedges, t.n_boundaries)
+
+
+# ---------------------------------------------------------------- PNM input (pnm.hpp, §8f row 3)
+def pnm_info(data: bytes) -> tuple[int, int, int]:
+    """(kind 1/2/4/5, width, height) of a PNM file's bytes (header parse only)."""
+    buf = np.frombuffer(data, dtype=np.uint8)
+    k, w, h = _i32(0), _i32(0), _i32(0)
+    _check(_lib.ychg_pnm_info(buf.ctypes.data_as(_vp), buf.size, ctypes.byref(k), ctypes.byref(w), ctypes.byref(h)),
+           "load_pnm")
+    return k.value, w.value, h.value
+
+
+def load_pnm(data: bytes, threshold: int = 128) -> BinaryImage:
+    """load_pnm (pnm.cpp:124-153): P4 as is, P5 thresholded on the device, P1/P2 parsed."""
+    buf = np.frombuffer(data, dtype=np.uint8)
+    if not 0 <= threshold <= 255:
+        raise ValidationError(f"load_pnm: pnm: threshold must lie in [0, 255], got {threshold}")
+    _, w, h = pnm_info(data)
+    img = BinaryImage(w, h)
+    _check(_lib.ychg_load_pnm(buf.ctypes.data_as(_vp), buf.size, int(threshold), img._ptr(), img.row_stride),
+           "load_pnm")
+    return img
+
+
+def save_pnm(image: BinaryImage) -> bytes:
+    """save_pnm (pnm.cpp:155-163): binary P4 whose payload is the image buffer."""
+    return f"P4\n{image.width} {image.height}\n".encode() + image.bytes().tobytes()
+
+
+def scan_pnm(data: bytes, threshold: int = 128, with_hyperedges: bool = True) -> ScanResult:
+    """scan() of a PNM file's bytes: the P4 raster goes to the device untouched, P5 is
+    thresholded and packed on the device."""
+    buf = np.frombuffer(data, dtype=np.uint8)
+    if not 0 <= threshold <= 255:
+        raise ValidationError(f"scan_pnm: pnm: threshold must lie in [0, 255], got {threshold}")
+    _, w, _ = pnm_info(data)
+    counts = np.zeros(max(w, 1), dtype=np.int32)
+    bounds = np.zeros(max(w, 1), dtype=np.int32)
+    t = Totals()
+    _check(_lib.ychg_scan_pnm(buf.ctypes.data_as(_vp), buf.size, int(threshold), int(with_hyperedges),
+                              counts.ctypes.data_as(_vp), bounds.ctypes.data_as(_vp), ctypes.byref(t)), "scan_pnm")
+    return ScanResult(counts[:w], bounds[: t.n_boundaries].copy(), t.total_runs, t.links, t.hyperedges,
+                      t.n_boundaries)
 
 
 def hyperedge_count(image: BinaryImage) -> int:
@@ -452,7 +511,7 @@ def synth(pattern: str, width: int, height: int, *, bands: int = 0, cell: int = 
 
 __all__ = [
     "BinaryImage", "ScanStrategy", "ScanResult", "ColumnProfile", "build_profile", "column_runs", "Error",
-    "Hypergraph", "decompose",
+    "Hypergraph", "decompose", "ParseError", "pnm_info", "load_pnm", "save_pnm", "scan_pnm",
     "ValidationError", "cut_vertex_counts",
     "detect_boundary_columns", "scan", "hyperedge_count", "Plan", "DeviceBuffer", "synth", "synth_device",
     "pitch_for", "device_count", "Totals", "PlanInfo", "LIB_PATH", "CXX_LIB_PATH", "EXPORTED_SYMBOLS",

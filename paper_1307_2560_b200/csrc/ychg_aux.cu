@@ -224,3 +224,50 @@ extern "C" int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }
+
+// ---------------------------------------------------------------------------- PNM rasters (§8f row 3)
+// P5 (pnm.cpp:116-123): W*H grey bytes -> packed MSB-first rows, foreground iff
+// sample < threshold.  One thread per output byte (8 samples).
+__global__ void pack_p5_kernel(const uint8_t* __restrict__ samples, int32_t width, int32_t height, int32_t threshold,
+                               uint8_t* __restrict__ bits, int64_t pitch) {
+    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+    const int64_t total = row_bytes * height;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t y = i / row_bytes, b = i - y * row_bytes;
+        const uint8_t* row = samples + y * width;
+        const int x0 = static_cast<int>(b * 8);
+        uint32_t v = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (x0 + k < width && __ldg(row + x0 + k) < threshold) v |= 0x80u >> k;
+        bits[y * pitch + b] = static_cast<uint8_t>(v);
+    }
+}
+
+// P4 (pnm.cpp:103-114): padding bits of the last byte of every row forced to 0.
+__global__ void mask_pad_kernel(uint8_t* __restrict__ bits, int64_t pitch, int32_t height, int64_t last, uint8_t mask) {
+    for (int64_t y = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; y < height; y += int64_t(gridDim.x) * blockDim.x)
+        bits[y * pitch + last] &= mask;
+}
+
+extern "C" int ychg_launch_pack_p5(const uint8_t* d_samples, int32_t width, int32_t height, int32_t threshold,
+                                   uint8_t* d_bits, int64_t pitch, cudaStream_t stream) {
+    const int64_t total = (int64_t(width) + 7) / 8 * height;
+    if (total <= 0) return 0;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    pack_p5_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_samples, width, height, threshold, d_bits, pitch);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+extern "C" int ychg_launch_mask_pad(uint8_t* d_bits, int64_t pitch, int32_t width, int32_t height,
+                                    cudaStream_t stream) {
+    if (width % 8 == 0 || height <= 0) return 0;
+    const uint8_t mask = static_cast<uint8_t>(0xFFu << (8 - width % 8));
+    int64_t blocks = (int64_t(height) + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    mask_pad_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_bits, pitch, height, (width + 7) / 8 - 1, mask);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}

@@ -23,6 +23,7 @@ using ychg_dev::ScanParams;
 namespace {
 
 thread_local std::string g_error;
+thread_local int64_t g_error_offset = -1;
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -31,6 +32,7 @@ int fail(int code, const char* fmt, ...) {
     std::vsnprintf(buf, sizeof(buf), fmt, ap);
     va_end(ap);
     g_error = buf;
+    g_error_offset = -1;
     return code;
 }
 
@@ -125,6 +127,8 @@ int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out) {
 extern "C" {
 
 const char* ychg_last_error(void) { return g_error.c_str(); }
+
+int64_t ychg_last_error_offset(void) { return g_error_offset; }
 
 int ychg_abi_version(void) { return YCHG_ABI_VERSION; }
 
@@ -590,19 +594,12 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
     return YCHG_OK;
 }
 
-extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
-                              int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
-                              ychg_totals* totals_out) {
-    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan: negative geometry %dx%d", width, height);
+// The host scan on a locked, ready context: `upload` fills c.d_bits (pitched)
+// on c.stream; then one scan and one D2H round trip.
+template <typename Upload>
+int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, int32_t with_hyperedges,
+                     int32_t* counts_out, int32_t* boundaries_out, ychg_totals* totals_out, Upload&& upload) {
     const int64_t row_bytes = (int64_t(width) + 7) / 8;
-    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
-        return fail(YCHG_ERR_INVALID, "scan: row_stride %lld < %lld", static_cast<long long>(row_stride),
-                    static_cast<long long>(row_bytes));
-    const int device = pick_device();
-    if (const int rc = require_device(device)) return rc;
-    HostContext& c = host_context(device);
-    std::lock_guard<std::mutex> lock(c.mu);
-    if (const int rc = ensure_context(c)) return rc;
 
     if (width == 0 || height == 0) {
         if (counts_out && width > 0) std::memset(counts_out, 0, size_t(width) * 4);
@@ -618,7 +615,7 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
         c.plan_h = height;
     }
     const int64_t pitch = (row_bytes + 15) / 16 * 16;
-    if (const int rc = upload_image(c, bits, width, height, row_stride)) return rc;
+    if (const int rc = upload()) return rc;
     if (const int rc = ensure_columns(c, width)) return rc;
     static const bool host_timing = [] {
         const char* v = getenv("YCHG_HOST_TIMING");
@@ -667,6 +664,23 @@ extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height
         std::memcpy(boundaries_out, c.h_out + width, size_t(t.n_boundaries) * 4);
     if (totals_out) *totals_out = t;
     return YCHG_OK;
+}
+
+extern "C" int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                              int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
+                              ychg_totals* totals_out) {
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan: negative geometry %dx%d", width, height);
+    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
+        return fail(YCHG_ERR_INVALID, "scan: row_stride %lld < %lld", static_cast<long long>(row_stride),
+                    static_cast<long long>(row_bytes));
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+    return scan_host_locked(c, device, width, height, with_hyperedges, counts_out, boundaries_out, totals_out,
+                            [&] { return upload_image(c, bits, width, height, row_stride); });
 }
 
 extern "C" int ychg_cut_vertex_counts(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
@@ -1048,3 +1062,256 @@ extern "C" int ychg_hypergraph_copy(const ychg_hypergraph* hg, int32_t* edge_run
 }
 
 extern "C" void ychg_hypergraph_destroy(ychg_hypergraph* hg) { release_hypergraph(hg); }
+
+// ---------------------------------------------------------------------------- PNM input (§8f row 3)
+namespace {
+
+// load_pnm's grammar (pnm.cpp:12-79): tokens separated by whitespace and '#'
+// comments; binary rasters after exactly one whitespace byte.
+struct PnmCursor {
+    const uint8_t* p;
+    int64_t n;
+    int64_t pos;
+    bool eof() const { return pos >= n; }
+    static bool space(uint8_t c) { return c == ' ' || c == '\t' || c == '\r' || c == '\n' || c == '\v' || c == '\f'; }
+    static bool digit(uint8_t c) { return c >= '0' && c <= '9'; }
+    void skip() {
+        while (!eof()) {
+            if (p[pos] == '#') {
+                while (!eof() && p[pos] != '\n') ++pos;
+            } else if (space(p[pos])) {
+                ++pos;
+            } else {
+                break;
+            }
+        }
+    }
+};
+
+int parse_fail(int64_t at, const char* fmt, ...) {
+    char buf[256];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    g_error_offset = at;
+    return YCHG_ERR_PARSE;
+}
+
+int pnm_uint(PnmCursor& r, const char* what, int32_t* out) {
+    r.skip();
+    if (r.eof() || !PnmCursor::digit(r.p[r.pos])) return parse_fail(r.pos, "pnm: expected %s", what);
+    long long v = 0;
+    while (!r.eof() && PnmCursor::digit(r.p[r.pos])) {
+        v = v * 10 + (r.p[r.pos++] - '0');
+        if (v > 2147483647LL) return parse_fail(r.pos, "pnm: %s out of range", what);
+    }
+    *out = static_cast<int32_t>(v);
+    return YCHG_OK;
+}
+
+struct PnmHeader {
+    char kind = 0;
+    int32_t width = 0, height = 0;
+    int64_t raster = 0;  // offset of the first raster byte (P4/P5) or of the ASCII samples (P1/P2)
+};
+
+// Header (+ the size check of a binary raster), in the reference's order.
+int pnm_header(const uint8_t* bytes, int64_t n, PnmHeader* hd) {
+    if (n > 0 && !bytes) return fail(YCHG_ERR_INVALID, "pnm: null bytes");
+    PnmCursor r{bytes, n, 0};
+    if (r.eof() || r.p[r.pos++] != 'P') return parse_fail(0, "pnm: missing magic number");
+    if (r.eof()) return parse_fail(1, "pnm: missing magic number");
+    const char kind = static_cast<char>(r.p[r.pos++]);
+    if (kind == '3' || kind == '6' || kind == '7')
+        return fail(YCHG_ERR_INVALID, "pnm: unsupported format P%c (only P1/P2/P4/P5)", kind);
+    if (kind != '1' && kind != '2' && kind != '4' && kind != '5') return parse_fail(1, "pnm: malformed magic number");
+    if (const int rc = pnm_uint(r, "width", &hd->width)) return rc;
+    if (const int rc = pnm_uint(r, "height", &hd->height)) return rc;
+    if (kind == '2' || kind == '5') {
+        int32_t maxval = 0;
+        if (const int rc = pnm_uint(r, "maxval", &maxval)) return rc;
+        if (maxval != 255) return fail(YCHG_ERR_INVALID, "pnm: unsupported maxval %d (must be 255)", maxval);
+    }
+    if (kind == '4' || kind == '5') {
+        if (r.eof() || !PnmCursor::space(r.p[r.pos]))
+            return parse_fail(r.pos, "pnm: expected single whitespace before raster");
+        ++r.pos;
+        const int64_t left = n - r.pos;
+        if (kind == '4') {
+            const int64_t stride = (int64_t(hd->width) + 7) / 8;
+            if (stride > 0 && left < stride * hd->height)
+                return parse_fail(r.pos + (left / stride) * stride, "pnm: truncated P4 raster");
+        } else if (left < int64_t(hd->width) * hd->height) {
+            return parse_fail(r.pos, "pnm: truncated P5 raster");
+        }
+    }
+    hd->kind = kind;
+    hd->raster = r.pos;
+    return YCHG_OK;
+}
+
+int check_threshold(int32_t threshold) {
+    if (threshold < 0 || threshold > 255)
+        return fail(YCHG_ERR_INVALID, "pnm: threshold must lie in [0, 255], got %d", threshold);
+    return YCHG_OK;
+}
+
+// ASCII rasters on the host (pnm.cpp:81-101) into zeroed rows of `stride` bytes.
+int pnm_ascii(const uint8_t* bytes, int64_t n, const PnmHeader& hd, int32_t threshold, uint8_t* bits, int64_t stride) {
+    PnmCursor r{bytes, n, hd.raster};
+    for (int32_t y = 0; y < hd.height; ++y) {
+        std::memset(bits + y * stride, 0, size_t((int64_t(hd.width) + 7) / 8));
+        for (int32_t x = 0; x < hd.width; ++x) {
+            bool fg;
+            if (hd.kind == '1') {
+                r.skip();
+                if (r.eof()) return parse_fail(r.pos, "pnm: truncated P1 raster");
+                const uint8_t ch = r.p[r.pos++];
+                if (ch != '0' && ch != '1') return parse_fail(r.pos - 1, "pnm: P1 raster sample must be 0 or 1");
+                fg = ch == '1';
+            } else {
+                const int64_t at = r.pos;
+                int32_t v = 0;
+                if (const int rc = pnm_uint(r, "P2 raster sample", &v)) return rc;
+                if (v > 255) return parse_fail(at, "pnm: P2 sample exceeds maxval");
+                fg = v < threshold;
+            }
+            if (fg) bits[y * stride + (x >> 3)] |= static_cast<uint8_t>(0x80u >> (x & 7));
+        }
+    }
+    return YCHG_OK;
+}
+
+template <typename T>
+int ensure_dev(T** p, int64_t* cap, int64_t bytes) {
+    if (bytes <= *cap) return YCHG_OK;
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<int64_t>(bytes, 16)));
+    *cap = bytes;
+    return YCHG_OK;
+}
+
+}  // namespace
+
+extern "C" int ychg_pnm_info(const uint8_t* bytes, int64_t n, int32_t* kind, int32_t* width, int32_t* height) {
+    PnmHeader hd;
+    if (const int rc = pnm_header(bytes, n, &hd)) return rc;
+    if (kind) *kind = hd.kind - '0';
+    if (width) *width = hd.width;
+    if (height) *height = hd.height;
+    return YCHG_OK;
+}
+
+extern "C" int ychg_load_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, uint8_t* bits_out,
+                             int64_t row_stride) {
+    if (const int rc = check_threshold(threshold)) return rc;
+    PnmHeader hd;
+    if (const int rc = pnm_header(bytes, n, &hd)) return rc;
+    const int64_t rb = (int64_t(hd.width) + 7) / 8;
+    if (hd.height > 0 && rb > 0 && (!bits_out || row_stride < rb))
+        return fail(YCHG_ERR_INVALID, "load_pnm: row_stride %lld < %lld", static_cast<long long>(row_stride),
+                    static_cast<long long>(rb));
+    if (hd.width == 0 || hd.height == 0) return YCHG_OK;
+    if (hd.kind == '1' || hd.kind == '2') return pnm_ascii(bytes, n, hd, threshold, bits_out, row_stride);
+    if (hd.kind == '4') {  // the payload IS the BinaryImage layout (pnm.cpp:103-114)
+        const uint8_t mask = static_cast<uint8_t>(hd.width % 8 ? 0xFFu << (8 - hd.width % 8) : 0xFFu);
+        for (int32_t y = 0; y < hd.height; ++y) {
+            std::memcpy(bits_out + y * row_stride, bytes + hd.raster + y * rb, size_t(rb));
+            bits_out[y * row_stride + rb - 1] &= mask;
+        }
+        return YCHG_OK;
+    }
+    // P5: threshold + pack on the device
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+    const int64_t ns = int64_t(hd.width) * hd.height;
+    if (const int rc = ensure_dev(&c.d_dense, &c.dense_cap, ns)) return rc;
+    if (const int rc = ensure_dev(&c.d_bits, &c.bits_cap, rb * hd.height)) return rc;
+    CK(cudaMemcpyAsync(c.d_dense, bytes + hd.raster, ns, cudaMemcpyHostToDevice, c.stream));
+    const int rc = ychg_launch_pack_p5(c.d_dense, hd.width, hd.height, threshold, c.d_bits, rb, c.stream);
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "P5 pack kernel");
+    CK(cudaMemcpy2DAsync(bits_out, row_stride, c.d_bits, rb, rb, hd.height, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return YCHG_OK;
+}
+
+extern "C" int ychg_load_pnm_device(const uint8_t* bytes, int64_t n, int32_t threshold, uint8_t* d_bits,
+                                    int64_t pitch, void* cuda_stream) {
+    if (const int rc = check_threshold(threshold)) return rc;
+    PnmHeader hd;
+    if (const int rc = pnm_header(bytes, n, &hd)) return rc;
+    const int64_t rb = (int64_t(hd.width) + 7) / 8;
+    if (hd.width == 0 || hd.height == 0) return YCHG_OK;
+    if (!d_bits || pitch < rb)
+        return fail(YCHG_ERR_INVALID, "load_pnm_device: pitch %lld < %lld", static_cast<long long>(pitch),
+                    static_cast<long long>(rb));
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (hd.kind == '4') {
+        CK(cudaMemcpy2DAsync(d_bits, pitch, bytes + hd.raster, rb, rb, hd.height, cudaMemcpyHostToDevice, st));
+        const int rc = ychg_launch_mask_pad(d_bits, pitch, hd.width, hd.height, st);
+        return rc ? cuda_fail(static_cast<cudaError_t>(rc), "P4 pad mask kernel") : YCHG_OK;
+    }
+    if (hd.kind == '5') {
+        const int64_t ns = int64_t(hd.width) * hd.height;
+        uint8_t* d_s = nullptr;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&d_s), ns, st));
+        CK(cudaMemcpyAsync(d_s, bytes + hd.raster, ns, cudaMemcpyHostToDevice, st));
+        const int rc = ychg_launch_pack_p5(d_s, hd.width, hd.height, threshold, d_bits, pitch, st);
+        CK(cudaFreeAsync(d_s, st));
+        return rc ? cuda_fail(static_cast<cudaError_t>(rc), "P5 pack kernel") : YCHG_OK;
+    }
+    std::vector<uint8_t> host(size_t(rb * hd.height));
+    if (const int rc = pnm_ascii(bytes, n, hd, threshold, host.data(), rb)) return rc;
+    CK(cudaMemcpy2DAsync(d_bits, pitch, host.data(), rb, rb, hd.height, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));  // `host` is released on return
+    return YCHG_OK;
+}
+
+extern "C" int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, int32_t with_hyperedges,
+                             int32_t* counts_out, int32_t* boundaries_out, ychg_totals* totals_out) {
+    if (const int rc = check_threshold(threshold)) return rc;
+    PnmHeader hd;
+    if (const int rc = pnm_header(bytes, n, &hd)) return rc;
+    const int64_t rb = (int64_t(hd.width) + 7) / 8;
+    // P4: the raster goes to the device untouched -- the kernels never read padding bits
+    if (hd.kind == '4')
+        return ychg_scan_host(bytes + hd.raster, hd.width, hd.height, rb, with_hyperedges, counts_out,
+                              boundaries_out, totals_out);
+    if (hd.kind == '1' || hd.kind == '2') {
+        std::vector<uint8_t> host(size_t(std::max<int64_t>(rb * hd.height, 1)));
+        if (const int rc = pnm_ascii(bytes, n, hd, threshold, host.data(), rb)) return rc;
+        return ychg_scan_host(host.data(), hd.width, hd.height, rb, with_hyperedges, counts_out, boundaries_out,
+                              totals_out);
+    }
+    const int device = pick_device();
+    if (const int rc = require_device(device)) return rc;
+    HostContext& c = host_context(device);
+    std::lock_guard<std::mutex> lock(c.mu);
+    if (const int rc = ensure_context(c)) return rc;
+    if (hd.width == 0 || hd.height == 0) {
+        if (counts_out && hd.width > 0) std::memset(counts_out, 0, size_t(hd.width) * 4);
+        if (totals_out) *totals_out = ychg_totals{0, 0, with_hyperedges ? 0 : -1, 0};
+        return YCHG_OK;
+    }
+    return scan_host_locked(c, device, hd.width, hd.height, with_hyperedges, counts_out, boundaries_out, totals_out,
+                            [&]() -> int {
+                                const int64_t ns = int64_t(hd.width) * hd.height;
+                                const int64_t pitch = (rb + 15) / 16 * 16;
+                                if (const int rc = ensure_dev(&c.d_dense, &c.dense_cap, ns)) return rc;
+                                if (const int rc = ensure_dev(&c.d_bits, &c.bits_cap, pitch * hd.height)) return rc;
+                                CK(cudaMemcpyAsync(c.d_dense, bytes + hd.raster, ns, cudaMemcpyHostToDevice,
+                                                   c.stream));
+                                const int rc = ychg_launch_pack_p5(c.d_dense, hd.width, hd.height, threshold,
+                                                                   c.d_bits, pitch, c.stream);
+                                return rc ? cuda_fail(static_cast<cudaError_t>(rc), "P5 pack kernel") : YCHG_OK;
+                            });
+}
