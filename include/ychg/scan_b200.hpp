@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <span>
 #include <vector>
 
 #include "ychg/image.hpp"
@@ -22,5 +23,9 @@ struct ScanResult {
 };
 
 ScanResult scan(const BinaryImage& image);
+
+/// scan() of a PNM file's bytes (pnm.cpp formats): the P4 raster goes to the
+/// device untouched, P5 is thresholded and packed on the device.
+ScanResult scan_pnm(std::span<const std::uint8_t> bytes, int threshold = 128);
 
 }  // namespace ychg

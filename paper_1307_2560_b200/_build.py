@@ -55,7 +55,7 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> None:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
     cxx_deps = [os.path.join(CSRC, "ychg_runscan.cpp"), CUDA_SO] + [
-        os.path.join(INCLUDE, "ychg", f) for f in ("errors.hpp", "image.hpp", "runscan.hpp", "scan_b200.hpp")]
+        os.path.join(INCLUDE, "ychg", f) for f in ("errors.hpp", "image.hpp", "runscan.hpp", "scan_b200.hpp", "pnm.hpp")]
     if force or _stale(CXX_SO, cxx_deps):
         _run([os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-fPIC", "-shared", "-I" + INCLUDE,
               "-o", CXX_SO, os.path.join(CSRC, "ychg_runscan.cpp"), "-L" + PKG, "-l:libychg_b200.so",

@@ -7,6 +7,7 @@
 
 #include "ychg/errors.hpp"
 #include "ychg/image.hpp"
+#include "ychg/pnm.hpp"
 #include "ychg/runscan.hpp"
 #include "ychg/scan_b200.hpp"
 #include "ychg_b200.h"
@@ -17,12 +18,58 @@ namespace {
 
 void check(int rc, const char* what) {
     if (rc == YCHG_OK) return;
+    if (rc == YCHG_ERR_PARSE)
+        throw ParseError(ychg_last_error(), static_cast<std::size_t>(ychg_last_error_offset()));
     const std::string msg = std::string(what) + ": " + ychg_last_error();
     if (rc == YCHG_ERR_INVALID) throw ValidationError(msg);
     throw Error(msg);
 }
 
+// The PNM loader's messages are the reference's own (pnm.cpp), unprefixed.
+void check_pnm(int rc) {
+    if (rc == YCHG_OK) return;
+    if (rc == YCHG_ERR_PARSE)
+        throw ParseError(ychg_last_error(), static_cast<std::size_t>(ychg_last_error_offset()));
+    if (rc == YCHG_ERR_INVALID) throw ValidationError(ychg_last_error());
+    throw Error(std::string("load_pnm: ") + ychg_last_error());
+}
+
 }  // namespace
+
+BinaryImage load_pnm(std::span<const std::uint8_t> bytes, int threshold) {
+    if (threshold < 0 || threshold > 255)
+        throw ValidationError("pnm: threshold must lie in [0, 255], got " + std::to_string(threshold));
+    std::int32_t kind = 0, w = 0, h = 0;
+    check_pnm(ychg_pnm_info(bytes.data(), static_cast<std::int64_t>(bytes.size()), &kind, &w, &h));
+    BinaryImage img(w, h);
+    if (w > 0 && h > 0)
+        check_pnm(ychg_load_pnm(bytes.data(), static_cast<std::int64_t>(bytes.size()), threshold, img.row(0),
+                                img.row_stride()));
+    return img;
+}
+
+std::vector<std::uint8_t> save_pnm(const BinaryImage& image) {
+    const std::string head = "P4\n" + std::to_string(image.width()) + " " + std::to_string(image.height()) + "\n";
+    std::vector<std::uint8_t> out(head.begin(), head.end());
+    out.insert(out.end(), image.bytes().begin(), image.bytes().end());
+    return out;
+}
+
+ScanResult scan_pnm(std::span<const std::uint8_t> bytes, int threshold) {
+    std::int32_t kind = 0, w = 0, h = 0;
+    check_pnm(ychg_pnm_info(bytes.data(), static_cast<std::int64_t>(bytes.size()), &kind, &w, &h));
+    ScanResult r;
+    r.counts.assign(static_cast<std::size_t>(w), 0);
+    r.boundaries.assign(static_cast<std::size_t>(w), 0);
+    ychg_totals t{};
+    check_pnm(ychg_scan_pnm(bytes.data(), static_cast<std::int64_t>(bytes.size()), threshold, 1, r.counts.data(),
+                            r.boundaries.data(), &t));
+    r.boundaries.resize(static_cast<std::size_t>(t.n_boundaries));
+    r.total_runs = t.total_runs;
+    r.links = t.links;
+    r.hyperedges = t.hyperedges;
+    return r;
+}
 
 std::int64_t foreground_count(const BinaryImage& image) {
     std::int64_t n = 0;

@@ -7,7 +7,9 @@
 
 #include "ychg/errors.hpp"
 #include "ychg/image.hpp"
+#include "ychg/pnm.hpp"
 #include "ychg/runscan.hpp"
+#include <string>
 #include "ychg/scan_b200.hpp"
 
 using namespace ychg;
@@ -131,6 +133,35 @@ int main() {
     CHECK(bp.runs[0] == (std::vector<Run>{{0, 0, 1}, {0, 3, 6}}));
     CHECK(bp.runs[1] == (std::vector<Run>{{1, 0, 4}, {1, 6, 6}}));
     CHECK(build_profile(frame(5, 5), ScanStrategy::parallel(16)) == fp);
+
+    // pnm (test_imagekit.cpp:172-257)
+    auto bytes_of = [](const std::string& s) { return std::vector<std::uint8_t>(s.begin(), s.end()); };
+    CHECK(load_pnm(bytes_of("P1\n2 2\n1 0\n0 1\n")) == load_pnm(bytes_of("P1 # binary\n2 2 # dims\n1001")));
+    CHECK(load_pnm(save_pnm(frame(5, 5))) == frame(5, 5));
+    CHECK(save_pnm(BinaryImage(0, 0)) == bytes_of("P4\n0 0\n"));
+    {
+        auto p5 = bytes_of("P5\n2 1\n255\n");
+        p5.push_back(10);
+        p5.push_back(200);
+        const BinaryImage g = load_pnm(p5);
+        CHECK(g.get(0, 0) && !g.get(1, 0));
+        std::size_t off = 0;
+        try {
+            load_pnm(bytes_of("P5 2 2 255\n\x01\x02"));
+        } catch (const ParseError& e) {
+            off = e.offset();
+        }
+        CHECK(off == 11);
+        bool inval = false;
+        try {
+            load_pnm(bytes_of("P6\n1 1\n255\n"));
+        } catch (const ValidationError&) {
+            inval = true;
+        }
+        CHECK(inval);
+        const ScanResult sr = scan_pnm(save_pnm(frame(5, 5)));
+        CHECK(sr.counts == (std::vector<int>{1, 2, 2, 2, 1}) && sr.hyperedges == 4);
+    }
 
     std::printf("dropin_test: %d failure(s)\n", failures);
     return failures;
