@@ -20,6 +20,7 @@ INCLUDE = os.path.join(ROOT, "include")
 
 CUDA_SO = os.path.join(PKG, "libychg_b200.so")
 CXX_SO = os.path.join(PKG, "libychg.so")
+CLI_BIN = os.path.join(PKG, "ychg_b200")
 
 NVCC_ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["ychg_scan.cu", "ychg_aux.cu", "ychg_profile.cu", "ychg_decompose.cu", "ychg_capi.cu"]
@@ -59,6 +60,11 @@ def build(verbose_ptxas: bool = False, force: bool = False) -> None:
     if force or _stale(CXX_SO, cxx_deps):
         _run([os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-fPIC", "-shared", "-I" + INCLUDE,
               "-o", CXX_SO, os.path.join(CSRC, "ychg_runscan.cpp"), "-L" + PKG, "-l:libychg_b200.so",
+              "-Wl,-rpath,$ORIGIN"])
+    cli_deps = [os.path.join(CSRC, "ychg_cli.cpp"), CXX_SO, CUDA_SO]
+    if force or _stale(CLI_BIN, cli_deps):
+        _run([os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-I" + INCLUDE, "-o", CLI_BIN,
+              os.path.join(CSRC, "ychg_cli.cpp"), "-L" + PKG, "-l:libychg.so", "-l:libychg_b200.so",
               "-Wl,-rpath,$ORIGIN"])
 
 
