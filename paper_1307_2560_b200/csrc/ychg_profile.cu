@@ -9,10 +9,11 @@
 //                             the band's first run in the column's list) and the
 //                             column total; then the exclusive prefix over columns
 //                             (= offset of the column's list in the flat array).
-//   P3 profile_fill_kernel    re-streams each band: a rise at row y opens run
-//                             {c, y, ?} at the column's next index, a fall at row y
-//                             closes the open run with y_bot = y-1; a virtual
-//                             background row H closes what is open at the bottom.
+//   P3 profile_fill_kernel    re-streams each band, one lane per column: a rise
+//                             at row y opens run {c, y, ?} at the column's next
+//                             index, a fall at row y closes it with y_bot = y-1 (one
+//                             12-byte record); a virtual background row H closes
+//                             what is open at the bottom.
 // The flat output is column-major and sorted by y_top inside a column -- exactly
 // ColumnProfile::runs flattened (runscan.hpp:40-50).
 #include <cuda_runtime.h>
@@ -25,6 +26,7 @@
 namespace {
 
 constexpr int kBandRows = 256;  // rows per band: counts per band <= 128 fit 8 bit-planes
+constexpr int kChunk = 16;      // rows loaded ahead per step (independent loads in flight)
 
 struct ProfileArgs {
     const uint8_t* bits;
@@ -66,15 +68,20 @@ __global__ void profile_count_kernel(const ProfileArgs a, uint32_t* __restrict__
     uint32_t pl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (w < a.n_words) {
         uint32_t pa = load_word(a, w, y0 - 1);
-        for (int y = y0; y < y1; ++y) {
-            const uint32_t cur = load_word(a, w, y);
-            uint32_t c = cur & ~pa;  // rises (runscan.cpp:57)
-            pa = cur;
+        for (int yb = y0; yb < y1; yb += kChunk) {
+            uint32_t v[kChunk];  // kChunk independent row loads in flight
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t t = pl[k] & c;
-                pl[k] ^= c;
-                c = t;
+            for (int k = 0; k < kChunk; ++k) v[k] = load_word(a, w, yb + k < y1 ? yb + k : -1);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                uint32_t c = v[k] & ~pa;  // rises (runscan.cpp:57); rows past y1 load 0
+                pa = v[k];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t t = pl[q] & c;
+                    pl[q] ^= c;
+                    c = t;
+                }
             }
         }
     }
@@ -94,10 +101,16 @@ __global__ void profile_colscan_kernel(const ProfileArgs a, uint32_t* __restrict
     const int64_t stride = static_cast<int64_t>(a.n_words) * 32;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.width; c += gridDim.x * blockDim.x) {
         uint32_t run = 0;
-        for (int b = 0; b < a.n_bands; ++b) {
-            const uint32_t v = band_counts[b * stride + c];
-            band_counts[b * stride + c] = run;
-            run += v;
+        for (int b0 = 0; b0 < a.n_bands; b0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = b0 + k < a.n_bands ? band_counts[(b0 + k) * stride + c] : 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (b0 + k < a.n_bands) {
+                    band_counts[(b0 + k) * stride + c] = run;
+                    run += v[k];
+                }
         }
         counts[c] = static_cast<int32_t>(run);
     }
@@ -141,48 +154,59 @@ __global__ void profile_offsets_kernel(int32_t n, const int32_t* __restrict__ co
     if (tid == 0) *n_runs = carry;
 }
 
-// P3: fill.  Per warp: one band of 32 words; per lane the 32 columns' next run
-// index lives in shared memory (index = columns' run count before the row).
+// P3: fill.  One warp per (band, word); lane j owns column c = 32w + j and walks
+// the band's rows (one broadcast word load per row), so each lane appends to ONE
+// contiguous output stream -- its column's list -- and writes every run it
+// opens and closes as one 12-byte record.  32 open streams per warp keep the
+// L2 write set small (a lane-per-word layout had 1024 streams per warp and
+// thrashed L2 with partial lines: 5x DRAM write amplification).  A run open at
+// the band's top was started by an earlier band (index base-1): only its y_bot
+// is written here; a run still open at the bottom gets {c, y_top} here and its
+// y_bot from a later band (or the virtual background row H in the last band).
 __global__ void __launch_bounds__(256) profile_fill_kernel(const ProfileArgs a, const uint32_t* __restrict__ band_base,
                                                            const int64_t* __restrict__ col_off,
                                                            int32_t* __restrict__ runs /* [n][3] */) {
-    __shared__ uint32_t next[8][32][33];  // [warp][lane][column-in-word], padded
-    const int wib = threadIdx.x >> 5;
-    const int gw = blockIdx.x * 8 + wib;
+    const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    const int strips = (a.n_words + 31) / 32;
-    if (gw >= strips * a.n_bands) return;
-    const int band = gw / strips, strip = gw - band * strips;
-    const int w = strip * 32 + lane;
+    if (gw >= a.n_words * a.n_bands) return;
+    const int w = gw / a.n_bands, band = gw - w * a.n_bands;  // consecutive warps: bands of one word
+    const int c = 32 * w + lane;
+    const bool live = c < a.width;
     const int y0 = band * kBandRows;
     const int y1 = min(a.height, y0 + kBandRows);
-    const bool last_band = (band == a.n_bands - 1);
-    if (w >= a.n_words) return;
-    const int64_t bstride = static_cast<int64_t>(a.n_words) * 32;
-    uint32_t* nx = next[wib][lane];
-    for (int j = 0; j < 32; ++j) nx[j] = band_base[band * bstride + 32 * w + j];
+    const int yend = band == a.n_bands - 1 ? y1 + 1 : y1;  // virtual background row H closes open runs
+    const uint32_t me = 0x80000000u >> lane;
+    int64_t idx = live ? col_off[c] + band_base[static_cast<int64_t>(band) * a.n_words * 32 + c] : 0;
+    int top = -1;  // y_top of a run opened in this band and still open
     uint32_t pa = load_word(a, w, y0 - 1);
-    const int yend = last_band ? y1 + 1 : y1;  // virtual background row H closes open runs
-    for (int y = y0; y < yend; ++y) {
-        const uint32_t cur = y < a.height ? load_word(a, w, y) : 0u;
-        uint32_t rises = cur & ~pa, falls = pa & ~cur;
-        pa = cur;
-        while (rises) {
-            const int j = __clz(rises);  // column 32w + j
-            rises &= ~(0x80000000u >> j);
-            const int c = 32 * w + j;
-            const int64_t r = col_off[c] + nx[j];
-            nx[j] += 1;
-            runs[3 * r + 0] = c;
-            runs[3 * r + 1] = y;
+    for (int yb = y0; yb < yend; yb += kChunk) {
+        uint32_t v[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) v[k] = load_word(a, w, yb + k < y1 ? yb + k : -1);  // >= y1: background
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            const int y = yb + k;
+            if (y >= yend) break;
+            const uint32_t rise = v[k] & ~pa, fall = pa & ~v[k];
+            pa = v[k];
+            if (!live) continue;
+            if (fall & me) {
+                if (top >= 0) {
+                    runs[3 * idx + 0] = c;
+                    runs[3 * idx + 1] = top;
+                    runs[3 * idx + 2] = y - 1;
+                    ++idx;
+                    top = -1;
+                } else {
+                    runs[3 * (idx - 1) + 2] = y - 1;  // opened in an earlier band
+                }
+            }
+            if (rise & me) top = y;
         }
-        while (falls) {
-            const int j = __clz(falls);
-            falls &= ~(0x80000000u >> j);
-            const int c = 32 * w + j;
-            const int64_t r = col_off[c] + nx[j] - 1;  // the run that is open in column c
-            runs[3 * r + 2] = y - 1;
-        }
+    }
+    if (live && top >= 0) {  // still open: a later band writes y_bot
+        runs[3 * idx + 0] = c;
+        runs[3 * idx + 1] = top;
     }
 }
 
@@ -202,12 +226,14 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
     const int strips = (a.n_words + 31) / 32;
     const int warps = strips * a.n_bands;
     const int blocks = (warps + 7) / 8;
+    const int64_t fill_warps = static_cast<int64_t>(a.n_words) * a.n_bands;
     if (phase == 0) {  // counts + offsets
         profile_count_kernel<<<blocks, 256, 0, stream>>>(a, d_band_counts);
         profile_colscan_kernel<<<(width + 255) / 256, 256, 0, stream>>>(a, d_band_counts, d_counts);
         profile_offsets_kernel<<<1, 1024, 0, stream>>>(width, d_counts, d_col_off, d_n_runs);
     } else {  // fill
-        profile_fill_kernel<<<blocks, 256, 0, stream>>>(a, d_band_counts, d_col_off, d_runs);
+        profile_fill_kernel<<<static_cast<unsigned>((fill_warps + 7) / 8), 256, 0, stream>>>(a, d_band_counts,
+                                                                                           d_col_off, d_runs);
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
