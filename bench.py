@@ -251,19 +251,26 @@ def run_ours(a):
     graph = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream()
     cap.wait_stream(stream)
-    with torch.cuda.stream(cap):
-        with torch.cuda.graph(graph, stream=cap, capture_error_mode="thread_local"):
-            csptr = torch.cuda.current_stream().cuda_stream
-            for i in range(a.steps):
-                b = bufs[(a.warmup + i) % nbuf]
-                plan.scan_device(b.data_ptr(), pitch, counts.data_ptr(), flags.data_ptr(), bounds.data_ptr(),
-                                 totals.data_ptr(), csptr, with_links)
-                if dist is not None:
-                    dist.all_gather_into_tensor(gathered, counts)
-                    dist.all_reduce(totals[:2])
-    stream.wait_stream(cap)
-    graph.replay()  # warm replay
-    torch.cuda.synchronize()
+    try:
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap, capture_error_mode="thread_local"):
+                csptr = torch.cuda.current_stream().cuda_stream
+                for i in range(a.steps):
+                    b = bufs[(a.warmup + i) % nbuf]
+                    plan.scan_device(b.data_ptr(), pitch, counts.data_ptr(), flags.data_ptr(), bounds.data_ptr(),
+                                     totals.data_ptr(), csptr, with_links)
+                    if dist is not None:
+                        dist.all_gather_into_tensor(gathered, counts)
+                        dist.all_reduce(totals[:2])
+        stream.wait_stream(cap)
+        graph.replay()  # warm replay
+        torch.cuda.synchronize()
+    except Exception as e:  # noqa: BLE001 -- e.g. a collective that refuses graph capture (N>1)
+        if dist is None:
+            raise
+        print(f"[bench] CUDA-graph capture with collectives failed ({e!r}); timing eager steps", file=sys.stderr)
+        graph = None
+        torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -273,7 +280,11 @@ def run_ours(a):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    graph.replay()
+    if graph is not None:
+        graph.replay()
+    else:
+        for i in range(a.steps):
+            step(a.warmup + i)
     ev1.record(stream)
     torch.cuda.synchronize()
     if dist is not None:
@@ -354,7 +365,9 @@ def run_ours(a):
                          "frac": round(achieved / peak, 4), "traffic": profiled_traffic(),
                          "kernel": "ychg_scan_kernel + ychg_finish_kernel (2 PDL launches per step)",
                          "kernel_ms": round(scan_avg, 5), "algorithmic_bytes": img_bytes,
-                         "peak_source": peak_src, "timing": "CUDA events around a K-step CUDA graph replay"},
+                         "peak_source": peak_src,
+                         "timing": "CUDA events around a K-step CUDA graph replay" if graph is not None
+                         else "CUDA events around K eager steps (graph capture with collectives failed)"},
             "eager_launch_ms": round(sorted(eager_ms)[len(eager_ms) // 2], 5),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": info.kernels_per_scan * a.steps,
