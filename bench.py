@@ -64,14 +64,16 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def profiled_traffic():
-    """dram bytes per launch of the scan kernel from the committed ncu capture, if any."""
+def profiled_traffic(algorithmic_bytes):
+    """dram bytes per launch of the scan kernel from the committed ncu capture (made
+    on the default 21000^2 workload), if this run is that workload."""
     p = os.path.join(ROOT, "profiles", "ncu_scan_summary.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            t = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         return None
+    return t if t and abs(t - algorithmic_bytes) < 0.05 * algorithmic_bytes else None
 
 
 class ClockSampler:
@@ -362,7 +364,7 @@ def run_ours(a):
                        "plan": {"grid": info.grid, "n_strips": info.n_strips, "seg_per_strip": info.seg_per_strip}},
             "hbm_gbs_step": round((img_bytes + 4 * Ws + 4 * n_b + 32) / (ms_step * 1e-3) / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": profiled_traffic(),
+                         "frac": round(achieved / peak, 4), "traffic": profiled_traffic(img_bytes),
                          "kernel": "ychg_scan_kernel + ychg_finish_kernel (2 PDL launches per step)",
                          "kernel_ms": round(scan_avg, 5), "algorithmic_bytes": img_bytes,
                          "peak_source": peak_src,

@@ -306,3 +306,32 @@ def test_reference_acceptance_on_gpu_library(gpu):
         out = subprocess.run([exe, str(crit)], capture_output=True, text=True, timeout=600)
         line = out.stdout.strip().splitlines()[0] if out.stdout.strip() else out.stderr
         assert out.returncode == 0 and line.startswith("[PASS]"), line
+
+
+def checker_hyperedges(w, h, c):
+    """checker(c): every foreground cell is a rectangle and its own hyperedge (cells
+    only touch diagonally); cell (0,0) is foreground (synth.cpp checker rule)."""
+    cx, cy = -(-w // c), -(-h // c)
+    return (cx * cy + 1) // 2
+
+
+@pytest.mark.parametrize("pattern", ["hbands", "checker"])
+def test_max_size_65536(gpu, orc, ref, pattern):
+    """BASELINE config 5 geometry on one GPU (512 MiB mask, 64 strips x k segments):
+    counts bit-exact vs the unmodified reference (parallel, all host cores), the
+    boundary list vs the reference's detect_boundary_columns, and the hyperedge total
+    vs its closed form (validated against the oracle on small sizes below)."""
+    y = gpu
+    for w, h, c in [(20, 20, 7), (65, 70, 7), (100, 33, 7)]:
+        assert orc.hyperedges(orc.synth(Spec.checker(w, h, c)), w)[0] == checker_hyperedges(w, h, c)
+    n = 65536
+    sp = Spec.hbands(n, n, 147) if pattern == "hbands" else Spec.checker(n, n, 7)
+    img = y.synth(pattern, n, n, bands=147 if pattern == "hbands" else 0, cell=7 if pattern == "checker" else 0)
+    r = y.scan(img)
+    rimg = ref.image_synth(sp)
+    assert np.array_equal(rimg.bytes(), img.bytes().reshape(n, -1)[:, : (n + 7) // 8])
+    want = rimg.counts(1, os.cpu_count() or 1)
+    assert np.array_equal(r.counts, want)
+    assert np.array_equal(r.boundaries, ref.boundaries(want))
+    assert r.total_runs == int(want.sum())
+    assert r.hyperedges == (147 if pattern == "hbands" else checker_hyperedges(n, n, 7))
