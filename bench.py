@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--counts-only", action="store_true", help="skip K3 (hyperedge total)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-collectives", action="store_true",
+                    help="N=1 only: run the N>1 side-stream/event structure with local copies (tests the graph)")
     ap.add_argument("--cpu-reps", type=int, default=3)
     return ap.parse_args()
 
@@ -221,49 +223,90 @@ def run_ours(a):
         raise SystemExit("multi-GPU bench uses column-independent patterns (hbands/checker/full)")
     for b in bufs:
         y.synth_device(a.pattern, Wimg, H, b.data_ptr(), pitch, stream=sptr, **kw)
-    counts = torch.empty(Ws, dtype=torch.int32, device="cuda")
+    # Per-step output slots (R of them, R > steps): the collectives of step i run on
+    # a side stream while the next steps scan into other slots, so the streaming
+    # pipeline (PDL between consecutive scans) never waits on a collective; a slot
+    # is only reused after its collectives completed (event wait).
+    R = a.steps + 1 if (dist is not None or a.emulate_collectives) else 2
+    counts2 = [torch.empty(Ws, dtype=torch.int32, device="cuda") for _ in range(R)]
     flags = torch.empty((Ws + 31) // 32 + 32, dtype=torch.int32, device="cuda")
     bounds = torch.empty(Ws, dtype=torch.int32, device="cuda")
-    totals = torch.zeros(4, dtype=torch.int64, device="cuda")
-    gathered = torch.empty(world * Ws, dtype=torch.int32, device="cuda") if world > 1 else None
+    totals2 = [torch.zeros(4, dtype=torch.int64, device="cuda") for _ in range(R)]
+    collective = dist is not None or a.emulate_collectives
+    gathered2 = [torch.empty(world * Ws, dtype=torch.int32, device="cuda") for _ in range(R)] if collective else None
+    tsum2 = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(R)] if collective else None
+    side = torch.cuda.Stream() if collective else None
     plan = y.Plan(Wimg, H, width_cnt=Ws, device=local)
     info = plan.info()
     with_links = not a.counts_only
+    pending = [None] * R
 
-    def step(i):
+    def step(i, s_main):
+        """One step: the scan of input i on s_main; for N>1 the all-gather of the
+        strip counts and the all-reduce of (runs, links) follow on the side stream,
+        overlapped with the next steps' scans."""
+        h = i % R
+        if pending[h] is not None:
+            s_main.wait_event(pending[h])  # an earlier step's collectives still read this slot
+            pending[h] = None
         b = bufs[i % nbuf]
-        plan.scan_device(b.data_ptr(), pitch, counts.data_ptr(), flags.data_ptr(), bounds.data_ptr(),
-                         totals.data_ptr(), sptr, with_links)
-        if dist is not None:
-            dist.all_gather_into_tensor(gathered, counts)
-            dist.all_reduce(totals[:2])
+        plan.scan_device(b.data_ptr(), pitch, counts2[h].data_ptr(), flags.data_ptr(), bounds.data_ptr(),
+                         totals2[h].data_ptr(), s_main.cuda_stream, with_links)
+        if not collective:
+            return
+        ev = torch.cuda.Event()
+        ev.record(s_main)
+        side.wait_event(ev)
+        with torch.cuda.stream(side):
+            if dist is not None:
+                dist.all_gather_into_tensor(gathered2[h], counts2[h])
+                tsum2[h].copy_(totals2[h][:2])
+                dist.all_reduce(tsum2[h])
+            else:  # --emulate-collectives (1 GPU): same stream/event structure, local copies
+                gathered2[h][:Ws].copy_(counts2[h])
+                tsum2[h].copy_(totals2[h][:2])
+        done = torch.cuda.Event()
+        done.record(side)
+        pending[h] = done
+
+    def join(s_main):
+        if collective:
+            s_main.wait_stream(side)
+        for k in range(R):
+            pending[k] = None
 
     for i in range(a.warmup):
-        step(i)
+        step(i, stream)
+    join(stream)
     torch.cuda.synchronize()
+    last = (a.warmup - 1) % R
+    counts, totals = counts2[last], totals2[last]
     # sanity: the synthetic workload's known answer
     tot = totals.cpu().tolist()
     exp = expected_hyperedges(a, Ws, H)
     if world == 1 and with_links and exp is not None and tot[2] != exp:
         raise SystemExit(f"hyperedge total {tot[2]} != expected {exp}: refusing to report a number")
+    if dist is not None:
+        # the all-gathered counts are the global counts (column strips, rank order)
+        g = gathered2[last]
+        if not torch.equal(g[rank * Ws:(rank + 1) * Ws], counts):
+            raise SystemExit("all-gathered counts do not match this rank's strip")
 
-    # The K timed steps are one CUDA graph (one kernel node per step, plus the
-    # NCCL nodes for N>1), so the device runs them back to back with no host
-    # launch overhead between steps -- the way a production caller drives scans.
+    # The K timed steps are one CUDA graph (two kernel nodes per step, plus the
+    # collective nodes on a forked side stream for N>1), so the device runs them
+    # back to back with no host launch overhead between steps.
     graph = torch.cuda.CUDAGraph()
     cap = torch.cuda.Stream()
     cap.wait_stream(stream)
     try:
         with torch.cuda.stream(cap):
             with torch.cuda.graph(graph, stream=cap, capture_error_mode="thread_local"):
-                csptr = torch.cuda.current_stream().cuda_stream
+                cs = torch.cuda.current_stream()
+                if collective:
+                    side.wait_stream(cs)
                 for i in range(a.steps):
-                    b = bufs[(a.warmup + i) % nbuf]
-                    plan.scan_device(b.data_ptr(), pitch, counts.data_ptr(), flags.data_ptr(), bounds.data_ptr(),
-                                     totals.data_ptr(), csptr, with_links)
-                    if dist is not None:
-                        dist.all_gather_into_tensor(gathered, counts)
-                        dist.all_reduce(totals[:2])
+                    step(a.warmup + i, cs)
+                join(cs)
         stream.wait_stream(cap)
         graph.replay()  # warm replay
         torch.cuda.synchronize()
@@ -272,6 +315,8 @@ def run_ours(a):
             raise
         print(f"[bench] CUDA-graph capture with collectives failed ({e!r}); timing eager steps", file=sys.stderr)
         graph = None
+        for k in range(R):
+            pending[k] = None
         torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -286,7 +331,8 @@ def run_ours(a):
         graph.replay()
     else:
         for i in range(a.steps):
-            step(a.warmup + i)
+            step(a.warmup + i, stream)
+        join(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
     if dist is not None:
@@ -351,6 +397,12 @@ def run_ours(a):
         except FileNotFoundError as e:
             cpu = {"unavailable": str(e)}
 
+    totals_json = {"total_runs": int(totals[0].item()), "links": int(totals[1].item()),
+                   "hyperedges": int(totals[2].item()), "n_boundaries": n_b}
+    if dist is not None:  # global (runs, links) from the all-reduce of the last timed step
+        g = tsum2[(a.warmup + a.steps - 1) % R].cpu().tolist()
+        totals_json = {"total_runs": g[0], "links": g[1], "hyperedges": g[0] - g[1] if with_links else -1,
+                       "n_boundaries_rank0_strip": n_b}
     if rank == 0:
         line = {
             "metric": "Gpixel/s", "value": round(value, 3), "unit": "Gpixel/s", "n_gpus": world,
@@ -373,8 +425,7 @@ def run_ours(a):
             "eager_launch_ms": round(sorted(eager_ms)[len(eager_ms) // 2], 5),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
             "gpu_launches": info.kernels_per_scan * a.steps,
-            "totals": {"total_runs": int(totals[0].item()), "links": int(totals[1].item()),
-                       "hyperedges": int(totals[2].item()), "n_boundaries": n_b},
+            "totals": totals_json,
         }
         print(json.dumps(line), flush=True)
     plan.close()
