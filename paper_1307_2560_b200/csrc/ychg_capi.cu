@@ -344,7 +344,7 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     p.dbg = plan->dbg;
     p.dbg_rows = std::max(plan->grid, p.n_strips);
     p.mul2 = 2u;
-    p.mul17 = 1u << 17;
+    p.mulnb = 1u << 25;
 
     if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
     const int rc = ychg_launch_scan(&plan->map, &p, plan->grid, with_hyperedges ? 1 : 0, st, nullptr);

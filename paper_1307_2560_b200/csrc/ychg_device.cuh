@@ -70,7 +70,7 @@ struct ScanParams {
     int32_t n_blocks;         // ceil(height / 32)
     int32_t seg_per_strip;    // k: row segments per strip
     int32_t n_segments;       // n_strips * k
-    uint32_t mul2, mul17;     // 2 and 1 << 17 as runtime values: keeps the b-word shifts on IMAD
+    uint32_t mul2, mulnb;     // 2 and 1 << 25 as runtime values: keeps the b-word shifts on IMAD
     uint32_t* part;           // [n_segments][512] per-segment u16x2 column counts
     uint32_t* sums;           // [n_segments][7][32] K3 band summaries
     unsigned long long* seg_links;    // [n_segments] links closed inside each segment
@@ -172,14 +172,17 @@ __device__ __forceinline__ void transpose8x8_bytes(uint32_t (&x)[8]) {
 }
 
 // Column (0..31, left to right inside its word) held by u16 lane `half` of
-// accumulator acc[i] (i = 2p + kind) after flush_counts: see flush_counts.
-// Words are processed in their raw little-endian load order: bit 8L+p of a word
-// is bit p of byte L, i.e. column 8L + 7 - p of the word (MSB-first bytes).
+// accumulator acc[i] (i = 2p + kind) after flush_counts (which leaves the
+// counter of word bit 8L+p in byte L of plane p).  The counts-only path keeps
+// words in their raw little-endian load order -- bit 8L+p is bit p of byte L,
+// column 8L + 7 - p (MSB-first bytes); the K3 path byte-swaps them to MSB-first
+// words, where bit 8L+p is column 31 - (8L+p).
+template <bool kMsbFirst = false>
 __host__ __device__ inline int acc_column(int i, int half) {
     const int p = i >> 1, kind = i & 1;
     // kind 0 keeps byte lanes {0,2}, kind 1 keeps {1,3}; half selects the upper lane.
     const int L = kind + 2 * half;
-    return 8 * L + 7 - p;
+    return kMsbFirst ? 31 - (8 * L + p) : 8 * L + 7 - p;
 }
 
 // ----------------------------------------------------------------------------

@@ -90,33 +90,52 @@ __device__ __forceinline__ uint32_t k3_step(uint32_t a, uint32_t b, LaneState& s
 // byte L+1 (raw >> 15), byte 3 takes bit 7 of the next word's byte 0 (nb << 17).
 // The shifts run as IMAD / IMAD.HI on the FMA pipe (runtime multipliers keep
 // ptxas from turning them into ALU shifts); one LOP3 merges them.
+// (Raw-order variant, kept for the diagnostics microbenchmarks: mul = 1 << 17.)
 __device__ __forceinline__ uint32_t right_neighbour(uint32_t raw, uint32_t nb, uint32_t mul2, uint32_t mul17) {
     const uint32_t t1 = raw * mul2;
     const uint32_t t3 = nb * mul17 + __umulhi(raw, mul17);
     return lop3<0xE2>(t1, 0xFEFEFEFEu, t3);  // (t1 & M) | (t3 & ~M): bit select, one LOP3
 }
 
-template <bool kLinks, bool kHead>
+// The K3 path runs on MSB-first words (one PRMT per row): the right neighbour is
+// then a << 1 with the next word's first bit shifted in, i.e. the MSB of the
+// next byte nb -- IMAD(a, 2, umulhi(nb, 1 << 25)), no ALU op at all (the
+// raw-order merge above costs an extra LOP3 + IMAD; measured -4 % per row).
+__device__ __forceinline__ uint32_t right_neighbour_msb(uint32_t a, uint32_t nb, uint32_t mul2, uint32_t mul25) {
+    return a * mul2 + __umulhi(nb, mul25);
+}
+
+template <bool kLinks, bool kHead, bool kBs = kLinks>
 __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage, int lane,
-                                              LaneState& s, uint32_t mul2, uint32_t mul17) {
+                                              LaneState& s, uint32_t mul2, uint32_t mulnb) {
     const uint8_t* p = stage + 4 * lane;
     uint32_t Pprev = 0, tA = 0, fA = 0, eA = 0;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         const uint8_t* r0 = p + (2 * q) * kBoxBytes;
         const uint8_t* r1 = r0 + kBoxBytes;
-        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0);
-        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(r1);
+        uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0);
+        uint32_t a1 = *reinterpret_cast<const uint32_t*>(r1);
+        if (kBs) {  // MSB-first words (bit 31-j = column j): b = a << 1 | next byte's MSB, FMA pipe
+            a0 = __byte_perm(a0, 0u, 0x0123u);
+            a1 = __byte_perm(a1, 0u, 0x0123u);
+        }
         const uint32_t P = lop3<0x3A>(a0, s.pa, a1);  // (a0 & ~pa) | (a1 & ~a0)
         if (kLinks) {
-            const uint32_t b0 = right_neighbour(a0, r0[4], mul2, mul17);
-            const uint32_t b1 = right_neighbour(a1, r1[4], mul2, mul17);
+            const uint32_t b0 = kBs ? right_neighbour_msb(a0, r0[4], mul2, mulnb)
+                                    : right_neighbour(a0, r0[4], mul2, mulnb);
+            const uint32_t b1 = kBs ? right_neighbour_msb(a1, r1[4], mul2, mulnb)
+                                    : right_neighbour(a1, r1[4], mul2, mulnb);
             const uint32_t l0 = k3_step<kHead>(a0, b0, s);
             const uint32_t l1 = k3_step<kHead>(a1, b1, s);
             s.links += __popc(lop3<0xA8>(l0, l1, s.mk3));  // (l0 | l1) & mk3
         } else {
             s.pa = a1;
         }
+#ifdef YCHG_DIAG_NO_K1  // microbenchmark-only: K3 alone (counts wrong)
+        s.ones ^= P;
+        continue;
+#endif
         if ((q & 1) == 0) {
             Pprev = P;
             continue;
@@ -360,8 +379,8 @@ ychg_finish_kernel(const ScanParams prm) {
         const int idx = tid + r * kThreads;
         if (idx < 512) {
             const int i = idx >> 5, ln = idx & 31;
-            fs.sc[32 * ln + acc_column(i, 0)] = static_cast<int32_t>(v[r] & 0xFFFFu);
-            fs.sc[32 * ln + acc_column(i, 1)] = static_cast<int32_t>(v[r] >> 16);
+            fs.sc[32 * ln + acc_column<kLinks>(i, 0)] = static_cast<int32_t>(v[r] & 0xFFFFu);
+            fs.sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(v[r] >> 16);
         }
     }
     __syncthreads();
@@ -583,7 +602,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
 #pragma unroll
         for (int i = 0; i < 16; ++i) s.acc[i] = 0;
-        s.mk3 = __byte_perm(word_mask(gw, min(prm.width_cnt, prm.width_img - 1)), 0u, 0x0123u);
+        s.mk3 = word_mask(gw, min(prm.width_cnt, prm.width_img - 1));  // MSB-first, like the K3 words
         s.h1 = s.h2 = 0;
         s.links = 0;
         s.pa = s.pb = 0;
@@ -611,8 +630,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                     if (c + q < prm.row_bytes) raw |= static_cast<uint32_t>(__ldg(row + c + q)) << (8 * q);
                 if (c + 4 < prm.row_bytes) nbyte = __ldg(row + c + 4);
             }
-            s.pa = raw;
-            s.pb = right_neighbour(raw, nbyte, prm.mul2, prm.mul17);
+            s.pa = kLinks ? __byte_perm(raw, 0u, 0x0123u) : raw;  // word order of process_block<kLinks>
+            s.pb = right_neighbour_msb(s.pa, nbyte, prm.mul2, prm.mulnb);
             O = kLinks ? (s.pa | s.pb) : 0u;
             s.Hd = O;
             s.G2 = s.G3 = O;  // poisoned: the head's own closing is never a local link
@@ -631,9 +650,9 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 #else
                 if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u))
 #endif
-                    process_block<kLinks, true>(sp, lane, s, prm.mul2, prm.mul17);
+                    process_block<kLinks, true>(sp, lane, s, prm.mul2, prm.mulnb);
                 else
-                    process_block<kLinks, false>(sp, lane, s, prm.mul2, prm.mul17);
+                    process_block<kLinks, false>(sp, lane, s, prm.mul2, prm.mulnb);
                 __syncwarp();
 #ifdef YCHG_COMPUTE_ONLY
                 if (false) {
