@@ -462,6 +462,9 @@ def run_ours(a):
 
 def main():
     a = parse()
+    if os.environ.get("YCHG_BENCH_WATCHDOG"):  # diagnostics: dump the Python stacks if a run stalls
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["YCHG_BENCH_WATCHDOG"]), exit=True)
     if a.impl == "reference":
         run_reference_arm(a)
     else:

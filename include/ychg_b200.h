@@ -198,6 +198,8 @@ YCHG_API int ychg_plan_last_ms(ychg_plan* plan, float* scan_ms, float* finish_ms
  * min(capacity, 4*grid*32) stamps. */
 YCHG_API int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, int32_t capacity,
                                     int32_t* n_ctas);
+/* Diagnostics: the stamp ring (mapped host memory) without synchronising. */
+YCHG_API int ychg_plan_debug_peek(ychg_plan* plan, uint64_t* host_out, int32_t capacity);
 
 /* ---- helpers ---- */
 /* Bit-exact with reference synth() for every pattern (synth.cpp:38-104);

@@ -78,6 +78,7 @@ _SIGS = {
     "ychg_plan_set_timing": (ctypes.c_int, [_vp, _i32]),
     "ychg_plan_last_ms": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
     "ychg_plan_debug_stamps": (ctypes.c_int, [_vp, _i32, _vp, _i32, ctypes.POINTER(_i32)]),
+    "ychg_plan_debug_peek": (ctypes.c_int, [_vp, _vp, _i32]),
     "ychg_synth_device": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64, _vp, _i64, _vp]),
     "ychg_device_alloc": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.POINTER(_vp)]),
     "ychg_device_free": (ctypes.c_int, [ctypes.c_int, _vp]),
@@ -441,6 +442,13 @@ class Plan:
         _check(_lib.ychg_plan_debug_stamps(self._h, 1, out.ctypes.data_as(_vp), out.size, ctypes.byref(n)),
                "debug_stamps")
         return out[:, : n.value]
+
+    def debug_peek(self):
+        """The stamp ring (4, max(grid, n_strips), 32) read without synchronising (diagnostics)."""
+        rows = max(self.info().grid, self.info().n_strips)
+        out = np.zeros((4, rows, 32), dtype=np.uint64)
+        _check(_lib.ychg_plan_debug_peek(self._h, out.ctypes.data_as(_vp), out.size), "debug_peek")
+        return out
 
     def scan_device(self, d_bits: int, pitch: int, d_counts: int, d_flags: int, d_boundaries: int,
                     d_totals: int, stream: int = 0, with_hyperedges: bool = True) -> None:

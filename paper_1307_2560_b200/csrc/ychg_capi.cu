@@ -89,7 +89,8 @@ struct ychg_plan {
     bool timing = false;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_recorded = false;
-    unsigned long long* dbg = nullptr;  // per-CTA %globaltimer stamps of the last scan
+    unsigned long long* dbg = nullptr;  // per-CTA %globaltimer stamps (device view of dbg_host)
+    unsigned long long* dbg_host = nullptr;  // mapped pinned memory: readable while kernels run
 };
 
 namespace {
@@ -232,7 +233,7 @@ void ychg_plan_destroy(ychg_plan* plan) {
     cudaGetDevice(&prev);
     cudaSetDevice(plan->device);
     if (plan->ws) cudaFree(plan->ws);
-    if (plan->dbg) cudaFree(plan->dbg);
+    if (plan->dbg_host) cudaFreeHost(plan->dbg_host);
     for (auto& e : plan->ev)
         if (e) cudaEventDestroy(e);
     cudaSetDevice(prev);
@@ -275,20 +276,33 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
                            int32_t* n_ctas) {
     if (!plan) return fail(YCHG_ERR_INVALID, "plan_debug_stamps: NULL plan");
     CK(cudaSetDevice(plan->device));
+    const int64_t bytes = int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4;
     if (enable && !plan->dbg && plan->grid > 0) {
-        CK(cudaMalloc(&plan->dbg, int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4));
-        CK(cudaMemset(plan->dbg, 0, int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4));
+        // zero-copy host memory, so a stalled pipeline can still be inspected (debug_peek)
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&plan->dbg_host), bytes, cudaHostAllocMapped));
+        std::memset(plan->dbg_host, 0, size_t(bytes));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&plan->dbg), plan->dbg_host, 0));
     }
     if (!enable && plan->dbg) {
-        CK(cudaFree(plan->dbg));
-        plan->dbg = nullptr;
+        CK(cudaDeviceSynchronize());
+        CK(cudaFreeHost(plan->dbg_host));
+        plan->dbg = plan->dbg_host = nullptr;
     }
     if (n_ctas) *n_ctas = plan->grid;
     if (host_out && plan->dbg) {
-        const int64_t n = std::min<int64_t>(capacity, int64_t(plan->grid) * 32 * 4);
+        const int64_t n = std::min<int64_t>(capacity, bytes / 8);
         CK(cudaDeviceSynchronize());
-        CK(cudaMemcpy(host_out, plan->dbg, n * 8, cudaMemcpyDeviceToHost));
+        std::memcpy(host_out, plan->dbg_host, size_t(n) * 8);
     }
+    return YCHG_OK;
+}
+
+// Diagnostics: copy the stamp ring without synchronising (works while kernels stall).
+int ychg_plan_debug_peek(ychg_plan* plan, uint64_t* host_out, int32_t capacity) {
+    if (!plan || !plan->dbg_host) return fail(YCHG_ERR_INVALID, "plan_debug_peek: stamps not enabled");
+    const int64_t bytes = int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4;
+    std::memcpy(host_out, const_cast<const unsigned long long*>(plan->dbg_host),
+                size_t(std::min<int64_t>(capacity, bytes / 8)) * 8);
     return YCHG_OK;
 }
 

@@ -414,8 +414,10 @@ ychg_finish_kernel(const ScanParams prm) {
     // writes anything (normally long done by now).
     if (tid == 0 && scan_no > 0) {
         const unsigned long long need = scan_no * static_cast<unsigned long long>(prm.n_strips);
+        YCHG_STAMP_AT(28, scan_no);
         while (ld_acquire(prm.fin_all) < need) {
         }
+        YCHG_STAMP(29);
     }
     __syncthreads();
     const bool last_strip = (s == prm.n_strips - 1);
@@ -707,8 +709,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         const unsigned long long scan_idx = static_cast<unsigned long long>(misc[kWarps + 2]);
         const int64_t par = static_cast<int64_t>(scan_idx & 1ull);
         if (tid == 0 && scan_idx >= 2) {
+            const int ring = static_cast<int>(scan_idx & 3ull);
+            YCHG_STAMP_AT(9, scan_idx);
+            YCHG_STAMP(10);
             while (ld_acquire(prm.fin_loaded + strip) < scan_idx - 1) {
             }
+            YCHG_STAMP(11);
         }
         __syncthreads();
         // ---- CTA merge: counts (sum over warps, coalesced u16x2 words), K3 (compose in row order).
