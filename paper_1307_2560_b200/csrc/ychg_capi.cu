@@ -185,14 +185,17 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
                                                           ychg_dev::kSmemTotal));
         if (per_sm < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
         plan->grid = std::min(plan->grid, per_sm * sms);
+        if ((p.n_segments + plan->grid - 1) / plan->grid > ychg_dev::kMaxSegPerCta)
+            return fail(YCHG_ERR_INVALID, "plan_create: %d segments over %d CTAs exceed %d per CTA", p.n_segments,
+                        plan->grid, ychg_dev::kMaxSegPerCta);
         const int64_t S = p.n_strips, G = p.n_segments;
         // part / sums / seg_links / seg_status are double-buffered by scan parity
         const int64_t sz_part = 2 * G * 512 * 4, sz_sums = 2 * G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = 2 * G * 8;
         if (height >= (1 << 22))
             return fail(YCHG_ERR_INVALID, "plan_create: height %d >= 2^22 rows is not supported", height);
         const int64_t sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
-        // order: part | sums | seg_links | seg_ticket | seg_status | fin_ticket | fin_all | rec
-        plan->ws_bytes = sz_part + sz_sums + 3 * sz_seg + 2 * S * 8 + 64 + sz_rec + 64;
+        // order: part | sums | seg_links | seg_ticket | seg_status | fin_ticket | fin_all | fin_loaded[2][S] | rec
+        plan->ws_bytes = sz_part + sz_sums + 3 * sz_seg + 3 * S * 8 + 64 + sz_rec + 64;
         cudaError_t e = cudaMalloc(&plan->ws, plan->ws_bytes);
         if (e != cudaSuccess) {
             plan->ws = nullptr;
@@ -220,7 +223,7 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
         p.fin_all = reinterpret_cast<unsigned long long*>(w);
         w += 64;
         p.fin_loaded = reinterpret_cast<unsigned long long*>(w);
-        w += S * 8;
+        w += 2 * S * 8;
         p.rec = reinterpret_cast<ychg_dev::StripRecord*>(w);
     }
     *out = plan.release();

@@ -34,6 +34,7 @@ constexpr int kSumPlanes = 7;                    // K3 band summary planes (see 
 constexpr int kMaxSegmentRows = 65504;           // u16 SWAR accumulators: counts <= rows/2 < 2^15
 
 constexpr int kMaxSegPerStrip = 128;            // the finisher keeps k summaries in smem
+constexpr int kMaxSegPerCta = 64;               // segments one streaming CTA processes per scan
 
 // Shared-memory layout of the scan kernel (bytes).
 constexpr int kSmemStages = kWarps * kStages * kStageBytes;            // 147456
@@ -78,7 +79,8 @@ struct ScanParams {
     unsigned long long* seg_status;   // [n_segments] epoch tag of the last merged segment (release)
     unsigned long long* fin_ticket;   // [n_strips] scans started per strip finisher (monotonic)
     unsigned long long* fin_all;      // [1] strip finishers completed (monotonic)
-    unsigned long long* fin_loaded;   // [n_strips] scans whose workspace the finisher has loaded
+    unsigned long long* fin_loaded;   // [2][n_strips] per buffer half: 1 + the last scan whose
+                                      // partials of that half the strip's finisher has loaded
     struct StripRecord* rec;  // [n_strips] published by each strip's finisher
     long long* totals;        // ychg_totals {total_runs, links, hyperedges, n_boundaries}
     int32_t* counts;          // [width_cnt] final per-column counts

@@ -302,19 +302,22 @@ ychg_finish_kernel(const ScanParams prm) {
     const int g0 = s * k;
     constexpr int kSumWords = kSumPlanes * 32;
 
-    // Let the next scan's streaming kernel launch right away (it only needs SMs;
-    // it waits on fin_loaded before reusing this scan's workspace).
-    asm volatile("griddepcontrol.launch_dependents;");
-    // (0) this strip's scan number, then wait until all k segments of this scan merged
+    // (0) this strip's scan number -- taken BEFORE releasing the next scan's
+    // streaming kernel, so tickets follow launch order (a later scan's finisher
+    // can never draw an earlier number) -- then let the next scan launch right
+    // away (it only needs SMs; it waits on fin_loaded before reusing this scan's
+    // workspace), then wait until all k segments of this scan merged.
     unsigned long long scan_no = 0;
     if (tid == 0) {
         scan_no = atomicAdd(prm.fin_ticket + s, 1ull);
         fs.base = static_cast<long long>(scan_no);
     }
     __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;");
     scan_no = static_cast<unsigned long long>(fs.base);
     const uint32_t epoch = static_cast<uint32_t>(scan_no % 4095ull) + 1u;
     const int ring = static_cast<int>(scan_no & 3ull);
+    if (tid == 0) YCHG_STAMP_AT(16, scan_no + 1);
     // Segment partials are double-buffered by scan parity (the next scan's
     // stream kernel writes the other half while this finisher reads).
     const int64_t par = static_cast<int64_t>(scan_no & 1ull);
@@ -335,7 +338,10 @@ ychg_finish_kernel(const ScanParams prm) {
         }
     }
     __syncthreads();
-    if (tid == 0) YCHG_STAMP(21);
+    if (tid == 0) {
+        YCHG_STAMP(21);
+        YCHG_STAMP_AT(30, scan_no + 1);  // identity stamps: scan number (+1) at each stage
+    }
 
     // (1) one batch of loads per 8 segments: partial counts (512 u16x2 words per
     //     segment over the CTA) and the K3 summaries (8 x 224 words).
@@ -386,9 +392,10 @@ ychg_finish_kernel(const ScanParams prm) {
     __syncthreads();
     if (tid == 0) {
         YCHG_STAMP(24);
+        YCHG_STAMP_AT(31, scan_no + 1);
         // this scan's workspace for strip s is in smem: the next scan's stream
         // kernel may overwrite it (it waits on this before its first partial write)
-        st_release(prm.fin_loaded + s, scan_no + 1);
+        st_release(prm.fin_loaded + par * prm.n_strips + s, scan_no + 1);
     }
 
     // (2) flags strictly inside the strip (columns 1..1023), counts out, run total
@@ -418,6 +425,7 @@ ychg_finish_kernel(const ScanParams prm) {
         while (ld_acquire(prm.fin_all) < need) {
         }
         YCHG_STAMP(29);
+        YCHG_STAMP_AT(19, scan_no + 1);
     }
     __syncthreads();
     const bool last_strip = (s == prm.n_strips - 1);
@@ -470,6 +478,7 @@ ychg_finish_kernel(const ScanParams prm) {
         for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
         if (lane == 0) {
             YCHG_STAMP(27);
+            YCHG_STAMP_AT(18, scan_no + 1);
             fs.edge = (first != carry_last) ? 1u : 0u;
             fs.base = off;
             if (last_strip) prm.totals[3] = off + fs.edge + inside;
@@ -544,6 +553,7 @@ ychg_finish_kernel(const ScanParams prm) {
     __syncthreads();
     if (tid == 0) {
         YCHG_STAMP(22);
+        YCHG_STAMP_AT(17, scan_no + 1);
         __threadfence();
         atomicAdd(prm.fin_all, 1ull);
     }
@@ -565,22 +575,30 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     const int warp = tid >> 5;
     const int lane = tid & 31;
 
-    // Let this scan's finisher kernel launch now: its CTAs are small, co-reside
-    // with ours and wait on the per-segment flags (programmatic dependent launch).
-    asm volatile("griddepcontrol.launch_dependents;");
+    // This CTA's scan number for each of its segments, drawn BEFORE releasing the
+    // finisher (and, through it, the next scan): tickets then follow launch order
+    // even when consecutive scans' CTAs overlap.
+    __shared__ unsigned long long seg_tick[kMaxSegPerCta];
     const unsigned long long t_entry = globaltimer();
     if (tid == 0) {
         for (int i = 0; i < kWarps * kStages; ++i) mbar_init(&bars[i], 1);
+        int i = 0;
+        for (int sg = blockIdx.x; sg < prm.n_segments && i < kMaxSegPerCta; sg += gridDim.x, ++i)
+            seg_tick[i] = atomicAdd(prm.seg_ticket + sg, 1ull);
     }
     fence_proxy_async();
     __syncthreads();
+    // Let this scan's finisher kernel launch now: its CTAs are small, co-reside
+    // with ours and wait on the per-segment flags (programmatic dependent launch).
+    asm volatile("griddepcontrol.launch_dependents;");
 
     uint8_t* my_stages = stages + warp * kStages * kStageBytes;
     uint64_t* my_bars = bars + warp * kStages;
     uint32_t it = 0;  // blocks consumed by this warp so far (stage = it % kStages)
 
     const int k = prm.seg_per_strip;
-    for (int seg = blockIdx.x; seg < prm.n_segments; seg += gridDim.x) {
+    int seg_i = 0;
+    for (int seg = blockIdx.x; seg < prm.n_segments; seg += gridDim.x, ++seg_i) {
         const int strip = seg / k;
         const int j = seg - strip * k;
         const int sb0 = seg_first_block(j, k, prm.n_blocks);
@@ -594,11 +612,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 
         // this segment's scan number (agrees with the finisher's strip ticket)
         if (tid == 0) {
-            const unsigned long long t = atomicAdd(prm.seg_ticket + seg, 1ull);
+            const unsigned long long t = seg_tick[seg_i];
             misc[kWarps + 1] = static_cast<int>(t % 4095ull) + 1;
             misc[kWarps + 2] = static_cast<int>(t);  // scans before this one (< 2^31 per plan)
             const int ring = static_cast<int>(t & 3ull);
             YCHG_STAMP_AT(0, t_entry);
+            YCHG_STAMP_AT(15, t + 1);
         }
         LaneState s;
         s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
@@ -712,9 +731,13 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             const int ring = static_cast<int>(scan_idx & 3ull);
             YCHG_STAMP_AT(9, scan_idx);
             YCHG_STAMP(10);
-            while (ld_acquire(prm.fin_loaded + strip) < scan_idx - 1) {
+            // per half: the NEXT scan's finisher (other half) may load first, so a
+            // single per-strip counter could release us before scan_idx-2's
+            // finisher has read this half (then its flags would be overwritten).
+            while (ld_acquire(prm.fin_loaded + par * prm.n_strips + strip) < scan_idx - 1) {
             }
             YCHG_STAMP(11);
+            YCHG_STAMP_AT(12, scan_idx + 1);
         }
         __syncthreads();
         // ---- CTA merge: counts (sum over warps, coalesced u16x2 words), K3 (compose in row order).
@@ -745,6 +768,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         if (tid == 0) {
             const int ring = misc[kWarps + 2] & 3;
             YCHG_STAMP(20);
+            YCHG_STAMP_AT(13, static_cast<unsigned long long>(misc[kWarps + 2]) + 1);
             st_release(prm.seg_status + par * prm.n_segments + seg, static_cast<unsigned long long>(misc[kWarps + 1]));
         }
         __syncthreads();
@@ -752,6 +776,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     if (tid == 0 && prm.n_segments > 0) {
         const int ring = misc[kWarps + 2] & 3;
         YCHG_STAMP(23);
+        YCHG_STAMP_AT(14, static_cast<unsigned long long>(misc[kWarps + 2]) + 1);
     }
 }
 
