@@ -338,6 +338,10 @@ def run_ours(a):
     if dist is not None:
         dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
+    if world == 1 and with_links and exp is not None and graph is not None:
+        last_t = totals2[(a.warmup + a.steps - 1) % R] if R > 2 else totals2[(a.warmup + a.steps - 1) & 1]
+        if int(last_t[2].item()) != exp:
+            raise SystemExit("hyperedge total of the timed graph's last step != expected: refusing to report")
     # The north-star subset (K1 + K2: counts, change flags, boundaries, no K3
     # hyperedge total) timed the same way on the same inputs, reported beside the
     # headline (1 GPU only).

@@ -257,6 +257,7 @@ struct FinishSmem {
     long long red[kWarps];
     long long red2[kWarps];
     long long base;
+    unsigned long long seglinks;  // links closed inside the strip's segments (loaded with the partials)
     uint32_t edge;                // flag of the strip's first column
 };
 
@@ -327,6 +328,7 @@ ychg_finish_kernel(const ScanParams prm) {
     const unsigned long long* seglinks_p = prm.seg_links + par * G;
     const unsigned long long* segstat_p = prm.seg_status + par * G;
     if (warp == 0) {
+        unsigned long long sl = 0;
         for (int jb = 0; jb < k; jb += 32) {
             const int j = jb + lane;
             const bool act = j < k;
@@ -335,7 +337,13 @@ ychg_finish_kernel(const ScanParams prm) {
                 if (!ok) ok = static_cast<uint32_t>(ld_acquire(segstat_p + g0 + (act ? j : 0))) == epoch;
                 if (__all_sync(0xFFFFFFFFu, ok)) break;
             }
+            // every per-segment input must be read before fin_loaded releases this
+            // half to scan t+2 -- including the segment link counts
+            if (kLinks && act) sl += __ldcg(seglinks_p + g0 + j);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xFFFFFFFFu, sl, o);
+        if (lane == 0) fs.seglinks = sl;
     }
     __syncthreads();
     if (tid == 0) {
@@ -486,11 +494,7 @@ ychg_finish_kernel(const ScanParams prm) {
     } else if (warp == 1) {
         // (4) release (runs, links) for the totals
         const unsigned long long links = strip_links;
-        unsigned long long sl = 0;  // links closed inside the strip's segments (lane-parallel loads)
-        if (kLinks)
-            for (int g = lane; g < k; g += 32) sl += __ldcg(seglinks_p + g0 + g);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xFFFFFFFFu, sl, o);
+        const unsigned long long sl = fs.seglinks;  // read before fin_loaded was released
         if (lane == 0) {
             long long runs = 0;
             for (int w = 0; w < kWarps; ++w) runs += fs.red[w];

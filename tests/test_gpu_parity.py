@@ -335,3 +335,61 @@ def test_max_size_65536(gpu, orc, ref, pattern):
     assert np.array_equal(r.boundaries, ref.boundaries(want))
     assert r.total_runs == int(want.sum())
     assert r.hyperedges == (147 if pattern == "hbands" else checker_hyperedges(n, n, 7))
+
+
+@pytest.mark.parametrize("segments", [None, 2, 3, 4])
+def test_pipelined_graph_distinct_images(gpu, orc, segments, monkeypatch):
+    """CUDA-graph replays of back-to-back scans of DISTINCT images, full and
+    counts-only interleaved, each into its own outputs, with forced row-segment
+    counts (regression: a cross-scan race once let scan t overwrite segment flags
+    scan t-2's finisher had not read -- a stall -- and scan tickets could be drawn
+    out of launch order -- mixed images).  A stall fails after 20 s."""
+    import time
+
+    import torch
+
+    y = gpu
+    if segments is not None:
+        monkeypatch.setenv("YCHG_SEGMENTS", str(segments))
+    W, H = 3100, 2600
+    specs = [Spec.random(W, H, 0.5, 21), Spec.hbands(W, H, 40), Spec.checker(W, H, 5), Spec.random(W, H, 0.3, 22),
+             Spec.frame(W, H)]
+    pitch = y.pitch_for(W)
+    imgs = []
+    for sp in specs:
+        bits = orc.synth(sp)
+        dev = np.zeros((H, pitch), np.uint8)
+        dev[:, : bits.shape[1]] = bits
+        counts = orc.counts(bits, W)
+        imgs.append((torch.from_numpy(dev).cuda(), counts, orc.boundaries(counts), orc.hyperedges(bits, W)[0]))
+    plan = y.Plan(W, H)
+    n = 24
+    outs = [(torch.full((W,), -7, dtype=torch.int32, device="cuda"), torch.zeros(W // 32 + 64, dtype=torch.int32, device="cuda"),
+             torch.full((W,), -7, dtype=torch.int32, device="cuda"), torch.zeros(4, dtype=torch.int64, device="cuda"))
+            for _ in range(n)]
+    stream = torch.cuda.current_stream()
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        with torch.cuda.graph(g, stream=cap):
+            cs = torch.cuda.current_stream().cuda_stream
+            for i in range(n):
+                c, f, b, t = outs[i]
+                plan.scan_device(imgs[i % len(imgs)][0].data_ptr(), pitch, c.data_ptr(), f.data_ptr(), b.data_ptr(),
+                                 t.data_ptr(), cs, i % 3 != 2)
+    stream.wait_stream(cap)
+    for rep in range(4):
+        g.replay()
+        t0 = time.time()
+        while not stream.query():
+            assert time.time() - t0 < 20, f"pipelined graph stalled (replay {rep}, segments {segments})"
+            time.sleep(0.01)
+    for i in range(n):
+        c, _, b, t = outs[i]
+        _, counts, bounds, he = imgs[i % len(imgs)]
+        tt = t.cpu().tolist()
+        assert np.array_equal(c.cpu().numpy(), counts), i
+        assert tt[3] == bounds.size and np.array_equal(b.cpu().numpy()[: bounds.size], bounds), i
+        assert tt[2] == (he if i % 3 != 2 else -1), i
+    plan.close()
