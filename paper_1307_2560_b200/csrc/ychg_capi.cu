@@ -102,6 +102,18 @@ int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out) {
     const int max_seg_blocks = ychg_dev::kMaxSegmentRows / ychg_dev::kBlockRows;
     int kmin = (n_blocks + max_seg_blocks - 1) / max_seg_blocks;
     if (kmin < 1) kmin = 1;
+    // Large masks: few long CTAs, about half an SM's worth per scan.  Each CTA pays
+    // a fixed ramp + merge (~5 us) and back-to-back scans fill the other half of the
+    // SMs (two streaming CTAs per SM, programmatic dependent launch), so fewer,
+    // longer CTAs amortise it: measured at 21000^2 (21 strips, K=100 graph),
+    // k = 3/4/5/6/7/8 -> 12.7/12.8/13.2/13.3/13.6/14.0 us per scan.
+    if (static_cast<long long>(n_strips) * n_blocks >= 8LL * sms * ychg_dev::kWarps) {
+        int k = std::max(1, (sms / 2 + std::max(1, n_strips) / 2) / std::max(1, n_strips));  // round(sms/2 / strips)
+        k = std::max(k, kmin);
+        k = std::min(k, std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip)));
+        *grid_out = static_cast<int>(std::min<long long>(sms, static_cast<long long>(n_strips) * k));
+        return k;
+    }
     double best = 1e300;
     int best_k = kmin;
     const int kmax = std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip));
