@@ -196,12 +196,20 @@ def run_ours(a):
 
     world, rank, local = dist_env()
     assert world == a.gpus, f"--gpus {a.gpus} but WORLD_SIZE={world}"
+    # YCHG_BENCH_SHARE_GPU=1 (function test of the N>1 code path on a 1-GPU box:
+    # ranks share cuda:0 and talk over gloo; no number from such a run is valid)
+    share = os.environ.get("YCHG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     y._check(y._lib.ychg_set_device(local), "set_device")
     dist = None
     if world > 1:
         import torch.distributed as dist_mod
-        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist_mod.init_process_group("gloo")
+        else:
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
