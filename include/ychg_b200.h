@@ -172,6 +172,12 @@ YCHG_API int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, i
  * (multi-GPU column strips).  A plan is not safe for concurrent use. */
 YCHG_API int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t height,
                      ychg_plan** out);
+/* Plan flags: YCHG_PLAN_LATENCY sizes the launch for one isolated scan (all SMs
+ * busy) instead of back-to-back pipelined scans (the default: fewer, longer CTAs
+ * for large masks so consecutive scans overlap). */
+#define YCHG_PLAN_LATENCY 1
+YCHG_API int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_t height, int32_t flags,
+                                 ychg_plan** out);
 YCHG_API void ychg_plan_destroy(ychg_plan* plan);
 YCHG_API int ychg_plan_get_info(const ychg_plan* plan, ychg_plan_info* out);
 

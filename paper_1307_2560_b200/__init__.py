@@ -72,6 +72,7 @@ _SIGS = {
     "ychg_hypergraph_copy": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "ychg_hypergraph_destroy": (None, [_vp]),
     "ychg_plan_create": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    "ychg_plan_create_ex": (ctypes.c_int, [ctypes.c_int, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "ychg_plan_destroy": (None, [_vp]),
     "ychg_plan_get_info": (ctypes.c_int, [_vp, ctypes.POINTER(PlanInfo)]),
     "ychg_scan_device": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
@@ -402,13 +403,16 @@ def decompose(source, strategy: ScanStrategy = ScanStrategy.serial()) -> Hypergr
 class Plan:
     """Geometry-specific launch plan + workspace on one device (ychg_plan_*)."""
 
-    def __init__(self, width_img: int, height: int, width_cnt: int | None = None, device: int = 0):
+    def __init__(self, width_img: int, height: int, width_cnt: int | None = None, device: int = 0,
+                 latency: bool = False):
+        """latency=True sizes the launch for isolated scans (YCHG_PLAN_LATENCY); the
+        default favours back-to-back (pipelined / graph-captured) scans."""
         self.device = device
         self.width_img, self.height = int(width_img), int(height)
         self.width_cnt = self.width_img if width_cnt is None else int(width_cnt)
         h = _vp()
-        _check(_lib.ychg_plan_create(device, self.width_img, self.width_cnt, self.height, ctypes.byref(h)),
-               "plan_create")
+        _check(_lib.ychg_plan_create_ex(device, self.width_img, self.width_cnt, self.height, int(bool(latency)),
+                                        ctypes.byref(h)), "plan_create")
         self._h = h
 
     def close(self) -> None:

@@ -98,7 +98,7 @@ namespace {
 // Pick the number of row segments per strip minimising the modelled makespan of
 // the persistent streaming kernel: waves of segments over the SMs, 8 warp bands
 // per segment, +1 block-time per segment for pipeline fill and the CTA merge.
-int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out) {
+int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out, bool latency = false) {
     const int max_seg_blocks = ychg_dev::kMaxSegmentRows / ychg_dev::kBlockRows;
     int kmin = (n_blocks + max_seg_blocks - 1) / max_seg_blocks;
     if (kmin < 1) kmin = 1;
@@ -107,7 +107,9 @@ int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out) {
     // SMs (two streaming CTAs per SM, programmatic dependent launch), so fewer,
     // longer CTAs amortise it: measured at 21000^2 (21 strips, K=100 graph),
     // k = 3/4/5/6/7/8 -> 12.7/12.8/13.2/13.3/13.6/14.0 us per scan.
-    if (static_cast<long long>(n_strips) * n_blocks >= 8LL * sms * ychg_dev::kWarps) {
+    // (A plan made for one isolated scan at a time -- the host entry points --
+    // keeps every SM busy instead: YCHG_PLAN_LATENCY.)
+    if (!latency && static_cast<long long>(n_strips) * n_blocks >= 8LL * sms * ychg_dev::kWarps) {
         int k = std::max(1, (sms / 2 + std::max(1, n_strips) / 2) / std::max(1, n_strips));  // round(sms/2 / strips)
         k = std::max(k, kmin);
         k = std::min(k, std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip)));
@@ -159,6 +161,11 @@ int ychg_set_device(int device) {
 }
 
 int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t height, ychg_plan** out) {
+    return ychg_plan_create_ex(device, width_img, width_cnt, height, 0, out);
+}
+
+int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_t height, int32_t flags,
+                        ychg_plan** out) {
     if (!out) return fail(YCHG_ERR_INVALID, "plan_create: out is NULL");
     *out = nullptr;
     if (width_img < 0 || height < 0 || width_cnt < 0 || width_cnt > width_img)
@@ -179,7 +186,7 @@ int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t h
     p.n_strips = (width_cnt + ychg_dev::kStripCols - 1) / ychg_dev::kStripCols;
     p.n_blocks = (height + ychg_dev::kBlockRows - 1) / ychg_dev::kBlockRows;
     if (p.n_strips > 0 && p.n_blocks > 0) {
-        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid);
+        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid, (flags & YCHG_PLAN_LATENCY) != 0);
         // experiment hooks (benchmarking only): force the segments per strip / grid
         if (const char* v = getenv("YCHG_SEGMENTS"); v && *v) {
             p.seg_per_strip = std::max(1, atoi(v));
@@ -639,7 +646,8 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
         ychg_plan_destroy(c.plan);
         c.plan = nullptr;
         c.plan_w = c.plan_h = -1;
-        if (const int rc = ychg_plan_create(device, width, width, height, &c.plan)) return rc;
+        // one scan per call, synchronised: size the plan for latency, not pipelining
+        if (const int rc = ychg_plan_create_ex(device, width, width, height, YCHG_PLAN_LATENCY, &c.plan)) return rc;
         c.plan_w = width;
         c.plan_h = height;
     }
