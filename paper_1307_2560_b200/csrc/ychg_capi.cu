@@ -111,9 +111,14 @@ int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out, bool lat
     // keeps every SM busy instead: YCHG_PLAN_LATENCY.)
     if (!latency && static_cast<long long>(n_strips) * n_blocks >= 8LL * sms * ychg_dev::kWarps) {
         int k = std::max(1, (sms / 2 + std::max(1, n_strips) / 2) / std::max(1, n_strips));  // round(sms/2 / strips)
+        // ... but segments of at most 16384 rows: a very tall mask is better served by
+        // two resident CTAs per SM than by few extremely long ones (65536^2, K=30:
+        // k=2/128 CTAs -> 110 us full, 140 us counts-only; k=4/256 CTAs -> 110 / 110-119)
+        k = std::max(k, (n_blocks + 511) / 512);
         k = std::max(k, kmin);
         k = std::min(k, std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip)));
-        *grid_out = static_cast<int>(std::min<long long>(sms, static_cast<long long>(n_strips) * k));
+        // all segments resident at once when they fit (plan_create clamps to what does)
+        *grid_out = static_cast<int>(std::min<long long>(2LL * sms, static_cast<long long>(n_strips) * k));
         return k;
     }
     double best = 1e300;
@@ -192,6 +197,8 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
             p.seg_per_strip = std::max(1, atoi(v));
             plan->grid = static_cast<int>(std::min<long long>(2LL * sms, 1LL * p.n_strips * p.seg_per_strip));
         }
+        if (const char* v = getenv("YCHG_GRID"); v && *v)
+            plan->grid = std::max(1, std::min(atoi(v), p.n_strips * p.seg_per_strip));
         p.n_segments = p.n_strips * p.seg_per_strip;
         if (p.seg_per_strip > ychg_dev::kMaxSegPerStrip)
             return fail(YCHG_ERR_INVALID, "plan_create: height %d needs more than %d row segments per strip",

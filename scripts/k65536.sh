@@ -1,0 +1,3 @@
+for k in 2 4 8 16; do
+  YCHG_SEGMENTS=$k python bench.py --size 65536 --no-cpu-baseline --no-e2e --steps 30 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('k', d['config']['plan'], round(d['ms_per_step']*1e3,2), 'us frac', d['roofline']['frac'], '| subset', round(d['north_star_subset']['ms_per_step']*1e3,2), d['north_star_subset']['roofline_frac'])"
+done
