@@ -365,13 +365,46 @@ class Hypergraph:
                 and np.array_equal(self.edge_offsets, other.edge_offsets))
 
 
-def _take_hypergraph(h: ctypes.c_void_p, width: int, height: int) -> Hypergraph:
+class HypergraphBuffers:
+    """Reusable pinned host arrays for decompose(..., out=...): the result arrays
+    are copied straight into page-locked memory (full PCIe rate, no first-touch
+    page faults) and returned as views -- valid until the next call that uses
+    the same buffers."""
+
+    def __init__(self, max_runs: int):
+        self.capacity = int(max(max_runs, 1))
+        self._ptrs = []
+        self.edge_runs = self._pinned((self.capacity, 3), np.int32)
+        self.edge_offsets = self._pinned((self.capacity + 1,), np.uint32)
+        self.run_to_edge = self._pinned((self.capacity,), np.uint32)
+
+    def _pinned(self, shape, dtype):
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        p = _vp()
+        _check(_lib.ychg_host_alloc_pinned(nbytes, ctypes.byref(p)), "host_alloc_pinned")
+        self._ptrs.append(p.value)
+        buf = (ctypes.c_uint8 * nbytes).from_address(p.value)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def close(self) -> None:
+        for p in getattr(self, "_ptrs", []):
+            if _lib is not None:
+                _lib.ychg_host_free_pinned(p)
+        self._ptrs = []
+
+    __del__ = close
+
+
+def _take_hypergraph(h: ctypes.c_void_p, width: int, height: int, out: "HypergraphBuffers | None" = None) -> Hypergraph:
     try:
         n, e, ms = _i64(0), _i64(0), ctypes.c_float(0)
         _check(_lib.ychg_hypergraph_info(h, ctypes.byref(n), ctypes.byref(e), ctypes.byref(ms)), "decompose")
-        er = np.empty((max(n.value, 1), 3), dtype=np.int32)
-        eo = np.empty(e.value + 1, dtype=np.uint32)
-        r2e = np.empty(max(n.value, 1), dtype=np.uint32)
+        if out is not None and n.value <= out.capacity:
+            er, eo, r2e = out.edge_runs, out.edge_offsets[: e.value + 1], out.run_to_edge
+        else:
+            er = np.empty((max(n.value, 1), 3), dtype=np.int32)
+            eo = np.empty(e.value + 1, dtype=np.uint32)
+            r2e = np.empty(max(n.value, 1), dtype=np.uint32)
         _check(_lib.ychg_hypergraph_copy(h, er.ctypes.data_as(_vp), eo.ctypes.data_as(_vp), r2e.ctypes.data_as(_vp)),
                "decompose")
         return Hypergraph(width, height, er[: n.value], eo, r2e[: n.value], float(ms.value))
@@ -379,15 +412,18 @@ def _take_hypergraph(h: ctypes.c_void_p, width: int, height: int) -> Hypergraph:
         _lib.ychg_hypergraph_destroy(h)
 
 
-def decompose(source, strategy: ScanStrategy = ScanStrategy.serial()) -> Hypergraph:
+def decompose(source, strategy: ScanStrategy = ScanStrategy.serial(),
+              out: "HypergraphBuffers | None" = None) -> Hypergraph:
     """decompose (hypergraph.cpp:94-170) on the GPU.  `source` is a ColumnProfile
     (validated like validate_profile, :62-90) or a BinaryImage (build_profile +
-    decompose without leaving the device)."""
+    decompose without leaving the device).  With `out` (HypergraphBuffers large
+    enough for the run count) the result arrays are views into those pinned
+    buffers; otherwise fresh arrays are allocated."""
     h = _vp()
     if isinstance(source, BinaryImage):
         _check(_lib.ychg_decompose_image(source._ptr(), source.width, source.height, source.row_stride,
                                          strategy.kind, strategy.threads, ctypes.byref(h)), "decompose")
-        return _take_hypergraph(h, source.width, source.height)
+        return _take_hypergraph(h, source.width, source.height, out)
     prof = source
     runs = np.ascontiguousarray(prof.runs_flat, dtype=np.int32).reshape(-1, 3)
     sizes = np.ascontiguousarray(prof.counts, dtype=np.int32)
@@ -396,7 +432,7 @@ def decompose(source, strategy: ScanStrategy = ScanStrategy.serial()) -> Hypergr
     _check(_lib.ychg_decompose_profile(prof.width, prof.height, sizes.ctypes.data_as(_vp) if sizes.size else None,
                                        runs.ctypes.data_as(_vp) if runs.size else None, runs.shape[0],
                                        ctypes.byref(h)), "decompose")
-    return _take_hypergraph(h, prof.width, prof.height)
+    return _take_hypergraph(h, prof.width, prof.height, out)
 
 
 # ---------------------------------------------------------------- device-resident plumbing
@@ -523,7 +559,7 @@ def synth(pattern: str, width: int, height: int, *, bands: int = 0, cell: int = 
 
 __all__ = [
     "BinaryImage", "ScanStrategy", "ScanResult", "ColumnProfile", "build_profile", "column_runs", "Error",
-    "Hypergraph", "decompose", "ParseError", "pnm_info", "load_pnm", "save_pnm", "scan_pnm",
+    "Hypergraph", "HypergraphBuffers", "decompose", "ParseError", "pnm_info", "load_pnm", "save_pnm", "scan_pnm",
     "ValidationError", "cut_vertex_counts",
     "detect_boundary_columns", "scan", "hyperedge_count", "Plan", "DeviceBuffer", "synth", "synth_device",
     "pitch_for", "device_count", "Totals", "PlanInfo", "LIB_PATH", "CXX_LIB_PATH", "EXPORTED_SYMBOLS",

@@ -30,8 +30,16 @@ for pat, w, h, kw in CASES:
         t0 = time.perf_counter()
         hg = y.decompose(img)
         t.append(time.perf_counter() - t0)
+    buf = y.HypergraphBuffers(hg.edge_runs.shape[0])
+    y.decompose(img, out=buf)
+    tp = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        hgp = y.decompose(img, out=buf)
+        tp.append(time.perf_counter() - t0)
+    assert np.array_equal(hgp.edge_runs, hg.edge_runs) and np.array_equal(hgp.run_to_edge, hg.run_to_edge)
     row = {"image": f"{pat}{kw} {w}x{h}", "runs": int(hg.edge_runs.shape[0]), "edges": hg.edge_count,
-           "gpu_e2e_s": min(t), "gpu_decompose_kernels_ms": hg.device_ms}
+           "gpu_e2e_s": min(t), "gpu_e2e_pinned_out_s": min(tp), "gpu_decompose_kernels_ms": hg.device_ms}
     if ref is not None and hg.edge_runs.shape[0] < 40_000_000:
         ri = ref.image(img.bytes(), w)
         t0 = time.perf_counter()
@@ -40,4 +48,7 @@ for pat, w, h, kw in CASES:
         row["identical"] = bool(np.array_equal(d.edge_runs, hg.edge_runs) and np.array_equal(d.edge_offsets, hg.edge_offsets)
                                 and np.array_equal(d.run_to_edge, hg.run_to_edge))
         row["speedup_e2e"] = row["ref_s"] / row["gpu_e2e_s"]
+        row["speedup_e2e_pinned_out"] = row["ref_s"] / row["gpu_e2e_pinned_out_s"]
+        buf.close()
+    buf.close()
     print(json.dumps(row), flush=True)
