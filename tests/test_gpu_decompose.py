@@ -128,3 +128,21 @@ def test_decompose_cxx_dropin(gpu):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "[PASS]" in out.stdout
+
+
+def test_decompose_into_pinned_buffers(gpu, orc):
+    """decompose(..., out=HypergraphBuffers): views into reusable pinned arrays equal
+    the freshly allocated result; too small a buffer falls back to fresh arrays."""
+    y = gpu
+    buf = y.HypergraphBuffers(200_000)
+    for sp in (Spec.random(500, 400, 0.5, 1), Spec.checker(300, 333, 3), Spec.random(500, 400, 0.5, 1)):
+        img = y.BinaryImage(sp.width, sp.height, orc.synth(sp))
+        fresh = y.decompose(img)
+        got = y.decompose(img, out=buf)
+        for a, b in zip(as_tuple(got), as_tuple(fresh)):
+            assert np.array_equal(a, b)
+    small = y.HypergraphBuffers(10)
+    img = y.BinaryImage(500, 400, orc.synth(Spec.random(500, 400, 0.5, 2)))
+    assert y.decompose(img, out=small) == y.decompose(img)
+    buf.close()
+    small.close()
