@@ -194,7 +194,8 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid, (flags & YCHG_PLAN_LATENCY) != 0);
         // experiment hooks (benchmarking only): force the segments per strip / grid
         if (const char* v = getenv("YCHG_SEGMENTS"); v && *v) {
-            p.seg_per_strip = std::max(1, atoi(v));
+            // (never more segments than 32-row blocks: a segment must not be empty)
+            p.seg_per_strip = std::max(1, std::min(atoi(v), p.n_blocks));
             plan->grid = static_cast<int>(std::min<long long>(2LL * sms, 1LL * p.n_strips * p.seg_per_strip));
         }
         if (const char* v = getenv("YCHG_GRID"); v && *v)

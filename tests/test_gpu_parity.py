@@ -393,3 +393,61 @@ def test_pipelined_graph_distinct_images(gpu, orc, segments, monkeypatch):
         assert tt[3] == bounds.size and np.array_equal(b.cpu().numpy()[: bounds.size], bounds), i
         assert tt[2] == (he if i % 3 != 2 else -1), i
     plan.close()
+
+
+def test_pipelined_graph_random_geometries(gpu, orc, monkeypatch):
+    """Random geometries (strip / word / byte edges, tall and wide), each captured as
+    a CUDA graph of back-to-back scans of distinct images with random segment counts
+    and full / counts-only mixed; every scan's outputs checked against the oracle."""
+    import time
+
+    import torch
+
+    y = gpu
+    rng = np.random.default_rng(777)
+    for trial in range(12):
+        W = int(rng.choice([1, 31, 33, 1023, 1025, 2049, 3000, 5000]))
+        H = int(rng.choice([1, 2, 31, 33, 257, 1000, 2500]))
+        monkeypatch.setenv("YCHG_SEGMENTS", str(int(rng.integers(1, 9))))
+        specs = [Spec.random(W, H, float(rng.choice([0.1, 0.5, 0.9])), int(rng.integers(0, 1 << 40))) for _ in range(3)]
+        pitch = y.pitch_for(W)
+        imgs = []
+        for sp in specs:
+            bits = orc.synth(sp)
+            dev = np.zeros((H, pitch), np.uint8)
+            dev[:, : bits.shape[1]] = bits
+            counts = orc.counts(bits, W)
+            imgs.append((torch.from_numpy(dev).cuda(), counts, orc.boundaries(counts), orc.hyperedges(bits, W)[0]))
+        plan = y.Plan(W, H)
+        n = 9
+        full = [bool(rng.integers(0, 2)) for _ in range(n)]
+        outs = [(torch.full((W,), -7, dtype=torch.int32, device="cuda"),
+                 torch.zeros(W // 32 + 64, dtype=torch.int32, device="cuda"),
+                 torch.full((W,), -7, dtype=torch.int32, device="cuda"), torch.zeros(4, dtype=torch.int64, device="cuda"))
+                for _ in range(n)]
+        stream = torch.cuda.current_stream()
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                cs = torch.cuda.current_stream().cuda_stream
+                for i in range(n):
+                    c, f, b, t = outs[i]
+                    plan.scan_device(imgs[i % 3][0].data_ptr(), pitch, c.data_ptr(), f.data_ptr(), b.data_ptr(),
+                                     t.data_ptr(), cs, full[i])
+        stream.wait_stream(cap)
+        for rep in range(2):
+            g.replay()
+            t0 = time.time()
+            while not stream.query():
+                assert time.time() - t0 < 20, f"stall: {W}x{H} trial {trial}"
+                time.sleep(0.005)
+        for i in range(n):
+            c, _, b, t = outs[i]
+            _, counts, bounds, he = imgs[i % 3]
+            tt = t.cpu().tolist()
+            assert np.array_equal(c.cpu().numpy(), counts), (W, H, i)
+            assert tt[3] == bounds.size and np.array_equal(b.cpu().numpy()[: bounds.size], bounds), (W, H, i)
+            assert tt[2] == (he if full[i] else -1), (W, H, i)
+        plan.close()
