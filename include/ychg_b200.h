@@ -19,8 +19,16 @@
  *                                   pass; its hyperedge total equals
  *                                   hyperedge_count(decompose(build_profile(img)))
  *                                   (hypergraph.cpp:192, :94-170, runscan.cpp:130-143)
+ *   ychg_build_profile_host /       replace ychg::build_profile / column_runs
+ *   ychg_column_runs_host            (runscan.hpp:54-66, runscan.cpp:78-143)
+ *   ychg_decompose_image /          decompose (hypergraph.cpp:94-170) on the device,
+ *   ychg_decompose_profile           results in a ychg_hypergraph handle
+ *   ychg_pnm_info / ychg_load_pnm / replace ychg::load_pnm (pnm.cpp:124-153); the
+ *   ychg_load_pnm_device /           scan straight from PNM bytes
+ *   ychg_scan_pnm
  *   ychg_plan_* / ychg_scan_device  the same pass on device-resident buffers and a
- *                                   caller stream (benchmarks, multi-GPU strips)
+ *                                   caller stream (benchmarks, CUDA graphs,
+ *                                   multi-GPU strips)
  *   ychg_synth_device               bit-exact on-device synth (synth.cpp:38-104)
  *
  * There is no CPU fallback: without a usable CUDA device every compute entry
