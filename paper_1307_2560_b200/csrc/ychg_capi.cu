@@ -208,8 +208,13 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         int per_sm = 0;
         if (const int rc2 = ychg_scan_kernel_prepare())
             return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ychg_scan_kernel_ptr(1), ychg_dev::kThreads,
-                                                          ychg_dev::kSmemTotal));
+        per_sm = 1 << 30;
+        for (int path = 0; path < 2; ++path) {  // both paths share the plan's grid
+            int thr = 0, smem = 0, n = 0;
+            ychg_scan_kernel_shape(path, &thr, &smem);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ychg_scan_kernel_ptr(path), thr, smem));
+            per_sm = std::min(per_sm, n);
+        }
         if (per_sm < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
         plan->grid = std::min(plan->grid, per_sm * sms);
         if ((p.n_segments + plan->grid - 1) / plan->grid > ychg_dev::kMaxSegPerCta)

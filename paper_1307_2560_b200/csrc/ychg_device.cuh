@@ -44,6 +44,28 @@ constexpr int kSmemSum = kWarps * kSumPlanes * 32 * 4;                 // per-wa
 constexpr int kSmemMisc = kWarps * 24 + 48;                            // links, tree scratch, flags
 constexpr int kSmemTotal = kSmemStages + kSmemBar + kSmemAcc + kSmemSum + kSmemMisc;
 
+// The streaming kernel is instantiated per path with its own CTA width: the
+// ALU-bound full path (K1+K3) runs 4-warp CTAs (more CTAs per SM, so more
+// consecutive scans overlap and each CTA's merge is cheaper: 12.2 vs 13.0 us per
+// scan at 21000^2), the HBM-bound counts path 8-warp CTAs (more loads in flight
+// per scan: 10.0 vs 11.5 us).  Shared-memory layout of an NW-warp CTA:
+#ifndef YCHG_WARPS_LINKS
+#define YCHG_WARPS_LINKS 4
+#endif
+constexpr int kWarpsLinks = YCHG_WARPS_LINKS;
+constexpr int kWarpsCounts = kWarps;
+template <int NW>
+struct ScanSmem {
+    static constexpr int kStagesB = NW * kStages * kStageBytes;
+    static constexpr int kBar = NW * kStages * 8;
+    static constexpr int kAcc = NW * 16 * 32 * 4;
+    static constexpr int kSum = NW * kSumPlanes * 32 * 4;
+    static constexpr int kMisc = NW * 24 + 48;
+    static constexpr int kTotal = kStagesB + kBar + kAcc + kSum + kMisc;
+};
+template <bool kLinks>
+constexpr int scan_warps() { return kLinks ? kWarpsLinks : kWarpsCounts; }
+
 // What a strip's finisher publishes for the strips to its right: `status`
 // packs the epoch, the number of change flags strictly inside the strip and the
 // counts of its first and last column (counts < 2^21, i.e. height < 2^22);

@@ -16,8 +16,9 @@ int ychg_launch_scan(const void* tmap, const ychg_dev::ScanParams* prm, int grid
 // Set the kernels' dynamic shared-memory opt-in on the current device.
 int ychg_scan_kernel_prepare(void);
 
-// The streaming kernel entry (for occupancy queries).
+// The streaming kernel entry and launch shape (for occupancy queries).
 const void* ychg_scan_kernel_ptr(int with_links);
+void ychg_scan_kernel_shape(int with_links, int* threads, int* smem_bytes);
 
 int ychg_launch_synth(int pattern, int width, int height, int bands, int cell, double density,
                       uint64_t seed, uint8_t* d_bits, int64_t pitch, cudaStream_t stream);

@@ -215,12 +215,13 @@ __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long 
 // of the CTA: level s composes slots (p*2s, p*2s+s) into p*2s.  Returns, in
 // every thread, the number of links resolved at the junctions.  Must be called
 // by the whole CTA (contains __syncthreads).
+template <int NW>
 __device__ unsigned long long tree_compose(uint32_t* base, int n, unsigned long long* red) {
     constexpr int kSW = kSumPlanes * 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long mine = 0;
     for (int st = 1; st < n; st <<= 1) {
-        for (int p = warp; p * 2 * st + st < n; p += kWarps) {
+        for (int p = warp; p * 2 * st + st < n; p += NW) {
             uint32_t* a = base + (p * 2 * st) * kSW;
             const uint32_t* b = base + (p * 2 * st + st) * kSW;
             const BandSummary A{a[lane], a[32 + lane], a[64 + lane], a[96 + lane], a[128 + lane], a[160 + lane],
@@ -244,7 +245,7 @@ __device__ unsigned long long tree_compose(uint32_t* base, int n, unsigned long 
     if (lane == 0) red[warp] = mine;
     __syncthreads();
     unsigned long long t = 0;
-    for (int w = 0; w < kWarps; ++w) t += red[w];
+    for (int w = 0; w < NW; ++w) t += red[w];
     __syncthreads();
     return t;
 }
@@ -456,7 +457,7 @@ ychg_finish_kernel(const ScanParams prm) {
     // (2b) K3: stitch the strip's segment summaries top to bottom (tree, all warps)
     unsigned long long strip_links = 0;
     if (kLinks) {
-        strip_links = tree_compose(ssum, k, reinterpret_cast<unsigned long long*>(fs.red2));
+        strip_links = tree_compose<kWarps>(ssum, k, reinterpret_cast<unsigned long long*>(fs.red2));
         if (tid == 0) YCHG_STAMP(26);
         if (warp == 1) {
             // close whatever is still open at row H (virtual background row)
@@ -564,16 +565,17 @@ ychg_finish_kernel(const ScanParams prm) {
 }
 
 // ----------------------------------------------------------------------------
-template <bool kLinks>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kLinks, int NW = scan_warps<kLinks>()>
+__global__ void __launch_bounds__(NW * 32, 1)
 ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm) {
+    using L = ScanSmem<NW>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stages = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemStages);
-    uint32_t* accs = reinterpret_cast<uint32_t*>(smem + kSmemStages + kSmemBar);
-    uint32_t* sums = accs + kWarps * 16 * 32;
-    unsigned long long* wlinks = reinterpret_cast<unsigned long long*>(sums + kWarps * kSumPlanes * 32);
-    int* misc = reinterpret_cast<int*>(wlinks + 2 * kWarps);  // [0..W) warp empty, [W+1] epoch, [W+2] scan index
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kStagesB);
+    uint32_t* accs = reinterpret_cast<uint32_t*>(smem + L::kStagesB + L::kBar);
+    uint32_t* sums = accs + NW * 16 * 32;
+    unsigned long long* wlinks = reinterpret_cast<unsigned long long*>(sums + NW * kSumPlanes * 32);
+    int* misc = reinterpret_cast<int*>(wlinks + 2 * NW);  // [0..W) warp empty, [W+1] epoch, [W+2] scan index
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -585,7 +587,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     __shared__ unsigned long long seg_tick[kMaxSegPerCta];
     const unsigned long long t_entry = globaltimer();
     if (tid == 0) {
-        for (int i = 0; i < kWarps * kStages; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < NW * kStages; ++i) mbar_init(&bars[i], 1);
         int i = 0;
         for (int sg = blockIdx.x; sg < prm.n_segments && i < kMaxSegPerCta; sg += gridDim.x, ++i)
             seg_tick[i] = atomicAdd(prm.seg_ticket + sg, 1ull);
@@ -608,8 +610,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         const int sb0 = seg_first_block(j, k, prm.n_blocks);
         const int sb1 = seg_first_block(j + 1, k, prm.n_blocks);
         const int nseg = sb1 - sb0;
-        const int wb0 = sb0 + (warp * nseg) / kWarps;
-        const int wb1 = sb0 + ((warp + 1) * nseg) / kWarps;
+        const int wb0 = sb0 + (warp * nseg) / NW;
+        const int wb1 = sb0 + ((warp + 1) * nseg) / NW;
         const int nb = wb1 - wb0;
         const int x0 = strip * kStripBytes;
         const int gw = strip * kStripWords + lane;
@@ -617,8 +619,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         // this segment's scan number (agrees with the finisher's strip ticket)
         if (tid == 0) {
             const unsigned long long t = seg_tick[seg_i];
-            misc[kWarps + 1] = static_cast<int>(t % 4095ull) + 1;
-            misc[kWarps + 2] = static_cast<int>(t);  // scans before this one (< 2^31 per plan)
+            misc[NW + 1] = static_cast<int>(t % 4095ull) + 1;
+            misc[NW + 2] = static_cast<int>(t);  // scans before this one (< 2^31 per plan)
             const int ring = static_cast<int>(t & 3ull);
             YCHG_STAMP_AT(0, t_entry);
             YCHG_STAMP_AT(15, t + 1);
@@ -700,7 +702,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             if (kLinks) {
                 const uint32_t m = s.mk3;
                 int slot = 0;
-                for (int w = 0; w < warp; ++w) slot += ((w + 1) * nseg) / kWarps > (w * nseg) / kWarps;
+                for (int w = 0; w < warp; ++w) slot += ((w + 1) * nseg) / NW > (w * nseg) / NW;
                 uint32_t* ws = sums + slot * kSumPlanes * 32;
                 ws[0 * 32 + lane] = O & m;
                 ws[1 * 32 + lane] = O & ~s.Hd & m;
@@ -722,14 +724,14 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         for (int i = 0; i < 16; ++i) wa[i * 32 + lane] = s.acc[i];
         if (lane == 0) {
             misc[warp] = (nb == 0);
-            const int ring = misc[kWarps + 2] & 3;
+            const int ring = misc[NW + 2] & 3;
             if (warp < 16) YCHG_STAMP(1 + warp);
         }
         __syncthreads();
 
         // ---- partials are double-buffered by scan parity: the finisher of the scan
         // two back (same half) must have loaded this strip before we overwrite it
-        const unsigned long long scan_idx = static_cast<unsigned long long>(misc[kWarps + 2]);
+        const unsigned long long scan_idx = static_cast<unsigned long long>(misc[NW + 2]);
         const int64_t par = static_cast<int64_t>(scan_idx & 1ull);
         if (tid == 0 && scan_idx >= 2) {
             const int ring = static_cast<int>(scan_idx & 3ull);
@@ -745,19 +747,19 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         }
         __syncthreads();
         // ---- CTA merge: counts (sum over warps, coalesced u16x2 words), K3 (compose in row order).
-        for (int idx = tid; idx < 16 * 32; idx += kThreads) {
+        for (int idx = tid; idx < 16 * 32; idx += (NW * 32)) {
             uint32_t v = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) v += accs[w * 16 * 32 + idx];
+            for (int w = 0; w < NW; ++w) v += accs[w * 16 * 32 + idx];
             prm.part[(par * prm.n_segments + seg) * 512 + idx] = v;
         }
         if (kLinks) {
             // non-empty warp bands were written to consecutive slots (row order)
             int nfull = 0;
-            for (int w = 0; w < kWarps; ++w) nfull += ((w + 1) * nseg) / kWarps > (w * nseg) / kWarps;
-            const unsigned long long jl = tree_compose(sums, nfull, wlinks + kWarps);
+            for (int w = 0; w < NW; ++w) nfull += ((w + 1) * nseg) / NW > (w * nseg) / NW;
+            const unsigned long long jl = tree_compose<NW>(sums, nfull, wlinks + NW);
             if (warp == 0) {
-                unsigned long long links = lane < kWarps ? wlinks[lane] : 0ull;
+                unsigned long long links = lane < NW ? wlinks[lane] : 0ull;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
                 uint32_t* gs = prm.sums + (par * prm.n_segments + seg) * kSumPlanes * 32;
@@ -770,17 +772,17 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         // writes before tid 0's release store of the epoch-tagged flag.
         __syncthreads();
         if (tid == 0) {
-            const int ring = misc[kWarps + 2] & 3;
+            const int ring = misc[NW + 2] & 3;
             YCHG_STAMP(20);
-            YCHG_STAMP_AT(13, static_cast<unsigned long long>(misc[kWarps + 2]) + 1);
-            st_release(prm.seg_status + par * prm.n_segments + seg, static_cast<unsigned long long>(misc[kWarps + 1]));
+            YCHG_STAMP_AT(13, static_cast<unsigned long long>(misc[NW + 2]) + 1);
+            st_release(prm.seg_status + par * prm.n_segments + seg, static_cast<unsigned long long>(misc[NW + 1]));
         }
         __syncthreads();
     }
     if (tid == 0 && prm.n_segments > 0) {
-        const int ring = misc[kWarps + 2] & 3;
+        const int ring = misc[NW + 2] & 3;
         YCHG_STAMP(23);
-        YCHG_STAMP_AT(14, static_cast<unsigned long long>(misc[kWarps + 2]) + 1);
+        YCHG_STAMP_AT(14, static_cast<unsigned long long>(misc[NW + 2]) + 1);
     }
 }
 
@@ -795,6 +797,12 @@ extern "C" const void* ychg_scan_kernel_ptr(int with_links) {
                       : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
 }
 
+// Launch shape of the streaming kernel of a path (for occupancy queries).
+extern "C" void ychg_scan_kernel_shape(int with_links, int* threads, int* smem_bytes) {
+    *threads = 32 * (with_links ? scan_warps<true>() : scan_warps<false>());
+    *smem_bytes = with_links ? ScanSmem<scan_warps<true>()>::kTotal : ScanSmem<scan_warps<false>()>::kTotal;
+}
+
 constexpr int kFinishSmemMax = 160 * 1024;
 
 // Opt-in to >48 KB dynamic shared memory (per device, all kernels and variants).
@@ -804,10 +812,10 @@ extern "C" int ychg_scan_kernel_prepare(void) {
     cudaGetDevice(&dev);
     if (dev < 64 && done[dev]) return 0;
     cudaError_t e = cudaFuncSetAttribute(&ychg_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kSmemTotal);
+                                         ScanSmem<scan_warps<true>()>::kTotal);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemTotal);
+                                 ScanSmem<scan_warps<false>()>::kTotal);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_finish_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kFinishSmemMax);
@@ -858,8 +866,8 @@ extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int gri
     void* args_a[2] = {&map, &p};
     cudaLaunchConfig_t ca{};
     ca.gridDim = dim3(grid);
-    ca.blockDim = dim3(kThreads);
-    ca.dynamicSmemBytes = kSmemTotal;
+    ca.blockDim = dim3(32 * (with_links ? scan_warps<true>() : scan_warps<false>()));
+    ca.dynamicSmemBytes = with_links ? ScanSmem<scan_warps<true>()>::kTotal : ScanSmem<scan_warps<false>()>::kTotal;
     ca.stream = stream;
     ca.attrs = attr;
     ca.numAttrs = 1;

@@ -29,7 +29,8 @@ st = plan.debug_stamps(True).astype(np.float64)
 G = info.grid
 for ring in range(4):
     e = st[ring, :G]
-    warps = e[:, 1:9]
+    nw = int((e[:, 1:17] > 0).any(0).sum()) or 8
+    warps = e[:, 1:1 + nw]
     dur = (e[:, 23] - e[:, 0]) / 1e3
     imb = (warps.max(1) - warps.min(1)) / 1e3
     first = (warps.min(1) - e[:, 0]) / 1e3
