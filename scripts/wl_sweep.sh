@@ -1,0 +1,9 @@
+run() { lib=$1; shift; env "$@" YCHG_LIB=paper_1307_2560_b200/$lib python bench.py --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$lib $*', d['config']['plan']['grid'], round(d['ms_per_step']*1e3,2), d['roofline']['frac'])"; }
+for rep in 1 2; do
+run libychg_b200.so
+run "libychg_b200_w8s2_warps_links=2.so"
+run "libychg_b200_w8s2_warps_links=2.so" YCHG_SEGMENTS=6
+run "libychg_b200_w8s2_warps_links=2.so" YCHG_SEGMENTS=8
+run "libychg_b200_w8s2_warps_links=6.so"
+run "libychg_b200_w8s2_warps_links=6.so" YCHG_SEGMENTS=3
+done
