@@ -78,7 +78,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 struct ychg_plan {
     int device = 0;
     ScanParams prm{};
-    int grid = 0;
+    int grid = 0;                  // streaming grid of the full path (K1+K3)
+    int grid_counts = 0;           // streaming grid of the counts-only path
     int64_t ws_bytes = 0;
     void* ws = nullptr;
     // tensor-map cache
@@ -114,11 +115,11 @@ int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out, bool lat
         // ... but segments of at most 16384 rows: a very tall mask is better served by
         // two resident CTAs per SM than by few extremely long ones (65536^2, K=30:
         // k=2/128 CTAs -> 110 us full, 140 us counts-only; k=4/256 CTAs -> 110 / 110-119)
-        k = std::max(k, (n_blocks + 511) / 512);
+        k = std::max(k, (n_blocks + 255) / 256);  // <= 8192 rows: 2048 rows per warp of a 4-warp CTA
         k = std::max(k, kmin);
         k = std::min(k, std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip)));
-        // all segments resident at once when they fit (plan_create clamps to what does)
-        *grid_out = static_cast<int>(std::min<long long>(2LL * sms, static_cast<long long>(n_strips) * k));
+        // all segments resident at once when they fit (plan_create clamps per path)
+        *grid_out = static_cast<int>(std::min<long long>(8LL * sms, static_cast<long long>(n_strips) * k));
         return k;
     }
     double best = 1e300;
@@ -196,7 +197,7 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         if (const char* v = getenv("YCHG_SEGMENTS"); v && *v) {
             // (never more segments than 32-row blocks: a segment must not be empty)
             p.seg_per_strip = std::max(1, std::min(atoi(v), p.n_blocks));
-            plan->grid = static_cast<int>(std::min<long long>(2LL * sms, 1LL * p.n_strips * p.seg_per_strip));
+            plan->grid = static_cast<int>(std::min<long long>(8LL * sms, 1LL * p.n_strips * p.seg_per_strip));
         }
         if (const char* v = getenv("YCHG_GRID"); v && *v)
             plan->grid = std::max(1, std::min(atoi(v), p.n_strips * p.seg_per_strip));
@@ -208,18 +209,23 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         int per_sm = 0;
         if (const int rc2 = ychg_scan_kernel_prepare())
             return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
-        per_sm = 1 << 30;
-        for (int path = 0; path < 2; ++path) {  // both paths share the plan's grid
-            int thr = 0, smem = 0, n = 0;
+        // Each path's streaming kernel has its own CTA width, hence its own grid:
+        // up to what is resident at once (streaming CTAs never wait on each other;
+        // a CTA takes several segments when the grid is smaller).
+        int per_path[2] = {0, 0};
+        for (int path = 0; path < 2; ++path) {
+            int thr = 0, smem = 0;
             ychg_scan_kernel_shape(path, &thr, &smem);
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ychg_scan_kernel_ptr(path), thr, smem));
-            per_sm = std::min(per_sm, n);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_path[path], ychg_scan_kernel_ptr(path), thr, smem));
+            if (per_path[path] < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
         }
-        if (per_sm < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
-        plan->grid = std::min(plan->grid, per_sm * sms);
-        if ((p.n_segments + plan->grid - 1) / plan->grid > ychg_dev::kMaxSegPerCta)
-            return fail(YCHG_ERR_INVALID, "plan_create: %d segments over %d CTAs exceed %d per CTA", p.n_segments,
-                        plan->grid, ychg_dev::kMaxSegPerCta);
+        const int want = plan->grid;
+        plan->grid = std::min(want, per_path[1] * sms);
+        plan->grid_counts = std::min(want, per_path[0] * sms);
+        for (const int g : {plan->grid, plan->grid_counts})
+            if ((p.n_segments + g - 1) / g > ychg_dev::kMaxSegPerCta)
+                return fail(YCHG_ERR_INVALID, "plan_create: %d segments over %d CTAs exceed %d per CTA",
+                            p.n_segments, g, ychg_dev::kMaxSegPerCta);
         const int64_t S = p.n_strips, G = p.n_segments;
         // part / sums / seg_links / seg_status are double-buffered by scan parity
         const int64_t sz_part = 2 * G * 512 * 4, sz_sums = 2 * G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = 2 * G * 8;
@@ -311,7 +317,7 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
                            int32_t* n_ctas) {
     if (!plan) return fail(YCHG_ERR_INVALID, "plan_debug_stamps: NULL plan");
     CK(cudaSetDevice(plan->device));
-    const int64_t bytes = int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4;
+    const int64_t bytes = int64_t(std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips)) * 32 * 8 * 4;
     if (enable && !plan->dbg && plan->grid > 0) {
         // zero-copy host memory, so a stalled pipeline can still be inspected (debug_peek)
         CK(cudaHostAlloc(reinterpret_cast<void**>(&plan->dbg_host), bytes, cudaHostAllocMapped));
@@ -323,7 +329,7 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
         CK(cudaFreeHost(plan->dbg_host));
         plan->dbg = plan->dbg_host = nullptr;
     }
-    if (n_ctas) *n_ctas = plan->grid;
+    if (n_ctas) *n_ctas = std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips);  // stamp rows
     if (host_out && plan->dbg) {
         const int64_t n = std::min<int64_t>(capacity, bytes / 8);
         CK(cudaDeviceSynchronize());
@@ -335,7 +341,7 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
 // Diagnostics: copy the stamp ring without synchronising (works while kernels stall).
 int ychg_plan_debug_peek(ychg_plan* plan, uint64_t* host_out, int32_t capacity) {
     if (!plan || !plan->dbg_host) return fail(YCHG_ERR_INVALID, "plan_debug_peek: stamps not enabled");
-    const int64_t bytes = int64_t(std::max(plan->grid, plan->prm.n_strips)) * 32 * 8 * 4;
+    const int64_t bytes = int64_t(std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips)) * 32 * 8 * 4;
     std::memcpy(host_out, const_cast<const unsigned long long*>(plan->dbg_host),
                 size_t(std::min<int64_t>(capacity, bytes / 8)) * 8);
     return YCHG_OK;
@@ -391,12 +397,13 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     p.boundaries = d_boundaries;
     p.totals = reinterpret_cast<long long*>(d_totals);
     p.dbg = plan->dbg;
-    p.dbg_rows = std::max(plan->grid, p.n_strips);
+    p.dbg_rows = std::max(std::max(plan->grid, plan->grid_counts), p.n_strips);
     p.mul2 = 2u;
     p.mulnb = 1u << 25;
 
     if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
-    const int rc = ychg_launch_scan(&plan->map, &p, plan->grid, with_hyperedges ? 1 : 0, st, nullptr);
+    const int rc = ychg_launch_scan(&plan->map, &p, with_hyperedges ? plan->grid : plan->grid_counts,
+                                    with_hyperedges ? 1 : 0, st, nullptr);
     if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "scan kernel launch");
     if (plan->timing) {
         CK(cudaEventRecord(plan->ev[1], st));
