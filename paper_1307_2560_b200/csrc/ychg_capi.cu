@@ -51,8 +51,13 @@ int cuda_fail(cudaError_t e, const char* what) {
     } while (0)
 
 int require_device(int device) {
-    int n = 0;
-    const cudaError_t e = cudaGetDeviceCount(&n);
+    static int cached = 0;  // a positive count never changes within a process
+    int n = cached;
+    cudaError_t e = cudaSuccess;
+    if (n == 0) {
+        e = cudaGetDeviceCount(&n);
+        if (e == cudaSuccess && n > 0) cached = n;
+    }
     if (e != cudaSuccess || n == 0)
         return fail(YCHG_ERR_NO_DEVICE, "no CUDA device available (%s); the yCHG path has no CPU fallback",
                     e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
@@ -524,6 +529,9 @@ struct HostContext {
     int32_t* d_runs = nullptr;
     int64_t runs_cap = 0;
     int32_t* h_out = nullptr;         // pinned staging: counts | boundaries (capacity cols_cap each)
+    char* d_block = nullptr;          // device [totals | counts | boundaries] (ensure_columns)
+    char* h_block = nullptr;          // pinned mirror of d_block
+    int64_t h_block_cap = 0;
     bool h2d_timing = false;
     cudaEvent_t h2d_ev[3] = {nullptr, nullptr, nullptr};
     int64_t h_out_cap = 0;
@@ -559,11 +567,13 @@ int ensure_context(HostContext& c) {
     return YCHG_OK;
 }
 
+// Outputs live in one device block [totals (64 B) | counts (cap) | boundaries (cap)]
+// so the host path reads all of them back with a single copy.
 int ensure_columns(HostContext& c, int64_t cols) {
     if (cols <= c.cols_cap) return YCHG_OK;
-    cudaFree(c.d_counts);
+    cudaFree(c.d_block);
     cudaFree(c.d_flags);
-    cudaFree(c.d_bounds);
+    c.d_block = nullptr;
     c.d_counts = nullptr;
     c.d_flags = nullptr;
     c.d_bounds = nullptr;
@@ -571,9 +581,11 @@ int ensure_columns(HostContext& c, int64_t cols) {
     const int64_t cap = std::max<int64_t>(cols, 1024);
     // flags: one word per 32 columns, rounded to whole 1024-column blocks, + per-block scratch
     const int64_t fwords = ((cap + 1023) / 1024) * 32 + (cap + 1023) / 1024 + 32;
-    CK(cudaMalloc(&c.d_counts, cap * 4));
+    CK(cudaMalloc(&c.d_block, 64 + cap * 8));
     CK(cudaMalloc(&c.d_flags, fwords * 4));
-    CK(cudaMalloc(&c.d_bounds, cap * 4));
+    c.d_totals = reinterpret_cast<ychg_totals*>(c.d_block);
+    c.d_counts = reinterpret_cast<int32_t*>(c.d_block + 64);
+    c.d_bounds = c.d_counts + cap;
     c.cols_cap = cap;
     return YCHG_OK;
 }
@@ -631,7 +643,12 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
         CK(cudaEventRecord(c.chunk_ev[0], c.stream));  // order after earlier work on c.stream
         CK(cudaStreamWaitEvent(c.copy_stream, c.chunk_ev[0], 0));
         if (c.h2d_timing) cudaEventRecord(c.h2d_ev[0], c.copy_stream);
-        const int nch = height >= HostContext::kChunks * 64 ? HostContext::kChunks : 1;
+        static const int max_chunks = [] {
+            const char* v = getenv("YCHG_H2D_CHUNKS");  // experiment hook (1..4)
+            const int n = v && *v ? atoi(v) : 2;  // 2: overlaps the re-pitch with fewer API calls
+            return n < 1 ? 1 : (n > HostContext::kChunks ? HostContext::kChunks : n);
+        }();
+        const int nch = height >= max_chunks * 64 ? max_chunks : 1;
         for (int i = 0; i < nch; ++i) {
             const int y0 = static_cast<int>((int64_t(height) * i) / nch);
             const int y1 = static_cast<int>((int64_t(height) * (i + 1)) / nch);
@@ -690,18 +707,16 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
     // D2H in one round trip: totals + counts + the whole boundary buffer into pinned
     // staging (W ints cost microseconds; a second synchronisation costs more), then
     // host copies of exactly what the caller asked for.
-    if (c.h_out_cap < 2 * int64_t(width)) {
-        cudaFreeHost(c.h_out);
-        c.h_out = nullptr;
-        c.h_out_cap = 0;
-        CK(cudaMallocHost(&c.h_out, 2 * int64_t(width) * 4));
-        c.h_out_cap = 2 * int64_t(width);
+    const int64_t blk = 64 + c.cols_cap * 4 + (boundaries_out ? int64_t(width) * 4 : 0);
+    if (c.h_block_cap < 64 + 8 * c.cols_cap) {
+        cudaFreeHost(c.h_block);
+        c.h_block = nullptr;
+        c.h_block_cap = 0;
+        CK(cudaMallocHost(&c.h_block, 64 + 8 * c.cols_cap));
+        c.h_block_cap = 64 + 8 * c.cols_cap;
     }
-    CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
-    if (counts_out)
-        CK(cudaMemcpyAsync(c.h_out, c.d_counts, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
-    if (boundaries_out)
-        CK(cudaMemcpyAsync(c.h_out + width, c.d_bounds, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(c.h_block, c.d_block, counts_out || boundaries_out ? blk : 64, cudaMemcpyDeviceToHost,
+                       c.stream));
     if (host_timing) cudaEventRecord(tev[2], c.stream);
     CK(cudaStreamSynchronize(c.stream));
     if (host_timing) {
@@ -715,10 +730,11 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
                      h1 * 1e3, h2 * 1e3, a * 1e3, b * 1e3);
         for (auto& e : tev) cudaEventDestroy(e);
     }
-    const ychg_totals t = *c.h_totals;
-    if (counts_out) std::memcpy(counts_out, c.h_out, size_t(width) * 4);
+    const ychg_totals t = *reinterpret_cast<const ychg_totals*>(c.h_block);
+    const int32_t* h_counts = reinterpret_cast<const int32_t*>(c.h_block + 64);
+    if (counts_out) std::memcpy(counts_out, h_counts, size_t(width) * 4);
     if (boundaries_out && t.n_boundaries > 0)
-        std::memcpy(boundaries_out, c.h_out + width, size_t(t.n_boundaries) * 4);
+        std::memcpy(boundaries_out, h_counts + c.cols_cap, size_t(t.n_boundaries) * 4);
     if (totals_out) *totals_out = t;
     return YCHG_OK;
 }
