@@ -18,7 +18,7 @@ namespace ychg_dev {
 #define YCHG_WARPS 8
 #endif
 #ifndef YCHG_STAGES
-#define YCHG_STAGES 2
+#define YCHG_STAGES 3
 #endif
 constexpr int kWarps = YCHG_WARPS;               // warps per CTA
 constexpr int kThreads = kWarps * 32;
