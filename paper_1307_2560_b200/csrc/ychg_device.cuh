@@ -36,8 +36,8 @@ constexpr int kMaxSegmentRows = 65504;           // u16 SWAR accumulators: count
 constexpr int kMaxSegPerStrip = 128;            // the finisher keeps k summaries in smem
 constexpr int kMaxSegPerCta = 64;               // segments one streaming CTA processes per scan
 
-// Shared-memory layout of the scan kernel (bytes).
-constexpr int kSmemStages = kWarps * kStages * kStageBytes;            // 147456
+// Shared-memory layout of an 8-warp scan CTA (bytes; see ScanSmem<NW> below).
+constexpr int kSmemStages = kWarps * kStages * kStageBytes;
 constexpr int kSmemBar = kWarps * kStages * 8;                         // mbarriers
 constexpr int kSmemAcc = kWarps * 16 * 32 * 4;                         // per-warp u16x2 counts
 constexpr int kSmemSum = kWarps * kSumPlanes * 32 * 4;                 // per-warp K3 summaries
@@ -48,7 +48,7 @@ constexpr int kSmemTotal = kSmemStages + kSmemBar + kSmemAcc + kSmemSum + kSmemM
 // ALU-bound full path (K1+K3) runs 4-warp CTAs (more CTAs per SM, so more
 // consecutive scans overlap and each CTA's merge is cheaper: 12.2 vs 13.0 us per
 // scan at 21000^2), the HBM-bound counts path 8-warp CTAs (more loads in flight
-// per scan: 10.0 vs 11.5 us).  Shared-memory layout of an NW-warp CTA:
+// per scan: 10.0 vs 11.5 us with 2-stage rings; 9.0-9.4 us with 3).  Shared-memory layout of an NW-warp CTA:
 #ifndef YCHG_WARPS_LINKS
 #define YCHG_WARPS_LINKS 4
 #endif
