@@ -28,4 +28,9 @@ ScanResult scan(const BinaryImage& image);
 /// device untouched, P5 is thresholded and packed on the device.
 ScanResult scan_pnm(std::span<const std::uint8_t> bytes, int threshold = 128);
 
+/// scan() over several GPUs of this process: n_parts column strips
+/// (multiples of 1024 columns, 8-column right halos) round-robin over `devices`
+/// (empty = the current device), one host thread per device; same results as scan().
+ScanResult scan_sharded(const BinaryImage& image, int n_parts, std::span<const int> devices = {});
+
 }  // namespace ychg

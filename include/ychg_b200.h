@@ -122,6 +122,16 @@ YCHG_API int ychg_scan_host(const uint8_t* bits, int32_t width, int32_t height, 
                    int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
                    ychg_totals* totals_out);
 
+/* ychg_scan_host over several devices of this process: column strips
+ * on multiples of 1024 columns (n_parts of them, round-robin over `devices`, NULL =
+ * the current device), each with an 8-column right halo; counts gathered, the
+ * boundary list computed once over them, runs and links summed.  Same outputs as
+ * ychg_scan_host. */
+YCHG_API int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                    int32_t n_parts, const int32_t* devices, int32_t n_devices,
+                                    int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
+                                    ychg_totals* totals_out);
+
 /* Run materialisation (build_profile / column_runs, runscan.cpp:78-143).
  * Runs are int32 triples {col, y_top, y_bot} (the layout of ychg::Run), column-major
  * and sorted by y_top inside a column -- ColumnProfile::runs flattened.

@@ -63,6 +63,8 @@ _SIGS = {
     "ychg_cut_vertex_counts": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp]),
     "ychg_detect_boundary_columns": (ctypes.c_int, [_vp, _i64, _vp, ctypes.POINTER(_i64)]),
     "ychg_scan_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, ctypes.POINTER(Totals)]),
+    "ychg_scan_host_sharded": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _i32, _i32, _vp, _vp,
+                                              ctypes.POINTER(Totals)]),
     "ychg_build_profile_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64)]),
     "ychg_column_runs_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
     "ychg_decompose_image": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_vp)]),
@@ -280,6 +282,23 @@ def scan_pnm(data: bytes, threshold: int = 128, with_hyperedges: bool = True) ->
     _check(_lib.ychg_scan_pnm(buf.ctypes.data_as(_vp), buf.size, int(threshold), int(with_hyperedges),
                               counts.ctypes.data_as(_vp), bounds.ctypes.data_as(_vp), ctypes.byref(t)), "scan_pnm")
     return ScanResult(counts[:w], bounds[: t.n_boundaries].copy(), t.total_runs, t.links, t.hyperedges,
+                      t.n_boundaries)
+
+
+def scan_sharded(image: BinaryImage, n_parts: int, devices=None, with_hyperedges: bool = True) -> ScanResult:
+    """scan() over several devices of this process: n_parts column strips (multiples of
+    1024 columns, 8-column right halos) spread round-robin over `devices` (default:
+    the current device), one host thread per device (ychg_scan_host_sharded)."""
+    counts = np.zeros(max(image.width, 1), dtype=np.int32)
+    bounds = np.zeros(max(image.width, 1), dtype=np.int32)
+    t = Totals()
+    devs = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+    _check(_lib.ychg_scan_host_sharded(image._ptr(), image.width, image.height, image.row_stride, int(n_parts),
+                                       devs.ctypes.data_as(_vp) if devs is not None else None,
+                                       0 if devs is None else int(devs.size), int(with_hyperedges),
+                                       counts.ctypes.data_as(_vp), bounds.ctypes.data_as(_vp), ctypes.byref(t)),
+           "scan_sharded")
+    return ScanResult(counts[: image.width], bounds[: t.n_boundaries].copy(), t.total_runs, t.links, t.hyperedges,
                       t.n_boundaries)
 
 
@@ -559,7 +578,7 @@ def synth(pattern: str, width: int, height: int, *, bands: int = 0, cell: int = 
 
 __all__ = [
     "BinaryImage", "ScanStrategy", "ScanResult", "ColumnProfile", "build_profile", "column_runs", "Error",
-    "Hypergraph", "HypergraphBuffers", "decompose", "ParseError", "pnm_info", "load_pnm", "save_pnm", "scan_pnm",
+    "Hypergraph", "HypergraphBuffers", "decompose", "scan_sharded", "ParseError", "pnm_info", "load_pnm", "save_pnm", "scan_pnm",
     "ValidationError", "cut_vertex_counts",
     "detect_boundary_columns", "scan", "hyperedge_count", "Plan", "DeviceBuffer", "synth", "synth_device",
     "pitch_for", "device_count", "Totals", "PlanInfo", "LIB_PATH", "CXX_LIB_PATH", "EXPORTED_SYMBOLS",

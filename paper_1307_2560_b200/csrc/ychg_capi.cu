@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ychg_b200.h"
@@ -512,7 +513,7 @@ struct HostContext {
     uint8_t* d_dense = nullptr;            // dense staging copy of the host rows
     int64_t dense_cap = 0;
     ychg_plan* plan = nullptr;
-    int32_t plan_w = -1, plan_h = -1;
+    int32_t plan_w = -1, plan_wc = -1, plan_h = -1;  // host plan: image width, counted width, height
     uint8_t* d_bits = nullptr;
     int64_t bits_cap = 0;
     int32_t* d_counts = nullptr;
@@ -669,28 +670,34 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
 
 // The host scan on a locked, ready context: `upload` fills c.d_bits (pitched)
 // on c.stream; then one scan and one D2H round trip.
+// `width` columns are counted; the image in c.d_bits holds width_img >= width
+// columns (a column strip with its right halo, see ychg_scan_host_sharded).
 template <typename Upload>
 int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, int32_t with_hyperedges,
-                     int32_t* counts_out, int32_t* boundaries_out, ychg_totals* totals_out, Upload&& upload) {
-    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+                     int32_t* counts_out, int32_t* boundaries_out, ychg_totals* totals_out, Upload&& upload,
+                     int32_t width_img = -1) {
+    if (width_img < width) width_img = width;
+    const int64_t row_bytes = (int64_t(width_img) + 7) / 8;
 
     if (width == 0 || height == 0) {
         if (counts_out && width > 0) std::memset(counts_out, 0, size_t(width) * 4);
         if (totals_out) *totals_out = ychg_totals{0, 0, with_hyperedges ? 0 : -1, 0};
         return YCHG_OK;
     }
-    if (c.plan_w != width || c.plan_h != height) {
+    if (c.plan_w != width_img || c.plan_wc != width || c.plan_h != height) {
         ychg_plan_destroy(c.plan);
         c.plan = nullptr;
-        c.plan_w = c.plan_h = -1;
+        c.plan_w = c.plan_wc = c.plan_h = -1;
         // one scan per call, synchronised: size the plan for latency, not pipelining
-        if (const int rc = ychg_plan_create_ex(device, width, width, height, YCHG_PLAN_LATENCY, &c.plan)) return rc;
-        c.plan_w = width;
+        if (const int rc = ychg_plan_create_ex(device, width_img, width, height, YCHG_PLAN_LATENCY, &c.plan))
+            return rc;
+        c.plan_w = width_img;
+        c.plan_wc = width;
         c.plan_h = height;
     }
     const int64_t pitch = (row_bytes + 15) / 16 * 16;
     if (const int rc = upload()) return rc;
-    if (const int rc = ensure_columns(c, width)) return rc;
+    if (const int rc = ensure_columns(c, width_img)) return rc;
     static const bool host_timing = [] {
         const char* v = getenv("YCHG_HOST_TIMING");
         return v && v[0] == '1';
@@ -1387,4 +1394,82 @@ extern "C" int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold,
                                                                    c.d_bits, pitch, c.stream);
                                 return rc ? cuda_fail(static_cast<cudaError_t>(rc), "P5 pack kernel") : YCHG_OK;
                             });
+}
+
+// ---------------------------------------------------------------------------- several devices, one process
+// the mask cut into 1024-column-aligned strips (each with an
+// 8-column right halo for the column pair at its right edge), strips spread
+// round-robin over the given devices, one host thread per device; the strip
+// counts are gathered, K2 runs once over them (ychg_detect_boundary_columns), and
+// runs / links add up (a strip counts its own pairs, the halo one included).
+extern "C" int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                      int32_t n_parts, const int32_t* devices, int32_t n_devices,
+                                      int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
+                                      ychg_totals* totals_out) {
+    if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan_sharded: negative geometry %dx%d", width, height);
+    if (n_parts < 1) return fail(YCHG_ERR_INVALID, "scan_sharded: n_parts must be >= 1, got %d", n_parts);
+    const int64_t row_bytes = (int64_t(width) + 7) / 8;
+    if (height > 0 && width > 0 && (!bits || row_stride < row_bytes))
+        return fail(YCHG_ERR_INVALID, "scan_sharded: row_stride %lld < %lld", static_cast<long long>(row_stride),
+                    static_cast<long long>(row_bytes));
+    std::vector<int32_t> devs;
+    if (devices && n_devices > 0) {
+        devs.assign(devices, devices + n_devices);
+    } else {
+        devs.push_back(pick_device());
+    }
+    for (const int32_t d : devs)
+        if (const int rc = require_device(d)) return rc;
+    // strips on multiples of 1024 columns
+    const int64_t units = (int64_t(width) + 1023) / 1024;
+    struct Part {
+        int32_t c0, c1, halo;
+        ychg_totals t;
+        int rc;
+        std::string err;
+    };
+    std::vector<Part> parts;
+    for (int32_t p = 0; p < n_parts; ++p) {
+        const int64_t u0 = p * units / n_parts, u1 = (p + 1) * units / n_parts;
+        const int32_t c0 = static_cast<int32_t>(std::min<int64_t>(width, u0 * 1024));
+        const int32_t c1 = static_cast<int32_t>(std::min<int64_t>(width, u1 * 1024));
+        if (c1 > c0) parts.push_back(Part{c0, c1, std::min<int32_t>(8, width - c1), {}, 0, {}});
+    }
+    std::vector<int32_t> counts(size_t(std::max(width, 1)), 0);
+    auto work = [&](size_t slot) {
+        for (size_t i = slot; i < parts.size(); i += devs.size()) {
+            Part& q = parts[i];
+            const int device = devs[slot];
+            HostContext& c = host_context(device);
+            std::lock_guard<std::mutex> lock(c.mu);
+            q.rc = ensure_context(c);
+            if (q.rc == YCHG_OK) {
+                const int32_t w_cnt = q.c1 - q.c0, w_img = w_cnt + q.halo;
+                const uint8_t* src = bits + q.c0 / 8;
+                q.rc = scan_host_locked(c, device, w_cnt, height, with_hyperedges, counts.data() + q.c0, nullptr, &q.t,
+                                        [&] { return upload_image(c, src, w_img, height, row_stride); }, w_img);
+            }
+            if (q.rc != YCHG_OK) q.err = ychg_last_error();
+        }
+    };
+    if (width > 0 && height > 0) {
+        std::vector<std::thread> threads;
+        for (size_t slot = 0; slot < devs.size() && slot < parts.size(); ++slot) threads.emplace_back(work, slot);
+        for (auto& t : threads) t.join();
+    }
+    long long runs = 0, links = 0;
+    for (const Part& q : parts) {
+        if (q.rc != YCHG_OK) return fail(q.rc, "%s", q.err.c_str());
+        runs += q.t.total_runs;
+        links += q.t.links;
+    }
+    int64_t nb = 0;
+    if (width > 0) {
+        std::vector<int32_t> bounds(static_cast<size_t>(width));
+        if (const int rc = ychg_detect_boundary_columns(counts.data(), width, bounds.data(), &nb)) return rc;
+        if (boundaries_out && nb > 0) std::memcpy(boundaries_out, bounds.data(), size_t(nb) * 4);
+    }
+    if (counts_out && width > 0) std::memcpy(counts_out, counts.data(), size_t(width) * 4);
+    if (totals_out) *totals_out = ychg_totals{runs, with_hyperedges ? links : 0, with_hyperedges ? runs - links : -1, nb};
+    return YCHG_OK;
 }

@@ -71,6 +71,22 @@ ScanResult scan_pnm(std::span<const std::uint8_t> bytes, int threshold) {
     return r;
 }
 
+ScanResult scan_sharded(const BinaryImage& image, int n_parts, std::span<const int> devices) {
+    ScanResult r;
+    r.counts.assign(static_cast<std::size_t>(image.width()), 0);
+    r.boundaries.assign(static_cast<std::size_t>(image.width()), 0);
+    ychg_totals t{};
+    check(ychg_scan_host_sharded(image.bytes().data(), image.width(), image.height(), image.row_stride(), n_parts,
+                                 devices.empty() ? nullptr : devices.data(), static_cast<std::int32_t>(devices.size()),
+                                 1, r.counts.data(), r.boundaries.data(), &t),
+          "scan_sharded");
+    r.boundaries.resize(static_cast<std::size_t>(t.n_boundaries));
+    r.total_runs = t.total_runs;
+    r.links = t.links;
+    r.hyperedges = t.hyperedges;
+    return r;
+}
+
 std::int64_t foreground_count(const BinaryImage& image) {
     std::int64_t n = 0;
     for (std::uint8_t b : image.bytes()) n += __builtin_popcount(b);

@@ -161,6 +161,9 @@ int main() {
         CHECK(inval);
         const ScanResult sr = scan_pnm(save_pnm(frame(5, 5)));
         CHECK(sr.counts == (std::vector<int>{1, 2, 2, 2, 1}) && sr.hyperedges == 4);
+        const BinaryImage wide = hbands(3000, 40, 7);
+        const ScanResult a = scan(wide), b = scan_sharded(wide, 3);
+        CHECK(a.counts == b.counts && a.boundaries == b.boundaries && a.hyperedges == b.hyperedges && b.hyperedges == 7);
     }
 
     std::printf("dropin_test: %d failure(s)\n", failures);

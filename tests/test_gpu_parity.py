@@ -451,3 +451,26 @@ def test_pipelined_graph_random_geometries(gpu, orc, monkeypatch):
             assert tt[3] == bounds.size and np.array_equal(b.cpu().numpy()[: bounds.size], bounds), (W, H, i)
             assert tt[2] == (he if full[i] else -1), (W, H, i)
         plan.close()
+
+
+def test_scan_sharded_matches_single_device(gpu, orc):
+    """ychg_scan_host_sharded (column strips + halos, gathered counts, one K2 pass,
+    summed runs/links): identical to the single-device scan and the oracle for 1..5
+    strips, with every strip on device 0 (the strip/merge logic is the same for
+    several devices)."""
+    y = gpu
+    rng = np.random.default_rng(99)
+    for sp in [Spec.random(5000, 700, 0.5, 3), Spec.hbands(4100, 600, 37), Spec.checker(3333, 500, 3),
+               Spec.random(1024, 300, 0.4, 4), Spec.random(1, 50, 0.5, 5), Spec.frame(2049, 9)]:
+        bits = orc.synth(sp)
+        img = y.BinaryImage(sp.width, sp.height, bits)
+        want = y.scan(img)
+        counts = orc.counts(bits, sp.width)
+        assert np.array_equal(want.counts, counts)
+        for n in (1, 2, 3, 5):
+            got = y.scan_sharded(img, n, devices=[0] * int(rng.integers(1, 3)))
+            assert np.array_equal(got.counts, want.counts), (sp, n)
+            assert np.array_equal(got.boundaries, want.boundaries), (sp, n)
+            assert (got.total_runs, got.links, got.hyperedges) == (want.total_runs, want.links, want.hyperedges), (sp, n)
+        c = y.scan_sharded(img, 3, with_hyperedges=False)
+        assert np.array_equal(c.counts, counts) and c.hyperedges == -1
