@@ -1,22 +1,32 @@
-// ychg_scan.cu -- the yCHG hot path on sm_100a: ONE persistent, cooperative
-// kernel per scan.
+// ychg_scan.cu -- the yCHG hot path on sm_100a: two kernels per scan, chained by
+// programmatic dependent launch (PDL), graph-capturable.
 //
 //   K1  per-column cut-vertex counts      (reference runscan.cpp:41-74,122-128)
 //   K2  change flags + ascending boundary  (runscan.cpp:145-153)
 //   K3  hyperedge total = runs - links     (hypergraph.cpp:94-170,192)
 //
-// Work split: the mask is cut into 1024-column strips (one 32-bit word per
-// lane) and every strip into k row segments; CTA g owns segments g, g+G, ...
-// A segment is split into 8 consecutive warp bands.  Each warp streams its band
-// through its own 4-stage TMA ring (cp.async.bulk.tensor, 32 rows x 144 B per
-// stage: 128 B of the strip + a 16 B right halo) and runs K1 + K3 bit-sliced
-// in registers; the CTA then merges its 8 warps in shared memory and writes one
-// partial per segment (coalesced).  The LAST CTA to finish a strip (ticket
-// counter) finishes it: sums the k partials, writes the counts, stitches the K3
-// summaries top to bottom, computes the change flags (waiting on the left
-// neighbour strip's last count) and compacts the boundary list with a
-// decoupled look-back over strips.  The last strip finisher writes the totals.
-// Cross-CTA waits are safe because the launch is cooperative (all CTAs resident).
+// ychg_scan_kernel<with_links, NW> (streaming): the mask is cut into 1024-column
+// strips (one 32-bit word per lane) and every strip into k row segments; CTA g
+// owns segments g, g+G, ...  A segment is split into NW consecutive warp bands
+// (NW = 4 for the ALU-bound K1+K3 path, 8 for the HBM-bound counts path).  Each
+// warp streams its band through its own 3-stage TMA ring (cp.async.bulk.tensor,
+// 32 rows x 144 B per stage: 128 B of the strip + a 16 B right halo) and runs K1
+// + K3 bit-sliced in registers; the CTA merges its warps in shared memory and
+// writes one partial per segment (counts + K3 band summary + links, coalesced)
+// into a workspace double-buffered by scan parity, then release-stores an
+// epoch-tagged segment flag.
+//
+// ychg_finish_kernel<with_links> (one small CTA per strip, co-resident with the
+// streaming CTAs): waits for its strip's k flags, loads the partials, releases
+// the buffer half, composes the K3 summaries, publishes a strip record and
+// derives its boundary offset and first-column flag from every record to its
+// left (warp-parallel look-back), compacts the boundary list; the right-most
+// strip writes the totals.
+//
+// Consecutive scans overlap (the finisher of scan t runs while scan t+1
+// streams).  The invariants that make this safe are listed in DESIGN.md §3
+// ("Cross-scan invariants"): per-half fin_loaded, every per-segment input read
+// before the half is released, scan tickets drawn before launch_dependents.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
