@@ -1,4 +1,5 @@
-// ychg_aux.cu -- K0 on-device synth and the stand-alone boundary detector.
+// ychg_aux.cu -- K0 on-device synth, the stand-alone boundary detector, the
+// host-path re-pitch and the PNM raster kernels (P5 threshold+pack, P4 pad mask).
 //
 // K0 reproduces the reference generators bit for bit (synth.cpp:38-104).  The
 // random pattern draws one SplitMix64 value per pixel in row-major order

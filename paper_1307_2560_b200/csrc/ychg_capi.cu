@@ -211,7 +211,7 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         if (p.seg_per_strip > ychg_dev::kMaxSegPerStrip)
             return fail(YCHG_ERR_INVALID, "plan_create: height %d needs more than %d row segments per strip",
                         height, ychg_dev::kMaxSegPerStrip);
-        // Cooperative launch: every CTA must be co-resident (cross-CTA waits).
+        // Occupancy of each path's streaming kernel (its grid is capped to what is resident).
         int per_sm = 0;
         if (const int rc2 = ychg_scan_kernel_prepare())
             return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
