@@ -212,7 +212,6 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
             return fail(YCHG_ERR_INVALID, "plan_create: height %d needs more than %d row segments per strip",
                         height, ychg_dev::kMaxSegPerStrip);
         // Occupancy of each path's streaming kernel (its grid is capped to what is resident).
-        int per_sm = 0;
         if (const int rc2 = ychg_scan_kernel_prepare())
             return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
         // Each path's streaming kernel has its own CTA width, hence its own grid:
