@@ -37,23 +37,18 @@ struct ProfileArgs {
 };
 
 // Word `w` of row y in MSB-first column order (bit 31 - j = column 32w + j),
-// bytes past the row are zero and columns >= width are masked off.
+// rows outside [0, height) are zero and columns >= width are masked off.
+// Branch-free so a chunk's loads issue back to back: the row index is clamped
+// and the result selected afterwards, and the word is always read whole -- the
+// pitch is a multiple of 16 B, and bytes past the row (padding) only feed
+// columns >= width, which the mask clears.
 __device__ __forceinline__ uint32_t load_word(const ProfileArgs& a, int w, int y) {
-    if (y < 0 || y >= a.height) return 0u;
-    const uint8_t* row = a.bits + static_cast<int64_t>(y) * a.pitch;
-    const int b0 = 4 * w;
-    uint32_t v;
-    if (b0 + 4 <= a.row_bytes) {
-        v = __ldg(reinterpret_cast<const uint32_t*>(row + b0));  // rows are 16 B aligned (pitch)
-    } else {
-        v = 0;
-        for (int q = 0; q < 4; ++q)
-            if (b0 + q < a.row_bytes) v |= static_cast<uint32_t>(__ldg(row + b0 + q)) << (8 * q);
-    }
+    const int yc = min(max(y, 0), a.height - 1);
+    uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(a.bits + static_cast<int64_t>(yc) * a.pitch + 4 * w));
     v = __byte_perm(v, 0u, 0x0123u);
     const int n = a.width - 32 * w;
     if (n < 32) v &= n <= 0 ? 0u : ~(0xFFFFFFFFu >> n);
-    return v;
+    return (y < 0 || y >= a.height) ? 0u : v;
 }
 
 // P1: counts[band][col] = rises of column col in rows [band*256, band*256+256).
