@@ -674,7 +674,7 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
 template <typename Upload>
 int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, int32_t with_hyperedges,
                      int32_t* counts_out, int32_t* boundaries_out, ychg_totals* totals_out, Upload&& upload,
-                     int32_t width_img = -1) {
+                     int32_t width_img = -1, int32_t* d_counts_dst = nullptr) {
     if (width_img < width) width_img = width;
     const int64_t row_bytes = (int64_t(width_img) + 7) / 8;
 
@@ -706,8 +706,10 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
         for (auto& e : tev) cudaEventCreate(&e);
         cudaEventRecord(tev[0], c.stream);
     }
-    if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, c.d_counts, c.d_flags,
-                                        c.d_bounds, c.d_totals, c.stream))
+    // d_counts_dst: the counts go straight to another buffer -- possibly on a peer
+    // GPU, so the finisher's stores are the gather (ychg_scan_host_sharded)
+    if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, d_counts_dst ? d_counts_dst : c.d_counts,
+                                        c.d_flags, c.d_bounds, c.d_totals, c.stream))
         return rc;
     if (host_timing) cudaEventRecord(tev[1], c.stream);
     // D2H in one round trip: totals + counts + the whole boundary buffer into pinned
@@ -1435,6 +1437,33 @@ extern "C" int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_
         if (c1 > c0) parts.push_back(Part{c0, c1, std::min<int32_t>(8, width - c1), {}, 0, {}});
     }
     std::vector<int32_t> counts(size_t(std::max(width, 1)), 0);
+    // Peer gather: every strip's finisher stores its counts straight into one
+    // array on the first device (over NVLink for the other devices), which then
+    // runs K2 once -- no host round trip.  Without peer access between every
+    // device and the first, the counts come back through the host instead.
+    const int target = devs[0];
+    bool peer = width > 0 && height > 0;
+    for (const int32_t d : devs)
+        if (peer && d != target) {
+            int ok = 0;
+            if (cudaDeviceCanAccessPeer(&ok, d, target) != cudaSuccess || !ok) peer = false;
+        }
+    int32_t* d_gather = nullptr;
+    if (peer) {
+        for (const int32_t d : devs)
+            if (d != target) {
+                CK(cudaSetDevice(d));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(target, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                    cudaGetLastError();
+                } else if (e != cudaSuccess) {
+                    return cuda_fail(e, "scan_sharded: cudaDeviceEnablePeerAccess");
+                }
+            }
+        CK(cudaSetDevice(target));
+        CK(cudaMalloc(&d_gather, int64_t(width) * 4));
+    }
+    std::unique_ptr<int32_t, void (*)(int32_t*)> gather_guard(d_gather, [](int32_t* q) { cudaFree(q); });
     auto work = [&](size_t slot) {
         for (size_t i = slot; i < parts.size(); i += devs.size()) {
             Part& q = parts[i];
@@ -1445,8 +1474,9 @@ extern "C" int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_
             if (q.rc == YCHG_OK) {
                 const int32_t w_cnt = q.c1 - q.c0, w_img = w_cnt + q.halo;
                 const uint8_t* src = bits + q.c0 / 8;
-                q.rc = scan_host_locked(c, device, w_cnt, height, with_hyperedges, counts.data() + q.c0, nullptr, &q.t,
-                                        [&] { return upload_image(c, src, w_img, height, row_stride); }, w_img);
+                q.rc = scan_host_locked(c, device, w_cnt, height, with_hyperedges, peer ? nullptr : counts.data() + q.c0,
+                                        nullptr, &q.t, [&] { return upload_image(c, src, w_img, height, row_stride); },
+                                        w_img, peer ? d_gather + q.c0 : nullptr);
             }
             if (q.rc != YCHG_OK) q.err = ychg_last_error();
         }
@@ -1463,7 +1493,23 @@ extern "C" int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_
         links += q.t.links;
     }
     int64_t nb = 0;
-    if (width > 0) {
+    if (peer) {  // K2 once, on the device that holds the gathered counts
+        HostContext& c = host_context(target);
+        std::lock_guard<std::mutex> lock(c.mu);
+        if (const int rc = ensure_context(c)) return rc;
+        if (const int rc = ensure_columns(c, width)) return rc;
+        const int rc = ychg_launch_boundaries(d_gather, width, c.d_flags, c.d_bounds,
+                                              reinterpret_cast<long long*>(&c.d_totals->n_boundaries), c.stream);
+        if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "boundary kernels launch");
+        CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(counts.data(), d_gather, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaStreamSynchronize(c.stream));
+        nb = c.h_totals->n_boundaries;
+        if (boundaries_out && nb > 0) {
+            CK(cudaMemcpyAsync(boundaries_out, c.d_bounds, nb * 4, cudaMemcpyDeviceToHost, c.stream));
+            CK(cudaStreamSynchronize(c.stream));
+        }
+    } else if (width > 0) {
         std::vector<int32_t> bounds(static_cast<size_t>(width));
         if (const int rc = ychg_detect_boundary_columns(counts.data(), width, bounds.data(), &nb)) return rc;
         if (boundaries_out && nb > 0) std::memcpy(boundaries_out, bounds.data(), size_t(nb) * 4);
