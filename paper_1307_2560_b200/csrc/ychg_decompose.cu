@@ -46,6 +46,40 @@ __device__ __forceinline__ int64_t first_reaching(const int32_t* __restrict__ ru
     return b;
 }
 
+// The same, galloping out from a guess g in [b, e): neighbouring columns hold
+// similar numbers of runs at similar heights, so the run of column c+1 reaching
+// row `top` sits near index g = b + i * n(c+1) / n(c) for the i-th run of column
+// c -- a few probes (cached by the neighbouring threads) instead of log2(n).
+__device__ __forceinline__ int64_t first_reaching_from(const int32_t* __restrict__ runs, int64_t b, int64_t e,
+                                                       int top, int64_t g) {
+    if (b >= e) return b;
+    g = g < b ? b : (g >= e ? e - 1 : g);
+    int64_t lo, hi;  // answer in [lo, hi]
+    if (__ldg(runs + 3 * g + 2) < top) {  // answer is right of g
+        int64_t step = 1;
+        lo = g + 1;
+        hi = g + 1;
+        while (hi < e && __ldg(runs + 3 * hi + 2) < top) {
+            lo = hi + 1;
+            step <<= 1;
+            hi = g + step;
+        }
+        if (hi > e) hi = e;
+    } else {  // answer is g or left of it
+        int64_t step = 1;
+        hi = g;
+        lo = g - 1;
+        while (lo >= b && __ldg(runs + 3 * lo + 2) >= top) {
+            hi = lo;
+            step <<= 1;
+            lo = g - step;
+        }
+        lo = lo < b ? b : lo + 1;
+    }
+    return first_reaching(runs, lo, hi, top);
+}
+
+
 // D1: for run g, the first overlapping run in column c+1 (resp. c-1) and the
 // overlap count saturated at 2.  ov = right | left << 2.
 __global__ void __launch_bounds__(kThreadsD) decomp_overlap_kernel(const int32_t* __restrict__ runs,
@@ -56,17 +90,22 @@ __global__ void __launch_bounds__(kThreadsD) decomp_overlap_kernel(const int32_t
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
         const int c = __ldg(runs + 3 * g), top = __ldg(runs + 3 * g + 1), bot = __ldg(runs + 3 * g + 2);
         uint32_t cnt_r = 0, cnt_l = 0, jr = kNoLink, jl = kNoLink;
+        const int64_t own0 = __ldg(col_off + c);
+        const int64_t i_own = g - own0;
+        const int32_t n_own = __ldg(counts + c);
         if (c + 1 < width) {
-            const int64_t b = __ldg(col_off + c + 1), e = b + __ldg(counts + c + 1);
-            const int64_t j = first_reaching(runs, b, e, top);
+            const int32_t n = __ldg(counts + c + 1);
+            const int64_t b = __ldg(col_off + c + 1), e = b + n;
+            const int64_t j = first_reaching_from(runs, b, e, top, b + (i_own * n) / (n_own > 0 ? n_own : 1));
             if (j < e && __ldg(runs + 3 * j + 1) <= bot) {
                 cnt_r = 1 + (j + 1 < e && __ldg(runs + 3 * (j + 1) + 1) <= bot);
                 jr = static_cast<uint32_t>(j);
             }
         }
         if (c > 0) {
-            const int64_t b = __ldg(col_off + c - 1), e = b + __ldg(counts + c - 1);
-            const int64_t j = first_reaching(runs, b, e, top);
+            const int32_t n = __ldg(counts + c - 1);
+            const int64_t b = __ldg(col_off + c - 1), e = b + n;
+            const int64_t j = first_reaching_from(runs, b, e, top, b + (i_own * n) / (n_own > 0 ? n_own : 1));
             if (j < e && __ldg(runs + 3 * j + 1) <= bot) {
                 cnt_l = 1 + (j + 1 < e && __ldg(runs + 3 * (j + 1) + 1) <= bot);
                 jl = static_cast<uint32_t>(j);
