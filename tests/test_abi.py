@@ -41,6 +41,14 @@ def test_cxx_dropin_exports_reference_api(y):
     assert "ychg::cut_vertex_counts(ychg::BinaryImage const&, ychg::ScanStrategy)" in out
     assert "ychg::detect_boundary_columns(std::span<int const, 18446744073709551615ul>)" in out
     assert "ychg::foreground_count(ychg::BinaryImage const&)" in out
+    # the rest of runscan.cpp and pnm.cpp (link-time drop-in) + extensions
+    for sym in ("ychg::column_runs(ychg::BinaryImage const&, int)",
+                "ychg::build_profile(ychg::BinaryImage const&, ychg::ScanStrategy)",
+                "ychg::load_pnm(std::span<unsigned char const, 18446744073709551615ul>, int)",
+                "ychg::save_pnm(ychg::BinaryImage const&)",
+                "ychg::scan(ychg::BinaryImage const&)",
+                "ychg::scan_sharded(ychg::BinaryImage const&, int, std::span<int const, 18446744073709551615ul>)"):
+        assert sym in out, sym
 
 
 def test_abi_version(y):
