@@ -234,8 +234,9 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         const int64_t S = p.n_strips, G = p.n_segments;
         // part / sums / seg_links / seg_status are double-buffered by scan parity
         const int64_t sz_part = 2 * G * 512 * 4, sz_sums = 2 * G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = 2 * G * 8;
-        if (height >= (1 << 22))
-            return fail(YCHG_ERR_INVALID, "plan_create: height %d >= 2^22 rows is not supported", height);
+        // strip records pack column counts (<= ceil(height/2)) in 21 bits
+        if (height > (1 << 22) - 2)
+            return fail(YCHG_ERR_INVALID, "plan_create: height %d > 2^22-2 rows is not supported", height);
         const int64_t sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
         // order: part | sums | seg_links | seg_ticket | seg_status | fin_ticket | fin_all | fin_loaded[2][S] | rec
         plan->ws_bytes = sz_part + sz_sums + 3 * sz_seg + 3 * S * 8 + 64 + sz_rec + 64;

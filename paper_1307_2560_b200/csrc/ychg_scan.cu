@@ -366,9 +366,12 @@ ychg_finish_kernel(const ScanParams prm) {
     //     segment over the CTA) and the K3 summaries (8 x 224 words).
     constexpr int kR = (512 + kThreads - 1) / kThreads;
     constexpr int kY = (8 * kSumWords + kThreads - 1) / kThreads;
-    uint32_t v[kR];
+    // Per-segment partials are u16x2 words (a segment has <= 65504 rows, so a
+    // column's count in it fits 16 bits); the strip total needs up to 21 bits
+    // (height < 2^22), so the two halves are summed separately.
+    uint32_t v[kR], vh[kR];
 #pragma unroll
-    for (int r = 0; r < kR; ++r) v[r] = 0;
+    for (int r = 0; r < kR; ++r) v[r] = vh[r] = 0;
     for (int g = 0; g < k; g += 8) {
         const int n = k - g < 8 ? k - g : 8;
         uint32_t x[kR][8], y[kY];
@@ -390,7 +393,10 @@ ychg_finish_kernel(const ScanParams prm) {
 #pragma unroll
         for (int r = 0; r < kR; ++r)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[r] += x[r][u];
+            for (int u = 0; u < 8; ++u) {
+                v[r] += x[r][u] & 0xFFFFu;
+                vh[r] += x[r][u] >> 16;
+            }
         if (kLinks) {
 #pragma unroll
             for (int u = 0; u < kY; ++u) {
@@ -404,8 +410,8 @@ ychg_finish_kernel(const ScanParams prm) {
         const int idx = tid + r * kThreads;
         if (idx < 512) {
             const int i = idx >> 5, ln = idx & 31;
-            fs.sc[32 * ln + acc_column<kLinks>(i, 0)] = static_cast<int32_t>(v[r] & 0xFFFFu);
-            fs.sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(v[r] >> 16);
+            fs.sc[32 * ln + acc_column<kLinks>(i, 0)] = static_cast<int32_t>(v[r]);
+            fs.sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(vh[r]);
         }
     }
     __syncthreads();

@@ -474,3 +474,16 @@ def test_scan_sharded_matches_single_device(gpu, orc):
             assert (got.total_runs, got.links, got.hyperedges) == (want.total_runs, want.links, want.hyperedges), (sp, n)
         c = y.scan_sharded(img, 3, with_hyperedges=False)
         assert np.array_equal(c.counts, counts) and c.hyperedges == -1
+
+
+def test_very_wide_and_very_tall(gpu, orc):
+    """Extreme aspect ratios: ~977 strips of one row segment each (a long
+    finisher look-back chain), and one strip of 4M rows (128 segments per strip)."""
+    y = gpu
+    for sp in (Spec.random(1_000_000, 40, 0.5, 17), Spec.random(40, 4_000_000, 0.5, 18)):
+        bits = orc.synth(sp)
+        r = y.scan(y.BinaryImage(sp.width, sp.height, bits))
+        counts = orc.counts(bits, sp.width)
+        assert np.array_equal(r.counts, counts)
+        assert np.array_equal(r.boundaries, orc.boundaries(counts))
+        assert r.hyperedges == orc.hyperedges(bits, sp.width)[0]
