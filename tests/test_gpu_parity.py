@@ -409,6 +409,8 @@ def test_pipelined_graph_random_geometries(gpu, orc, monkeypatch):
         W = int(rng.choice([1, 31, 33, 1023, 1025, 2049, 3000, 5000]))
         H = int(rng.choice([1, 2, 31, 33, 257, 1000, 2500]))
         monkeypatch.setenv("YCHG_SEGMENTS", str(int(rng.integers(1, 9))))
+        # some trials with a tiny grid: every CTA then streams several segments
+        monkeypatch.setenv("YCHG_GRID", str(int(rng.choice([1, 2, 3, 1000]))))
         specs = [Spec.random(W, H, float(rng.choice([0.1, 0.5, 0.9])), int(rng.integers(0, 1 << 40))) for _ in range(3)]
         pitch = y.pitch_for(W)
         imgs = []
