@@ -146,3 +146,17 @@ def test_decompose_into_pinned_buffers(gpu, orc):
     assert y.decompose(img, out=small) == y.decompose(img)
     buf.close()
     small.close()
+
+
+def test_profile_and_decompose_tall(gpu, orc):
+    """Columns with > 65535 runs (tall masks): build_profile and decompose vs the oracle."""
+    y = gpu
+    sp = Spec.random(37, 300_001, 0.5, 23)
+    bits = orc.synth(sp)
+    img = y.BinaryImage(sp.width, sp.height, bits)
+    prof = y.build_profile(img)
+    assert np.array_equal(prof.runs_flat, orc.profile(bits, sp.width))
+    assert prof.counts.max() > 65535
+    got = y.decompose(img)
+    for a, b in zip(as_tuple(got), orc.decompose(bits, sp.width)):
+        assert np.array_equal(a, b)
