@@ -29,7 +29,7 @@ st = plan.debug_stamps(True).astype(np.float64)
 G = info.grid
 for ring in range(4):
     e = st[ring, :G]
-    nw = int((e[:, 1:17] > 0).any(0).sum()) or 8
+    nw = 4 if links else 8  # streaming CTA width per path (ychg_device.cuh scan_warps)
     warps = e[:, 1:1 + nw]
     dur = (e[:, 23] - e[:, 0]) / 1e3
     imb = (warps.max(1) - warps.min(1)) / 1e3
