@@ -456,6 +456,7 @@ def run_ours(a):
             "hbm_gbs_step": round((img_bytes + 4 * Ws + 4 * n_b + 32) / (ms_step * 1e-3) / 1e9, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": profiled_traffic(img_bytes),
+                         "frac_of_nominal_7700": round(achieved / 7700.0, 4),  # HGX B200 HBM3e nominal, context only
                          "kernel": "ychg_scan_kernel + ychg_finish_kernel (2 PDL launches per step)",
                          "kernel_ms": round(scan_avg, 5), "algorithmic_bytes": img_bytes,
                          "peak_source": peak_src,
