@@ -417,9 +417,23 @@ def run_ours(a):
         if with_links and exp is not None and r.hyperedges != exp:
             raise SystemExit("e2e hyperedge total mismatch")
         t_med = sorted(ts)[len(ts) // 2]
+        # the PCIe floor on this box: a bare pinned H2D copy of the same bytes (context only)
+        dev = torch.empty_like(host, device="cuda")
+        fl = []
+        for _ in range(max(3, min(a.steps, 10))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dev.copy_(host, non_blocking=True)
+            torch.cuda.synchronize()
+            fl.append(time.perf_counter() - t0)
+        del dev
+        f_med = sorted(fl)[len(fl) // 2]
         e2e = {"value": round(Ws * H / t_med / 1e9, 3), "unit": "Gpixel/s",
                "h2d_bytes_per_step": img_bytes, "d2h_bytes_per_step": 4 * Ws + 32 + 4 * n_b,
-               "ms_per_step": round(t_med * 1e3, 3), "api": "ychg_scan_host (pinned host buffer)"}
+               "ms_per_step": round(t_med * 1e3, 3), "api": "ychg_scan_host (pinned host buffer)",
+               "h2d_copy_floor_ms": round(f_med * 1e3, 3),
+               "h2d_copy_gbs": round(host.numel() / f_med / 1e9, 2),
+               "frac_of_copy_floor": round(f_med / t_med, 4)}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

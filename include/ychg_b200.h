@@ -194,6 +194,14 @@ YCHG_API int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, 
  * busy) instead of back-to-back pipelined scans (the default: fewer, longer CTAs
  * for large masks so consecutive scans overlap). */
 #define YCHG_PLAN_LATENCY 1
+/* YCHG_PLAN_SYNC_INPUTS: the streaming kernel waits (griddepcontrol.wait) for the
+ * kernel launched just before it on the stream to complete and flush before it
+ * reads the image.  Without it the streaming kernel is a programmatic dependent
+ * launch that does not wait: d_bits must then be complete before the kernel that
+ * immediately precedes the scan starts (written by a memcpy, an event-ordered
+ * stream, or any earlier kernel -- as in back-to-back scans of resident images).
+ * Set it when a kernel of yours writes d_bits right before ychg_scan_device. */
+#define YCHG_PLAN_SYNC_INPUTS 2
 YCHG_API int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_t height, int32_t flags,
                                  ychg_plan** out);
 YCHG_API void ychg_plan_destroy(ychg_plan* plan);

@@ -459,14 +459,17 @@ class Plan:
     """Geometry-specific launch plan + workspace on one device (ychg_plan_*)."""
 
     def __init__(self, width_img: int, height: int, width_cnt: int | None = None, device: int = 0,
-                 latency: bool = False):
+                 latency: bool = False, sync_inputs: bool = False):
         """latency=True sizes the launch for isolated scans (YCHG_PLAN_LATENCY); the
-        default favours back-to-back (pipelined / graph-captured) scans."""
+        default favours back-to-back (pipelined / graph-captured) scans.
+        sync_inputs=True (YCHG_PLAN_SYNC_INPUTS): the streaming kernel waits for the
+        kernel launched just before it, for images written by that kernel."""
         self.device = device
         self.width_img, self.height = int(width_img), int(height)
         self.width_cnt = self.width_img if width_cnt is None else int(width_cnt)
         h = _vp()
-        _check(_lib.ychg_plan_create_ex(device, self.width_img, self.width_cnt, self.height, int(bool(latency)),
+        _check(_lib.ychg_plan_create_ex(device, self.width_img, self.width_cnt, self.height,
+                                        int(bool(latency)) | 2 * int(bool(sync_inputs)),
                                         ctypes.byref(h)), "plan_create")
         self._h = h
 

@@ -189,38 +189,60 @@ extern "C" int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32
 
 // ---- dense host layout -> pitched device layout (TMA needs 16 B-aligned row strides).
 // dst row y byte x (x < pitch) = src[y * row_bytes + x] for x < row_bytes, else 0.
-// Each thread assembles 4 destination bytes from two aligned source words.
+// One warp per row, one 16 B destination word per lane and step: two aligned
+// 16 B source loads, shifted into place.  The source offset within a 16 B word
+// depends on the row only, so the word select below is warp-uniform.
 namespace {
-__global__ void repitch_kernel(const uint8_t* __restrict__ src, int64_t row_bytes, uint8_t* __restrict__ dst,
-                               int64_t pitch, int y0, int y1) {
-    const int64_t words_per_row = pitch >> 2;
-    const int64_t total = static_cast<int64_t>(y1 - y0) * words_per_row;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t yy = i / words_per_row;
-        const int64_t x = (i - yy * words_per_row) * 4;
-        const int64_t y = y0 + yy;
-        uint32_t out = 0;
-        if (x < row_bytes) {
-            const int64_t s = y * row_bytes + x;
-            const uint32_t* base = reinterpret_cast<const uint32_t*>(src + (s & ~int64_t(3)));
-            const uint32_t sh = static_cast<uint32_t>(s & 3) * 8;
-            out = __funnelshift_r(__ldg(base), __ldg(base + 1), sh);
-            const int64_t valid = row_bytes - x;
-            if (valid < 4) out &= (1u << (8 * valid)) - 1u;
+__global__ void __launch_bounds__(256) repitch_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
+                                                       uint8_t* __restrict__ dst, int64_t pitch, int y0, int y1) {
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const int64_t nq = pitch >> 4;
+    for (int y = y0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); y < y1; y += warps) {
+        const int64_t row0 = int64_t(y) * row_bytes;
+        const int off = static_cast<int>(row0 & 15);
+        const int kw = off >> 2;
+        const uint32_t sh = static_cast<uint32_t>(off & 3) * 8;
+        const uint4* srow = reinterpret_cast<const uint4*>(src + (row0 - off));
+        uint4* drow = reinterpret_cast<uint4*>(dst + int64_t(y) * pitch);
+        for (int64_t q = lane; q < nq; q += 32) {
+            uint4 o = make_uint4(0, 0, 0, 0);
+            const int64_t valid = row_bytes - q * 16;
+            if (valid > 0) {
+                const uint4 A = __ldg(srow + q), B = __ldg(srow + q + 1);
+                uint32_t u0, u1, u2, u3, u4;
+                switch (kw) {
+                    case 0: u0 = A.x, u1 = A.y, u2 = A.z, u3 = A.w, u4 = B.x; break;
+                    case 1: u0 = A.y, u1 = A.z, u2 = A.w, u3 = B.x, u4 = B.y; break;
+                    case 2: u0 = A.z, u1 = A.w, u2 = B.x, u3 = B.y, u4 = B.z; break;
+                    default: u0 = A.w, u1 = B.x, u2 = B.y, u3 = B.z, u4 = B.w; break;
+                }
+                o.x = __funnelshift_r(u0, u1, sh);
+                o.y = __funnelshift_r(u1, u2, sh);
+                o.z = __funnelshift_r(u2, u3, sh);
+                o.w = __funnelshift_r(u3, u4, sh);
+                if (valid < 16) {  // the row's last word: zero the bytes past row_bytes
+                    auto keep = [&](int j) {
+                        const int64_t v = valid - 4 * j;
+                        return v >= 4 ? 0xFFFFFFFFu : v <= 0 ? 0u : (1u << (8 * v)) - 1u;
+                    };
+                    o.x &= keep(0), o.y &= keep(1), o.z &= keep(2), o.w &= keep(3);
+                }
+            }
+            drow[q] = o;
         }
-        reinterpret_cast<uint32_t*>(dst + y * pitch)[x >> 2] = out;
     }
 }
 }  // namespace
 
-// src must have >= 8 readable bytes past its last row (the caller over-allocates).
+// src must have >= 32 readable bytes past its last row (the caller over-allocates)
+// and be 16 B aligned; dst rows are `pitch` (multiple of 16) bytes.
 extern "C" int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint8_t* d_dst, int64_t pitch, int y0,
                                    int y1, cudaStream_t stream) {
-    const int64_t total = static_cast<int64_t>(y1 - y0) * (pitch >> 2);
-    if (total <= 0) return 0;
-    int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    const int64_t rows = static_cast<int64_t>(y1) - y0;
+    if (rows <= 0 || pitch <= 0) return 0;
+    int64_t blocks = (rows + 7) / 8;  // 8 warps (rows) per block
+    if (blocks > 148 * 8) blocks = 148 * 8;
     repitch_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_src, row_bytes, d_dst, pitch, y0, y1);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);

@@ -199,6 +199,7 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
     p.n_blocks = (height + ychg_dev::kBlockRows - 1) / ychg_dev::kBlockRows;
     if (p.n_strips > 0 && p.n_blocks > 0) {
         p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid, (flags & YCHG_PLAN_LATENCY) != 0);
+        p.wait_inputs = (flags & YCHG_PLAN_SYNC_INPUTS) ? 1 : 0;
         // experiment hooks (benchmarking only): force the segments per strip / grid
         if (const char* v = getenv("YCHG_SEGMENTS"); v && *v) {
             // (never more segments than 32-row blocks: a segment must not be empty)
@@ -634,12 +635,12 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
                              c.stream));
     } else {
         const int64_t dense = row_bytes * height;
-        if (dense + 16 > c.dense_cap) {
+        if (dense + 32 > c.dense_cap) {
             cudaFree(c.d_dense);
             c.d_dense = nullptr;
             c.dense_cap = 0;
-            CK(cudaMalloc(&c.d_dense, dense + 16));
-            c.dense_cap = dense + 16;
+            CK(cudaMalloc(&c.d_dense, dense + 32));
+            c.dense_cap = dense + 32;
         }
         CK(cudaEventRecord(c.chunk_ev[0], c.stream));  // order after earlier work on c.stream
         CK(cudaStreamWaitEvent(c.copy_stream, c.chunk_ev[0], 0));
@@ -650,9 +651,12 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
             return n < 1 ? 1 : (n > HostContext::kChunks ? HostContext::kChunks : n);
         }();
         const int nch = height >= max_chunks * 64 ? max_chunks : 1;
+        // The last chunk is an eighth of the rows: only its re-pitch is exposed after
+        // the final copy; the earlier chunks' re-pitch hides under the later copies.
+        const int tail = nch > 1 ? height / 8 : 0;
         for (int i = 0; i < nch; ++i) {
-            const int y0 = static_cast<int>((int64_t(height) * i) / nch);
-            const int y1 = static_cast<int>((int64_t(height) * (i + 1)) / nch);
+            const int y0 = static_cast<int>((int64_t(height - tail) * i) / (nch - (nch > 1)));
+            const int y1 = i == nch - 1 ? height : static_cast<int>((int64_t(height - tail) * (i + 1)) / (nch - 1));
             CK(cudaMemcpyAsync(c.d_dense + y0 * row_bytes, bits + y0 * row_bytes, (y1 - y0) * row_bytes,
                                cudaMemcpyHostToDevice, c.copy_stream));
             CK(cudaEventRecord(c.chunk_ev[i], c.copy_stream));
@@ -689,7 +693,9 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
         c.plan = nullptr;
         c.plan_w = c.plan_wc = c.plan_h = -1;
         // one scan per call, synchronised: size the plan for latency, not pipelining
-        if (const int rc = ychg_plan_create_ex(device, width_img, width, height, YCHG_PLAN_LATENCY, &c.plan))
+        // the image is written by the kernel just before the scan (re-pitch / PNM pack)
+        if (const int rc = ychg_plan_create_ex(device, width_img, width, height,
+                                               YCHG_PLAN_LATENCY | YCHG_PLAN_SYNC_INPUTS, &c.plan))
             return rc;
         c.plan_w = width_img;
         c.plan_wc = width;

@@ -110,6 +110,7 @@ struct ScanParams {
     int32_t* boundaries;      // [<= width_cnt] ascending boundary columns
     unsigned long long* dbg;  // optional [4][dbg_rows][32] %globaltimer stamps (diagnostics), or null
     int32_t dbg_rows;
+    int32_t wait_inputs;      // 1: griddepcontrol.wait before the first image load (YCHG_PLAN_SYNC_INPUTS)
 };
 
 // Segment j of a strip covers row blocks [seg_first(j), seg_first(j+1)).

@@ -613,6 +613,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     // Let this scan's finisher kernel launch now: its CTAs are small, co-reside
     // with ours and wait on the per-segment flags (programmatic dependent launch).
     asm volatile("griddepcontrol.launch_dependents;");
+    // The streaming kernel is a programmatic dependent of whatever kernel precedes
+    // it on the stream.  Back-to-back scans need no wait (the image was written
+    // before the previous scan's finisher ran); a plan whose image is written by
+    // the immediately preceding kernel (host path: re-pitch / PNM pack) waits for
+    // that grid's completion and memory flush here.
+    if (prm.wait_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");
 
     uint8_t* my_stages = stages + warp * kStages * kStageBytes;
     uint64_t* my_bars = bars + warp * kStages;
