@@ -489,3 +489,35 @@ def test_very_wide_and_very_tall(gpu, orc):
         assert np.array_equal(r.counts, counts)
         assert np.array_equal(r.boundaries, orc.boundaries(counts))
         assert r.hyperedges == orc.hyperedges(bits, sp.width)[0]
+
+
+def test_sync_inputs_image_written_by_preceding_kernel(gpu, orc):
+    """YCHG_PLAN_SYNC_INPUTS: each image is written by the synth kernel launched right
+    before the scan on the same stream, into one reused buffer, with no host sync in
+    between -- the streaming kernel must wait for that grid before its first load."""
+    import torch
+    y = gpu
+    W, H = 5000, 3000
+    pitch = y.pitch_for(W)
+    d = torch.zeros((H, pitch), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    specs = [Spec.random(W, H, 0.5, 31), Spec.hbands(W, H, 40), Spec.checker(W, H, 2), Spec.random(W, H, 0.1, 32)] * 2
+    for latency in (False, True):
+        plan = y.Plan(W, H, latency=latency, sync_inputs=True)
+        outs = []
+        for sp in specs:
+            name = {v: k for k, v in y.PATTERNS.items()}[sp.pattern]
+            y.synth_device(name, W, H, d.data_ptr(), pitch, bands=sp.bands, cell=sp.cell, density=sp.density,
+                           seed=sp.seed, stream=stream)
+            c = torch.full((W,), -7, dtype=torch.int32, device="cuda")
+            f = torch.zeros(W // 32 + 64, dtype=torch.int32, device="cuda")
+            b = torch.full((W,), -7, dtype=torch.int32, device="cuda")
+            t = torch.zeros(4, dtype=torch.int64, device="cuda")
+            plan.scan_device(d.data_ptr(), pitch, c.data_ptr(), f.data_ptr(), b.data_ptr(), t.data_ptr(), stream)
+            outs.append((sp, c, t))
+        torch.cuda.synchronize()
+        for sp, c, t in outs:
+            bits = orc.synth(sp)
+            assert np.array_equal(c.cpu().numpy(), orc.counts(bits, W)), sp
+            assert t.cpu().tolist()[2] == orc.hyperedges(bits, W)[0], sp
+        plan.close()
