@@ -56,6 +56,25 @@ def parse():
     return ap.parse_args()
 
 
+HOLD_NOTE = ("spin kernel holds the stream while the host submits the timed work, so the region "
+             "measures device execution, not graph-submission latency (nvbench's blocking-kernel method)")
+
+
+def hold_cycles(steps: int) -> int:
+    """Spin length before the start event: ~10 us of submission budget per step, >= 0.2 ms.
+    YCHG_BENCH_HOLD_CYCLES overrides (0 disables)."""
+    v = os.environ.get("YCHG_BENCH_HOLD_CYCLES")
+    return int(v) if v is not None else max(400_000, 20_000 * steps)
+
+
+def hold_stream(stream, steps: int) -> None:
+    n = hold_cycles(steps)
+    if n > 0:
+        import torch
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(n)
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -334,6 +353,7 @@ def run_ours(a):
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hold_stream(stream, a.steps)
     ev0.record(stream)
     if graph is not None:
         graph.replay()
@@ -367,6 +387,7 @@ def run_ours(a):
         g2.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        hold_stream(stream, a.steps)
         e0.record(stream)
         g2.replay()
         e1.record(stream)
@@ -474,8 +495,9 @@ def run_ours(a):
                          "kernel": "ychg_scan_kernel + ychg_finish_kernel (2 PDL launches per step)",
                          "kernel_ms": round(scan_avg, 5), "algorithmic_bytes": img_bytes,
                          "peak_source": peak_src,
-                         "timing": "CUDA events around a K-step CUDA graph replay" if graph is not None
-                         else "CUDA events around K eager steps (graph capture with collectives failed)"},
+                         "timing": ("CUDA events around a K-step CUDA graph replay" if graph is not None
+                                    else "CUDA events around K eager steps (graph capture with collectives failed)")
+                         + (f"; a {HOLD_NOTE}" if hold_cycles(a.steps) > 0 else "")},
             "eager_launch_ms": round(sorted(eager_ms)[len(eager_ms) // 2], 5),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "north_star_subset": alt,
             "gpu_launches": info.kernels_per_scan * a.steps,  # per timed graph (the subset graph: as many again)
