@@ -406,6 +406,7 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     p.dbg = plan->dbg;
     p.dbg_rows = std::max(std::max(plan->grid, plan->grid_counts), p.n_strips);
     p.mul2 = 2u;
+    p.mul1 = 1u;
     p.mulnb = 1u << 25;
 
     if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));

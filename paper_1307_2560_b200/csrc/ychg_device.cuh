@@ -94,6 +94,7 @@ struct ScanParams {
     int32_t seg_per_strip;    // k: row segments per strip
     int32_t n_segments;       // n_strips * k
     uint32_t mul2, mulnb;     // 2 and 1 << 25 as runtime values: keeps the b-word shifts on IMAD
+    uint32_t mul1;            // 1 as a runtime value: keeps the link adds on IMAD
     uint32_t* part;           // [n_segments][512] per-segment u16x2 column counts
     uint32_t* sums;           // [n_segments][7][32] K3 band summaries
     unsigned long long* seg_links;    // [n_segments] links closed inside each segment

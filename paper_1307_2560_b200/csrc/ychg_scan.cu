@@ -115,9 +115,14 @@ __device__ __forceinline__ uint32_t right_neighbour_msb(uint32_t a, uint32_t nb,
     return a * mul2 + __umulhi(nb, mul25);
 }
 
-template <bool kLinks, bool kHead, bool kBs = kLinks>
+// kMask (strips with invalid column pairs -- the image's last column, or a
+// multi-GPU strip's right halo): the right-hand column of an invalid pair is
+// zeroed, so its components hold one run and never link.  Full strips skip it,
+// which lets the two row links of a pair be added on the FMA pipe (they are
+// disjoint bit sets) instead of a masked LOP3.
+template <bool kLinks, bool kHead, bool kBs = kLinks, bool kMask = false>
 __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage, int lane,
-                                              LaneState& s, uint32_t mul2, uint32_t mulnb) {
+                                              LaneState& s, uint32_t mul2, uint32_t mulnb, uint32_t mul1) {
     const uint8_t* p = stage + 4 * lane;
     uint32_t Pprev = 0, tA = 0, fA = 0, eA = 0;
 #pragma unroll
@@ -132,13 +137,18 @@ __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage,
         }
         const uint32_t P = lop3<0x3A>(a0, s.pa, a1);  // (a0 & ~pa) | (a1 & ~a0)
         if (kLinks) {
-            const uint32_t b0 = kBs ? right_neighbour_msb(a0, r0[4], mul2, mulnb)
-                                    : right_neighbour(a0, r0[4], mul2, mulnb);
-            const uint32_t b1 = kBs ? right_neighbour_msb(a1, r1[4], mul2, mulnb)
-                                    : right_neighbour(a1, r1[4], mul2, mulnb);
+            uint32_t b0 = kBs ? right_neighbour_msb(a0, r0[4], mul2, mulnb)
+                              : right_neighbour(a0, r0[4], mul2, mulnb);
+            uint32_t b1 = kBs ? right_neighbour_msb(a1, r1[4], mul2, mulnb)
+                              : right_neighbour(a1, r1[4], mul2, mulnb);
+            if (kMask) {
+                b0 &= s.mk3;
+                b1 &= s.mk3;
+            }
             const uint32_t l0 = k3_step<kHead>(a0, b0, s);
             const uint32_t l1 = k3_step<kHead>(a1, b1, s);
-            s.links += __popc(lop3<0xA8>(l0, l1, s.mk3));  // (l0 | l1) & mk3
+            // l0 | l1 == l0 + l1 (disjoint); IMADs keep both adds off the ALU pipe
+            s.links = __popc(l0 * mul1 + l1) * mul1 + s.links;
         } else {
             s.pa = a1;
         }
@@ -652,6 +662,8 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 #pragma unroll
         for (int i = 0; i < 16; ++i) s.acc[i] = 0;
         s.mk3 = word_mask(gw, min(prm.width_cnt, prm.width_img - 1));  // MSB-first, like the K3 words
+        // every column pair of this warp's strip valid (warp-uniform): no per-row mask
+        const bool full = !kLinks || __all_sync(0xFFFFFFFFu, s.mk3 == 0xFFFFFFFFu);
         s.h1 = s.h2 = 0;
         s.links = 0;
         s.pa = s.pb = 0;
@@ -699,9 +711,13 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 #else
                 if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u))
 #endif
-                    process_block<kLinks, true>(sp, lane, s, prm.mul2, prm.mulnb);
-                else
-                    process_block<kLinks, false>(sp, lane, s, prm.mul2, prm.mulnb);
+                {
+                    if (full) process_block<kLinks, true, kLinks, false>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
+                    else process_block<kLinks, true, kLinks, true>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
+                } else {
+                    if (full) process_block<kLinks, false, kLinks, false>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
+                    else process_block<kLinks, false, kLinks, true>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
+                }
                 __syncwarp();
 #ifdef YCHG_COMPUTE_ONLY
                 if (false) {

@@ -16,7 +16,7 @@ __global__ void __launch_bounds__(256) blk(uint32_t* out, int iters, uint32_t mu
     const int lane = threadIdx.x & 31;
     for (int it = 0; it < iters; ++it) {
         asm volatile("" ::: "memory");  // force the smem reloads every iteration (no hoisting)
-        process_block<kLinks, kHead, kBs>(stage, lane, s, mul2, mul17);
+        process_block<kLinks, kHead, kBs>(stage, lane, s, mul2, mul17, mul2 >> 1);
         if ((it & 15) == 15) flush_counts(s);
     }
     uint32_t r = s.links ^ s.G2 ^ s.G3 ^ s.h1;
