@@ -49,6 +49,9 @@ void run(int threads, int blocks_per_sm) {
 }
 
 int main() {
+    run<false>(128, 1);  // the streaming CTA shape (4 warps): 1..3 resident per SM
+    run<false>(128, 2);
+    run<false>(128, 3);
     run<false>(256, 1);
     run<false>(256, 2);
     run<false>(256, 4);
