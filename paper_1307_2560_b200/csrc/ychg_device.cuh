@@ -54,17 +54,25 @@ constexpr int kSmemTotal = kSmemStages + kSmemBar + kSmemAcc + kSmemSum + kSmemM
 #endif
 constexpr int kWarpsLinks = YCHG_WARPS_LINKS;
 constexpr int kWarpsCounts = kWarps;
-template <int NW>
+#ifndef YCHG_STAGES_LINKS
+#define YCHG_STAGES_LINKS YCHG_STAGES
+#endif
+constexpr int kStagesLinks = YCHG_STAGES_LINKS;  // TMA ring depth per warp of the full path
+template <int NW, int ST = kStages>
 struct ScanSmem {
-    static constexpr int kStagesB = NW * kStages * kStageBytes;
-    static constexpr int kBar = NW * kStages * 8;
+    static constexpr int kStagesB = NW * ST * kStageBytes;
+    static constexpr int kBar = NW * ST * 8;
     static constexpr int kAcc = NW * 16 * 32 * 4;
     static constexpr int kSum = NW * kSumPlanes * 32 * 4;
     static constexpr int kMisc = NW * 24 + 48;
     static constexpr int kTotal = kStagesB + kBar + kAcc + kSum + kMisc;
 };
 template <bool kLinks>
-constexpr int scan_warps() { return kLinks ? kWarpsLinks : kWarpsCounts; }
+__host__ __device__ constexpr int scan_warps() { return kLinks ? kWarpsLinks : kWarpsCounts; }
+template <bool kLinks>
+__host__ __device__ constexpr int scan_stages() { return kLinks ? kStagesLinks : kStages; }
+template <bool kLinks>
+__host__ __device__ constexpr int scan_smem() { return ScanSmem<scan_warps<kLinks>(), scan_stages<kLinks>()>::kTotal; }
 
 // What a strip's finisher publishes for the strips to its right: `status`
 // packs the epoch, the number of change flags strictly inside the strip and the

@@ -594,7 +594,8 @@ ychg_finish_kernel(const ScanParams prm) {
 template <bool kLinks, int NW = scan_warps<kLinks>()>
 __global__ void __launch_bounds__(NW * 32, 1)
 ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm) {
-    using L = ScanSmem<NW>;
+    constexpr int kS = scan_stages<kLinks>();  // TMA ring depth of this path
+    using L = ScanSmem<NW, kS>;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stages = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kStagesB);
@@ -613,7 +614,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     __shared__ unsigned long long seg_tick[kMaxSegPerCta];
     const unsigned long long t_entry = globaltimer();
     if (tid == 0) {
-        for (int i = 0; i < NW * kStages; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < NW * kS; ++i) mbar_init(&bars[i], 1);
         int i = 0;
         for (int sg = blockIdx.x; sg < prm.n_segments && i < kMaxSegPerCta; sg += gridDim.x, ++i)
             seg_tick[i] = atomicAdd(prm.seg_ticket + sg, 1ull);
@@ -630,9 +631,9 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     // that grid's completion and memory flush here.
     if (prm.wait_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    uint8_t* my_stages = stages + warp * kStages * kStageBytes;
-    uint64_t* my_bars = bars + warp * kStages;
-    uint32_t it = 0;  // blocks consumed by this warp so far (stage = it % kStages)
+    uint8_t* my_stages = stages + warp * kS * kStageBytes;
+    uint64_t* my_bars = bars + warp * kS;
+    uint32_t it = 0;  // blocks consumed by this warp so far (stage = it % kS)
 
     const int k = prm.seg_per_strip;
     int seg_i = 0;
@@ -672,9 +673,9 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         if (nb > 0) {
             // Kick off the ring first so the halo-row load overlaps it.
             if (lane == 0) {
-                const int npre = nb < kStages ? nb : kStages;
+                const int npre = nb < kS ? nb : kS;
                 for (int i = 0; i < npre; ++i) {
-                    const int st = (it + i) % kStages;
+                    const int st = (it + i) % kS;
                     mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
                     tma_load_2d(my_stages + st * kStageBytes, &tmap, &my_bars[st], x0,
                                 (wb0 + i) * kBlockRows);
@@ -699,11 +700,11 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 
             int since_flush = 0;
             for (int bi = 0; bi < nb; ++bi) {
-                const int st = it % kStages;
-#ifdef YCHG_COMPUTE_ONLY  // diagnostics build: reuse the first kStages blocks, no TMA after the fill
-                if (bi < kStages) mbar_wait(&my_bars[st], (it / kStages) & 1u);
+                const int st = it % kS;
+#ifdef YCHG_COMPUTE_ONLY  // diagnostics build: reuse the first kS blocks, no TMA after the fill
+                if (bi < kS) mbar_wait(&my_bars[st], (it / kS) & 1u);
 #else
-                mbar_wait(&my_bars[st], (it / kStages) & 1u);
+                mbar_wait(&my_bars[st], (it / kS) & 1u);
 #endif
                 const uint8_t* sp = my_stages + st * kStageBytes;
 #ifdef YCHG_NO_HEAD  // diagnostics build: never take the head-mode block (wrong results, timing only)
@@ -722,12 +723,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 #ifdef YCHG_COMPUTE_ONLY
                 if (false) {
 #else
-                if (lane == 0 && bi + kStages < nb) {
+                if (lane == 0 && bi + kS < nb) {
 #endif
                     fence_proxy_async();
                     mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
                     tma_load_2d(my_stages + st * kStageBytes, &tmap, &my_bars[st], x0,
-                                (wb0 + bi + kStages) * kBlockRows);
+                                (wb0 + bi + kS) * kBlockRows);
                 }
                 ++it;
                 if (++since_flush == kFlushBlocks) {
@@ -838,7 +839,7 @@ extern "C" const void* ychg_scan_kernel_ptr(int with_links) {
 // Launch shape of the streaming kernel of a path (for occupancy queries).
 extern "C" void ychg_scan_kernel_shape(int with_links, int* threads, int* smem_bytes) {
     *threads = 32 * (with_links ? scan_warps<true>() : scan_warps<false>());
-    *smem_bytes = with_links ? ScanSmem<scan_warps<true>()>::kTotal : ScanSmem<scan_warps<false>()>::kTotal;
+    *smem_bytes = with_links ? scan_smem<true>() : scan_smem<false>();
 }
 
 constexpr int kFinishSmemMax = 160 * 1024;
@@ -850,10 +851,10 @@ extern "C" int ychg_scan_kernel_prepare(void) {
     cudaGetDevice(&dev);
     if (dev < 64 && done[dev]) return 0;
     cudaError_t e = cudaFuncSetAttribute(&ychg_scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         ScanSmem<scan_warps<true>()>::kTotal);
+                                         scan_smem<true>());
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 ScanSmem<scan_warps<false>()>::kTotal);
+                                 scan_smem<false>());
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_finish_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kFinishSmemMax);
@@ -905,7 +906,7 @@ extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int gri
     cudaLaunchConfig_t ca{};
     ca.gridDim = dim3(grid);
     ca.blockDim = dim3(32 * (with_links ? scan_warps<true>() : scan_warps<false>()));
-    ca.dynamicSmemBytes = with_links ? ScanSmem<scan_warps<true>()>::kTotal : ScanSmem<scan_warps<false>()>::kTotal;
+    ca.dynamicSmemBytes = with_links ? scan_smem<true>() : scan_smem<false>();
     ca.stream = stream;
     ca.attrs = attr;
     ca.numAttrs = 1;
