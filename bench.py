@@ -67,12 +67,18 @@ def hold_cycles(steps: int) -> int:
     return int(v) if v is not None else max(400_000, 20_000 * steps)
 
 
-def hold_stream(stream, steps: int) -> None:
+def hold_stream(stream, steps: int) -> bool:
+    """Enqueue the hold; False (no hold, the region then includes submission) if torch lacks _sleep."""
     n = hold_cycles(steps)
-    if n > 0:
-        import torch
-        with torch.cuda.stream(stream):
-            torch.cuda._sleep(n)
+    if n <= 0:
+        return False
+    import torch
+    sleep = getattr(torch.cuda, "_sleep", None)
+    if sleep is None:
+        return False
+    with torch.cuda.stream(stream):
+        sleep(n)
+    return True
 
 
 def measured_peak():
@@ -353,7 +359,7 @@ def run_ours(a):
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    hold_stream(stream, a.steps)
+    held = hold_stream(stream, a.steps)
     ev0.record(stream)
     if graph is not None:
         graph.replay()
@@ -497,7 +503,7 @@ def run_ours(a):
                          "peak_source": peak_src,
                          "timing": ("CUDA events around a K-step CUDA graph replay" if graph is not None
                                     else "CUDA events around K eager steps (graph capture with collectives failed)")
-                         + (f"; a {HOLD_NOTE}" if hold_cycles(a.steps) > 0 else "")},
+                         + (f"; a {HOLD_NOTE}" if held else "")},
             "eager_launch_ms": round(sorted(eager_ms)[len(eager_ms) // 2], 5),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "north_star_subset": alt,
             "gpu_launches": info.kernels_per_scan * a.steps,  # per timed graph (the subset graph: as many again)
