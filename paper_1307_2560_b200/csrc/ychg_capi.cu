@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -545,6 +547,11 @@ struct HostContext {
     unsigned long long* h_dscal = nullptr;  // pinned
     int* h_flag = nullptr;                  // pinned: jump-round change flag
     cudaEvent_t dec_ev[2] = {nullptr, nullptr};
+    // pageable host input: pinned staging ring (see h2d_staged)
+    static constexpr int kStageSlots = 3;
+    uint8_t* h_stage[kStageSlots] = {};
+    int64_t stage_bytes = 0;
+    cudaEvent_t stage_ev[kStageSlots] = {};
 };
 
 HostContext& host_context(int device) {
@@ -559,6 +566,7 @@ int ensure_context(HostContext& c) {
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
         for (auto& e : c.chunk_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : c.stage_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         const char* ht = getenv("YCHG_HOST_TIMING");
         c.h2d_timing = ht && ht[0] == '1';
         if (c.h2d_timing)
@@ -567,6 +575,115 @@ int ensure_context(HostContext& c) {
         CK(cudaMallocHost(&c.h_totals, sizeof(ychg_totals)));
         c.ready = true;
     }
+    return YCHG_OK;
+}
+
+// Parallel host memcpy for pageable inputs: the caller plus persistent workers
+// split each chunk.  One job at a time (callers of several devices serialise
+// here); the pool is never destroyed, so no worker outlives its condition
+// variables at process exit.
+class CopyPool {
+   public:
+    static CopyPool& get() {
+        static CopyPool* pool = new CopyPool();
+        return *pool;
+    }
+    void copy(uint8_t* dst, const uint8_t* src, size_t n) {
+        const int parts = static_cast<int>(workers_.size()) + 1;
+        if (parts == 1 || n < (size_t(1) << 18)) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = dst;
+            src_ = src;
+            n_ = n;
+            parts_ = parts;
+            pending_ = parts - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+   private:
+    CopyPool() {
+        // 3-4 copiers saturate a B200 host's memory copy rate (scripts/stage_sweep.sh)
+        int t = std::min(4, static_cast<int>(std::thread::hardware_concurrency()));
+        if (const char* v = getenv("YCHG_COPY_THREADS"); v && *v) t = atoi(v);
+        t = std::max(1, std::min(t, 16));
+        for (int i = 1; i < t; ++i) {
+            workers_.emplace_back([this, i] { loop(i); });
+            workers_.back().detach();
+        }
+    }
+    void part(int i) {
+        // 4 KB-aligned slices
+        const size_t per = ((n_ + parts_ - 1) / parts_ + 4095) & ~size_t(4095);
+        const size_t b = std::min(n_, per * i), e = std::min(n_, b + per);
+        if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
+    }
+    void loop(int i) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return gen_ != seen; });
+                seen = gen_;
+            }
+            part(i);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    int pending_ = 0, parts_ = 1;
+    uint8_t* dst_ = nullptr;
+    const uint8_t* src_ = nullptr;
+    size_t n_ = 0;
+};
+
+// H2D of `bytes` bytes of PAGEABLE host memory into d_dst, ending on c.stream:
+// chunks go through a ring of pinned slots, each filled by the copy pool while
+// the DMA of the previous one runs on c.copy_stream (the driver's own staging of
+// pageable copies reaches ~19 GB/s; this pipeline runs at the DMA rate).
+int h2d_staged(HostContext& c, uint8_t* d_dst, const uint8_t* src, int64_t bytes) {
+    static const int64_t chunk = [] {
+        const char* v = getenv("YCHG_STAGE_MB");  // experiment hook
+        const int64_t mb = v && *v ? atoll(v) : 4;
+        return std::max<int64_t>(1, mb) << 20;
+    }();
+    if (c.stage_bytes < chunk) {
+        for (auto& p : c.h_stage) {
+            cudaFreeHost(p);
+            p = nullptr;
+        }
+        c.stage_bytes = 0;
+        for (auto& p : c.h_stage) CK(cudaMallocHost(&p, chunk));
+        c.stage_bytes = chunk;
+    }
+    // the copy stream must not overwrite device memory still read by earlier work on c.stream
+    CK(cudaEventRecord(c.chunk_ev[0], c.stream));
+    CK(cudaStreamWaitEvent(c.copy_stream, c.chunk_ev[0], 0));
+    CopyPool& pool = CopyPool::get();
+    int64_t i = 0;
+    for (int64_t off = 0; off < bytes; off += chunk, ++i) {
+        const int slot = static_cast<int>(i % HostContext::kStageSlots);
+        if (i >= HostContext::kStageSlots) CK(cudaEventSynchronize(c.stage_ev[slot]));  // slot's DMA done
+        const int64_t len = std::min(chunk, bytes - off);
+        pool.copy(c.h_stage[slot], src + off, static_cast<size_t>(len));
+        CK(cudaMemcpyAsync(d_dst + off, c.h_stage[slot], len, cudaMemcpyHostToDevice, c.copy_stream));
+        CK(cudaEventRecord(c.stage_ev[slot], c.copy_stream));
+    }
+    CK(cudaEventRecord(c.chunk_ev[1], c.copy_stream));
+    CK(cudaStreamWaitEvent(c.stream, c.chunk_ev[1], 0));
     return YCHG_OK;
 }
 
@@ -628,9 +745,12 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
         c.bits_cap = need;
     }
 
-    (void)is_pinned;
+    // pageable rows (e.g. the reference BinaryImage's std::vector) go through the
+    // pinned staging pipeline; strided pageable rows are left to the driver
+    const bool pinned = is_pinned(bits);
     if (row_stride == pitch) {
-        CK(cudaMemcpyAsync(c.d_bits, bits, pitch * height, cudaMemcpyHostToDevice, c.stream));
+        if (pinned) CK(cudaMemcpyAsync(c.d_bits, bits, pitch * height, cudaMemcpyHostToDevice, c.stream));
+        else if (const int rc = h2d_staged(c, c.d_bits, bits, pitch * height)) return rc;
     } else if (row_stride != row_bytes) {
         CK(cudaMemcpy2DAsync(c.d_bits, pitch, bits, row_stride, row_bytes, height, cudaMemcpyHostToDevice,
                              c.stream));
@@ -642,6 +762,15 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
             c.dense_cap = 0;
             CK(cudaMalloc(&c.d_dense, dense + 32));
             c.dense_cap = dense + 32;
+        }
+        if (!pinned) {
+            if (c.h2d_timing) cudaEventRecord(c.h2d_ev[0], c.stream);
+            if (const int rc = h2d_staged(c, c.d_dense, bits, dense)) return rc;
+            if (c.h2d_timing) cudaEventRecord(c.h2d_ev[1], c.stream);
+            const int rc = ychg_launch_repitch(c.d_dense, row_bytes, c.d_bits, pitch, 0, height, c.stream);
+            if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "repitch kernel launch");
+            if (c.h2d_timing) cudaEventRecord(c.h2d_ev[2], c.stream);
+            return YCHG_OK;
         }
         CK(cudaEventRecord(c.chunk_ev[0], c.stream));  // order after earlier work on c.stream
         CK(cudaStreamWaitEvent(c.copy_stream, c.chunk_ev[0], 0));
