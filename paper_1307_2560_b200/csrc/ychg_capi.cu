@@ -725,6 +725,15 @@ bool is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
+// H2D into context memory on c.stream: pinned sources by DMA, pageable ones via h2d_staged.
+int h2d_any(HostContext& c, uint8_t* d_dst, const uint8_t* src, int64_t bytes) {
+    if (is_pinned(src)) {
+        CK(cudaMemcpyAsync(d_dst, src, bytes, cudaMemcpyHostToDevice, c.stream));
+        return YCHG_OK;
+    }
+    return h2d_staged(c, d_dst, src, bytes);
+}
+
 }  // namespace
 
 // H2D of the caller's rows into the context's pitched device image.  Row strides
@@ -1452,7 +1461,7 @@ extern "C" int ychg_load_pnm(const uint8_t* bytes, int64_t n, int32_t threshold,
     const int64_t ns = int64_t(hd.width) * hd.height;
     if (const int rc = ensure_dev(&c.d_dense, &c.dense_cap, ns)) return rc;
     if (const int rc = ensure_dev(&c.d_bits, &c.bits_cap, rb * hd.height)) return rc;
-    CK(cudaMemcpyAsync(c.d_dense, bytes + hd.raster, ns, cudaMemcpyHostToDevice, c.stream));
+    if (const int rc = h2d_any(c, c.d_dense, bytes + hd.raster, ns)) return rc;
     const int rc = ychg_launch_pack_p5(c.d_dense, hd.width, hd.height, threshold, c.d_bits, rb, c.stream);
     if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "P5 pack kernel");
     CK(cudaMemcpy2DAsync(bits_out, row_stride, c.d_bits, rb, rb, hd.height, cudaMemcpyDeviceToHost, c.stream));
@@ -1526,8 +1535,7 @@ extern "C" int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold,
                                 const int64_t pitch = (rb + 15) / 16 * 16;
                                 if (const int rc = ensure_dev(&c.d_dense, &c.dense_cap, ns)) return rc;
                                 if (const int rc = ensure_dev(&c.d_bits, &c.bits_cap, pitch * hd.height)) return rc;
-                                CK(cudaMemcpyAsync(c.d_dense, bytes + hd.raster, ns, cudaMemcpyHostToDevice,
-                                                   c.stream));
+                                if (const int rc = h2d_any(c, c.d_dense, bytes + hd.raster, ns)) return rc;
                                 const int rc = ychg_launch_pack_p5(c.d_dense, hd.width, hd.height, threshold,
                                                                    c.d_bits, pitch, c.stream);
                                 return rc ? cuda_fail(static_cast<cudaError_t>(rc), "P5 pack kernel") : YCHG_OK;
