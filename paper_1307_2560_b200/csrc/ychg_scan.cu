@@ -44,6 +44,7 @@ struct LaneState {
     uint32_t ones, twos, fours, eights, u16, u32, u64, u128;
     uint32_t acc[16];          // u16x2 per-column totals (see acc_column)
     uint32_t pa, pb;           // previous row: column c and column c+1 bits
+    uint32_t pab;              // pa & pb (K3)
     uint32_t mk3;              // valid column pairs of this word
     // K3
     uint32_t G2, G3;           // open component holds >= 2 / >= 3 runs
@@ -67,27 +68,31 @@ __device__ __forceinline__ void flush_counts(LaneState& s) {
 // row iff (a & pa) | (b & pb).  A new run can only join an open component on a
 // row where both columns are set and exactly one of them was set above:
 // f = a & b & (pa ^ pb).  N >= 2 <=> ab | (cont & G2); N >= 3 <=> (cont & G3) | (G2 & f).
+// G2 implies pa | pb and contains pab (= pa & pb, the previous row's ab), so
+// G2 & f == ab & G2 & ~pab: one LOP3, and f itself is never formed (7 LOP3/row).
 // A component that closes with exactly two runs is a decompose() link
 // (hypergraph.cpp:137-143).  Head pairs (open across the band's top edge) start
 // "poisoned" at N >= 3 so their unknown-prefix component never counts here;
-// kHead additionally tracks their new runs (h1, h2) until they close.
+// kHead additionally tracks their new runs (h1, h2) until they close (Hd <= G2,
+// so Hd & f == Hd & ab & ~pab likewise).
 template <bool kHead>
 __device__ __forceinline__ uint32_t k3_step(uint32_t a, uint32_t b, LaneState& s) {
     const uint32_t ab = a & b;
-    const uint32_t f = lop3<0x60>(ab, s.pa, s.pb);            // ab & (pa ^ pb)
     const uint32_t cont = lop3<0xF8>(a & s.pa, b, s.pb);       // (a & pa) | (b & pb)
     const uint32_t lk = lop3<0x04>(cont, s.G2, s.G3);          // ~cont & G2 & ~G3
     if (kHead) {
         s.Hd &= cont;
-        const uint32_t t = s.Hd & f;
+        const uint32_t t = lop3<0x40>(s.Hd, ab, s.pab);        // Hd & ab & ~pab
         s.h2 = lop3<0xF8>(s.h2, s.h1, t);                      // h2 | (h1 & t)
         s.h1 |= t;
     }
-    const uint32_t g3 = lop3<0xEA>(cont, s.G3, s.G2 & f);     // (cont & G3) | (G2 & f)
+    const uint32_t g2f = lop3<0x40>(ab, s.G2, s.pab);          // ab & G2 & ~pab == G2 & f
+    const uint32_t g3 = lop3<0xF8>(g2f, cont, s.G3);           // (cont & G3) | (G2 & f)
     s.G2 = lop3<0xF8>(ab, cont, s.G2);                         // ab | (cont & G2)
     s.G3 = g3;
     s.pa = a;
     s.pb = b;
+    s.pab = ab;
     return lk;
 }
 
@@ -667,7 +672,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         const bool full = !kLinks || __all_sync(0xFFFFFFFFu, s.mk3 == 0xFFFFFFFFu);
         s.h1 = s.h2 = 0;
         s.links = 0;
-        s.pa = s.pb = 0;
+        s.pa = s.pb = s.pab = 0;
         uint32_t O = 0;
 
         if (nb > 0) {
@@ -697,6 +702,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             O = kLinks ? (s.pa | s.pb) : 0u;
             s.Hd = O;
             s.G2 = s.G3 = O;  // poisoned: the head's own closing is never a local link
+            s.pab = s.pa & s.pb;
 
             int since_flush = 0;
             for (int bi = 0; bi < nb; ++bi) {

@@ -74,6 +74,7 @@ def band(a_rows, b_rows, halo_a, halo_b, mk3, block_rows):
     O = pa | pb
     Hd = O
     G2 = G3 = O
+    pab = pa & pb
     h1 = h2 = 0
     links = 0
     for start in range(0, len(a_rows), block_rows):
@@ -81,18 +82,21 @@ def band(a_rows, b_rows, halo_a, halo_b, mk3, block_rows):
         lks = []
         for a, b in zip(a_rows[start:start + block_rows], b_rows[start:start + block_rows]):
             ab = a & b
-            f = ab & (pa ^ pb)
             cont = (a & pa) | (b & pb)
             lk = n(cont) & G2 & n(G3)
+            # G2 & f == ab & G2 & ~pab: G2 implies pa | pb, and f = ab & (pa ^ pb)
+            assert G2 & ~(pa | pb) == 0 and pab & ~G2 == 0
             if head:
                 Hd &= cont
-                t = Hd & f
+                t = Hd & ab & n(pab)  # Hd <= G2
+                assert t == Hd & ab & (pa ^ pb)
                 h2 |= h1 & t
                 h1 |= t
-            g3 = (cont & G3) | (G2 & f)
+            g3 = (cont & G3) | (ab & G2 & n(pab))
+            assert g3 == (cont & G3) | (G2 & ab & (pa ^ pb))
             G2 = ab | (cont & G2)
             G3 = g3
-            pa, pb = a, b
+            pa, pb, pab = a, b, ab
             lks.append(lk)
         links += sum(popc(x & mk3) for x in lks)
     m = mk3
