@@ -1,4 +1,4 @@
-"""Summarise an ncu capture of ychg_scan_kernel into profiles/ (json + markdown)."""
+"""Summarise an ncu capture of one kernel (ychg_scan_kernel, ychg_finish_kernel, ...) into profiles/ (json + markdown)."""
 import csv, io, json, os, subprocess, sys
 
 rep = sys.argv[1]
@@ -31,7 +31,7 @@ rd = f("dram__bytes_read.sum"); wr = f("dram__bytes_write.sum")
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 rd_b = rd * scale.get(u.get("dram__bytes_read.sum"), 1) if rd is not None else None
 wr_b = wr * scale.get(u.get("dram__bytes_write.sum"), 1) if wr is not None else None
-res = {"kernel": "ychg_scan_kernel<true>", "report": os.path.basename(rep), "metrics": summ, "stalls_per_issue": stalls,
+res = {"kernel": (d.get("Kernel Name") or "?").split("(")[0], "report": os.path.basename(rep), "metrics": summ, "stalls_per_issue": stalls,
        "dram_bytes_per_launch": (rd_b + wr_b) if rd_b is not None and wr_b is not None else None,
        "note": "one ncu --set full replay of one launch (cold-cache, serialised): shares, not absolutes"}
 with open(out_prefix + ".json", "w") as fh:
