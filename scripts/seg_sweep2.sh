@@ -1,5 +1,5 @@
 # segments-per-strip sweep at 21000^2, K=100 steady state (full path and K1+K2 subset)
-for k in 2 3 4 2 3 4; do
+for k in ${KS:-2 3 4 2 3 4}; do
   r=$(YCHG_SEGMENTS=$k timeout 120 python bench.py --no-cpu-baseline --no-e2e 2>&1 | tail -1)
   python - "$k" "$r" <<'PY'
 import json, sys
