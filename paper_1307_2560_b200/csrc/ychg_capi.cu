@@ -535,8 +535,12 @@ struct HostContext {
     int64_t runs_cap = 0;
     int32_t* h_out = nullptr;         // pinned staging: counts | boundaries (capacity cols_cap each)
     char* d_block = nullptr;          // device [totals | counts | boundaries] (ensure_columns)
-    char* h_block = nullptr;          // pinned mirror of d_block
-    int64_t h_block_cap = 0;
+    // host scan outputs [totals (64 B) | counts (cols_cap) | boundaries (cols_cap)] in
+    // MAPPED pinned memory: the finisher's stores cross PCIe as it runs, so the
+    // host path needs no separate D2H copy after the scan (one fewer round trip)
+    char* m_block = nullptr;
+    char* m_block_dev = nullptr;
+    int64_t m_block_cap = 0;
     bool h2d_timing = false;
     cudaEvent_t h2d_ev[3] = {nullptr, nullptr, nullptr};
     int64_t h_out_cap = 0;
@@ -852,26 +856,28 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
         for (auto& e : tev) cudaEventCreate(&e);
         cudaEventRecord(tev[0], c.stream);
     }
+    // Outputs land in mapped pinned memory (see HostContext::m_block).
     // d_counts_dst: the counts go straight to another buffer -- possibly on a peer
     // GPU, so the finisher's stores are the gather (ychg_scan_host_sharded)
-    if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, d_counts_dst ? d_counts_dst : c.d_counts,
-                                        c.d_flags, c.d_bounds, c.d_totals, c.stream))
-        return rc;
-    if (host_timing) cudaEventRecord(tev[1], c.stream);
-    // D2H in one round trip: totals + counts + the whole boundary buffer into pinned
-    // staging (W ints cost microseconds; a second synchronisation costs more), then
-    // host copies of exactly what the caller asked for.
-    const int64_t blk = 64 + c.cols_cap * 4 + (boundaries_out ? int64_t(width) * 4 : 0);
-    if (c.h_block_cap < 64 + 8 * c.cols_cap) {
-        cudaFreeHost(c.h_block);
-        c.h_block = nullptr;
-        c.h_block_cap = 0;
-        CK(cudaMallocHost(&c.h_block, 64 + 8 * c.cols_cap));
-        c.h_block_cap = 64 + 8 * c.cols_cap;
+    if (c.m_block_cap < 64 + 8 * c.cols_cap) {
+        cudaFreeHost(c.m_block);
+        c.m_block = c.m_block_dev = nullptr;
+        c.m_block_cap = 0;
+        CK(cudaHostAlloc(&c.m_block, 64 + 8 * c.cols_cap, cudaHostAllocMapped | cudaHostAllocPortable));
+        void* dp = nullptr;
+        CK(cudaHostGetDevicePointer(&dp, c.m_block, 0));
+        c.m_block_dev = static_cast<char*>(dp);
+        c.m_block_cap = 64 + 8 * c.cols_cap;
     }
-    CK(cudaMemcpyAsync(c.h_block, c.d_block, counts_out || boundaries_out ? blk : 64, cudaMemcpyDeviceToHost,
-                       c.stream));
-    if (host_timing) cudaEventRecord(tev[2], c.stream);
+    int32_t* m_counts = reinterpret_cast<int32_t*>(c.m_block_dev + 64);
+    if (const int rc = ychg_scan_device(c.plan, c.d_bits, pitch, with_hyperedges, d_counts_dst ? d_counts_dst : m_counts,
+                                        c.d_flags, m_counts + c.cols_cap,
+                                        reinterpret_cast<ychg_totals*>(c.m_block_dev), c.stream))
+        return rc;
+    if (host_timing) {
+        cudaEventRecord(tev[1], c.stream);
+        cudaEventRecord(tev[2], c.stream);  // no D2H step: the outputs are already in host memory
+    }
     CK(cudaStreamSynchronize(c.stream));
     if (host_timing) {
         float a = 0, b = 0;
@@ -884,8 +890,9 @@ int scan_host_locked(HostContext& c, int device, int32_t width, int32_t height, 
                      h1 * 1e3, h2 * 1e3, a * 1e3, b * 1e3);
         for (auto& e : tev) cudaEventDestroy(e);
     }
-    const ychg_totals t = *reinterpret_cast<const ychg_totals*>(c.h_block);
-    const int32_t* h_counts = reinterpret_cast<const int32_t*>(c.h_block + 64);
+    ychg_totals t;
+    std::memcpy(&t, c.m_block, sizeof(t));
+    const int32_t* h_counts = reinterpret_cast<const int32_t*>(c.m_block + 64);
     if (counts_out) std::memcpy(counts_out, h_counts, size_t(width) * 4);
     if (boundaries_out && t.n_boundaries > 0)
         std::memcpy(boundaries_out, h_counts + c.cols_cap, size_t(t.n_boundaries) * 4);
