@@ -794,9 +794,14 @@ int upload_image(HostContext& c, const uint8_t* bits, int32_t width, int32_t hei
             return n < 1 ? 1 : (n > HostContext::kChunks ? HostContext::kChunks : n);
         }();
         const int nch = height >= max_chunks * 64 ? max_chunks : 1;
-        // The last chunk is an eighth of the rows: only its re-pitch is exposed after
+        // The last chunk is a sixteenth of the rows: only its re-pitch is exposed after
         // the final copy; the earlier chunks' re-pitch hides under the later copies.
-        const int tail = nch > 1 ? height / 8 : 0;
+        static const int tail_div = [] {
+            const char* v = getenv("YCHG_H2D_TAIL_DIV");  // experiment hook: tail chunk = rows / div
+            const int d = v && *v ? atoi(v) : 16;  // 1/8 1.071, 1/16 1.068, 1/32 1.070 ms (21000^2)
+            return d < 2 ? 2 : d;
+        }();
+        const int tail = nch > 1 ? height / tail_div : 0;
         for (int i = 0; i < nch; ++i) {
             const int y0 = static_cast<int>((int64_t(height - tail) * i) / (nch - (nch > 1)));
             const int y1 = i == nch - 1 ? height : static_cast<int>((int64_t(height - tail) * (i + 1)) / (nch - 1));
