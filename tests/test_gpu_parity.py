@@ -553,3 +553,26 @@ def test_host_path_pageable_pinned_and_strided_inputs(gpu, orc, monkeypatch):
             assert np.array_equal(counts, want_c), arr.strides
             assert t.n_boundaries == want_b.size and np.array_equal(bounds[: t.n_boundaries], want_b)
             assert t.hyperedges == want_h
+
+
+def test_host_path_output_buffers_grow_and_shrink(gpu, orc):
+    """The host entry point's mapped output block is reallocated as images widen
+    (counts | boundaries | totals written by the finisher straight into host
+    memory): alternate narrow / wide / narrow images, counts-only and full path,
+    every result equal to the oracle (also after a shrink, with stale data from
+    the wider scan still in the block)."""
+    y = gpu
+    for k, (W, H, dens) in enumerate([(100, 37, 0.5), (40000, 64, 0.3), (1500, 900, 0.6), (70001, 33, 0.5),
+                                      (9, 5, 0.5), (2049, 2049, 0.45)]):
+        sp = Spec.random(W, H, dens, 99 + k)
+        bits = orc.synth(sp)
+        img = y.BinaryImage(W, H, bits)
+        want_c = orc.counts(bits, W)
+        want_b = orc.boundaries(want_c)
+        for links in (True, False):
+            r = y.scan(img, with_hyperedges=links)
+            assert np.array_equal(r.counts, want_c), (W, H, links)
+            assert np.array_equal(r.boundaries, want_b), (W, H, links)
+            if links:
+                assert r.hyperedges == orc.hyperedges(bits, W)[0], (W, H)
+        assert np.array_equal(y.cut_vertex_counts(img), want_c)
