@@ -20,7 +20,7 @@ for pat, arg, cpu in (("hbands", ["--bands", "147"], True), ("hbands", ["--bands
     runs.append(("hyperedges", ["--size", "21000", "--pattern", pat, *arg] + ([] if cpu else ["--no-cpu-baseline"])))
 rows = []
 for axis, args in runs:
-    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "20", "--warmup", "5",
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "100", "--warmup", "10",
                           "--cpu-reps", "3", *args], capture_output=True, text=True, timeout=900)
     line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else ""
     try:
@@ -39,7 +39,7 @@ with open(os.path.join(root, "gpurun_out", f"{tag}_sweeps.jsonl"), "w") as f:
     for d in rows:
         f.write(json.dumps(d) + "\n")
 with open(os.path.join(root, "gpurun_out", f"{tag}_sweeps.md"), "w") as f:
-    f.write("# BASELINE configs 3-4 on one B200 (bench.py per point; full path: counts+flags+boundaries+hyperedges)\n\n")
+    f.write("# BASELINE configs 3-4 on one B200 (bench.py per point, K=100-step graph; full path: counts+flags+boundaries+hyperedges)\n\n")
     f.write("| axis | workload | hyperedges | device us/step | Gpix/s | HBM frac | e2e Gpix/s (H2D incl.) | CPU ref Gpix/s (cores) | GPU/CPU e2e |\n")
     f.write("|---|---|---|---|---|---|---|---|---|\n")
     for d in rows:
