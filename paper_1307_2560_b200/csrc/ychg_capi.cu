@@ -990,7 +990,7 @@ int profile_phase0(HostContext& c, const uint8_t* bits, int32_t width, int32_t h
         c.col_off_cap = width;
     }
     const int rc = ychg_launch_profile(c.d_bits, pitch, width, height, c.d_band, c.d_counts, c.d_col_off,
-                                       &c.d_totals->total_runs, nullptr, 0, c.stream);
+                                       &c.d_totals->total_runs, nullptr, 0, 0, c.stream);
     if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "profile count kernels launch");
     CK(cudaMemcpyAsync(c.h_totals, c.d_totals, sizeof(ychg_totals), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
@@ -1008,7 +1008,7 @@ int profile_fill(HostContext& c, int32_t width, int32_t height, int64_t n_runs) 
     }
     const int64_t pitch = ((int64_t(width) + 7) / 8 + 15) / 16 * 16;
     const int rc = ychg_launch_profile(c.d_bits, pitch, width, height, c.d_band, c.d_counts, c.d_col_off, nullptr,
-                                       c.d_runs, 1, c.stream);
+                                       c.d_runs, 1, n_runs, c.stream);
     if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "profile fill kernel launch");
     return YCHG_OK;
 }

@@ -30,7 +30,7 @@ int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint8_t* d_dst,
 // column offsets (+ run total); phase 1 = fill the flat [n][3] int32 run array.
 int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t width, int32_t height, uint32_t* d_band_counts,
                         int32_t* d_counts, int64_t* d_col_off, int64_t* d_n_runs, int32_t* d_runs, int phase,
-                        cudaStream_t stream);
+                        int64_t n_runs_hint, cudaStream_t stream);
 int64_t ychg_profile_band_words(int32_t width, int32_t height);
 
 // Hyperedge decomposition (ychg_decompose.cu).

@@ -9,16 +9,21 @@
 //                             the band's first run in the column's list) and the
 //                             column total; then the exclusive prefix over columns
 //                             (= offset of the column's list in the flat array).
-//   P3 profile_fill_kernel    re-streams each band, one lane per column: a rise
+//   P3 fill                   re-streams each band, one lane per column: a rise
 //                             at row y opens run {c, y, ?} at the column's next
 //                             index, a fall at row y closes it with y_bot = y-1 (one
 //                             12-byte record); a virtual background row H closes
-//                             what is open at the bottom.
+//                             what is open at the bottom.  Three kernels, chosen by
+//                             run density (ychg_launch_profile): a transposed
+//                             fall walk (sparse), row stepping (mid), the walk with
+//                             a staged coalesced write-out (dense).
 // The flat output is column-major and sorted by y_top inside a column -- exactly
 // ColumnProfile::runs flattened (runscan.hpp:40-50).
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "ychg_device.cuh"
 #include "ychg_kernels.h"
@@ -149,6 +154,7 @@ __global__ void profile_offsets_kernel(int32_t n, const int32_t* __restrict__ co
     if (tid == 0) *n_runs = carry;
 }
 
+// P3 (mid density): one warp per (band, word), lanes step the rows together.
 // P3: fill.  One warp per (band, word); lane j owns column c = 32w + j and walks
 // the band's rows (one broadcast word load per row), so each lane appends to ONE
 // contiguous output stream -- its column's list -- and writes every run it
@@ -158,7 +164,7 @@ __global__ void profile_offsets_kernel(int32_t n, const int32_t* __restrict__ co
 // the band's top was started by an earlier band (index base-1): only its y_bot
 // is written here; a run still open at the bottom gets {c, y_top} here and its
 // y_bot from a later band (or the virtual background row H in the last band).
-__global__ void __launch_bounds__(256) profile_fill_kernel(const ProfileArgs a, const uint32_t* __restrict__ band_base,
+__global__ void __launch_bounds__(256) profile_fill_rowwise_kernel(const ProfileArgs a, const uint32_t* __restrict__ band_base,
                                                            const int64_t* __restrict__ col_off,
                                                            int32_t* __restrict__ runs /* [n][3] */) {
     const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -205,11 +211,145 @@ __global__ void __launch_bounds__(256) profile_fill_kernel(const ProfileArgs a, 
     }
 }
 
+
+// 32x32 bit transpose across a warp: on entry bit b of lane k's x is M[k][b];
+// on exit bit k of lane j's x is M[k][j].  Five shuffle stages swap the
+// off-diagonal blocks of size s (Hacker's Delight's block transpose, one lane
+// per row).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int sh = 16 >> i;
+        const uint32_t m = masks[i];
+        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, x, sh);
+        x = (lane & sh) ? ((x & ~m) | ((o & ~m) >> sh)) : ((x & m) | ((o & m) << sh));
+    }
+    return x;
+}
+
+// P3: fill.  One warp per (band, word).  Per 32-row chunk, lane k loads row k's
+// raw little-endian word (one load per lane instead of 32 broadcast loads per
+// warp) and a warp bit transpose hands lane j the 32-row bit sequence of the
+// column at raw bit j: c = 32w + 8(j/8) + 7 - j%8 (MSB-first bytes,
+// image.hpp:17-72).  Rises (s & ~(s<<1 | prev)) and falls are then walked with
+// ffs, in row order: work per lane is proportional to its runs, not its rows.
+// Every run that closes inside the chunk is a complete 12-byte record {c, y_top,
+// y_bot}; a lane's records of one chunk are consecutive entries of its column's
+// list, so they are staged in shared memory (<= 16 per lane per chunk) and the
+// warp then writes each lane's segment with coalesced stores -- full sectors
+// instead of 32 partial 4-byte stores per instruction.  The two boundary cases
+// are written directly (once per lane and band at most): a run open at the
+// band's top was started by an earlier band (index base-1) and only its y_bot is
+// written here; a run still open at the bottom gets {c, y_top} here and its y_bot
+// from a later band (or the virtual background row H in the last band).
+template <bool kStaged>
+__host__ __device__ constexpr int fill_warps_per_cta() { return kStaged ? 4 : 8; }
+constexpr int kLaneSlot = 3 * 16 + 1;  // 16 records per lane and chunk; odd stride: no bank conflicts
+
+template <bool kStaged>
+__global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fill_kernel(const ProfileArgs a,
+                                                                       const uint32_t* __restrict__ band_base,
+                                                                       const int64_t* __restrict__ col_off,
+                                                                       int32_t* __restrict__ runs /* [n][3] */) {
+    constexpr int kFillWarps = fill_warps_per_cta<kStaged>();
+    __shared__ int32_t stage[kStaged ? kFillWarps : 1][kStaged ? 32 * kLaneSlot : 1];
+    const int wib = threadIdx.x >> 5;
+    const int gw = blockIdx.x * kFillWarps + wib;
+    const int lane = threadIdx.x & 31;
+    if (gw >= a.n_words * a.n_bands) return;
+    const int w = gw / a.n_bands, band = gw - w * a.n_bands;  // consecutive warps: bands of one word
+    const int c = 32 * w + 8 * (lane >> 3) + 7 - (lane & 7);
+    const bool live = c < a.width;
+    const int y0 = band * kBandRows;
+    const int y1 = min(a.height, y0 + kBandRows);
+    const uint8_t* col = a.bits + 4 * static_cast<int64_t>(w);
+    // The whole band's rows are loaded up front: 8 independent loads per lane.
+    constexpr int kChunks = kBandRows / 32;
+    uint32_t raw[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        const int y = y0 + 32 * q + lane;
+        raw[q] = y < y1 ? __ldg(reinterpret_cast<const uint32_t*>(col + static_cast<int64_t>(y) * a.pitch)) : 0u;
+    }
+    uint32_t prev = y0 > 0 ? (__ldg(reinterpret_cast<const uint32_t*>(col + static_cast<int64_t>(y0 - 1) * a.pitch)) >> lane) & 1u
+                           : 0u;
+    int64_t idx = live ? col_off[c] + band_base[static_cast<int64_t>(band) * a.n_words * 32 + c] : 0;
+    int top = -1;  // y_top of a run opened in this band and still open
+    int32_t* mine = kStaged ? &stage[wib][lane * kLaneSlot] : nullptr;
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        const int yb = y0 + 32 * q;
+        if (yb >= y1) break;  // warp-uniform
+        const uint32_t s = warp_transpose32(raw[q], lane);  // bit k = row yb + k
+        const int nk = min(32, y1 - yb);
+        const uint32_t valid = nk == 32 ? 0xFFFFFFFFu : (1u << nk) - 1u;
+        const uint32_t above = (s << 1) | prev;  // bit k = row yb + k - 1
+        const uint32_t rises = s & ~above;
+        prev = (s >> (nk - 1)) & 1u;
+        // One iteration per run that closes in this chunk (a fall at row k): its
+        // y_top is the last rise below k, or the carried `top`.  Uniform body,
+        // half the iterations of an event walk.
+        uint32_t falls = live ? (above & ~s) & valid : 0u;
+        uint32_t rs = live ? rises & valid : 0u;
+        int n = 0;  // records of this lane in this chunk
+        while (falls) {
+            const int k = __ffs(falls) - 1;
+            falls &= falls - 1;
+            const uint32_t below = (1u << k) - 1u;
+            const uint32_t r = rs & below;
+            rs &= ~below;
+            const int t = r ? yb + 31 - __clz(r) : top;
+            top = -1;
+            if (t >= 0) {
+                int32_t* rec = kStaged ? mine + 3 * n : runs + 3 * (idx + n);
+                rec[0] = c;
+                rec[1] = t;
+                rec[2] = yb + k - 1;
+                ++n;
+            } else {
+                runs[3 * (idx - 1) + 2] = yb + k - 1;  // opened in an earlier band
+            }
+        }
+        if (rs) top = yb + 31 - __clz(rs);  // a run left open (at most one rise after the last fall)
+        if (kStaged) {
+        __syncwarp();
+        // Coalesced write-out: lane l's n_l records go to runs[3*idx_l ...].
+        uint32_t pending = __ballot_sync(0xFFFFFFFFu, n > 0);
+        while (pending) {
+            const int l = __ffs(pending) - 1;
+            pending &= pending - 1;
+            const int nl = __shfl_sync(0xFFFFFFFFu, n, l);
+            const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
+            const int32_t* src = &stage[wib][l * kLaneSlot];
+            int32_t* dst = runs + 3 * base;
+            for (int t = lane; t < 3 * nl; t += 32) dst[t] = src[t];
+        }
+        __syncwarp();
+        }
+        idx += n;
+    }
+    if (!live) return;
+    if (band == a.n_bands - 1 && prev) {  // the virtual background row H closes what is open
+        if (top >= 0) {
+            runs[3 * idx + 0] = c;
+            runs[3 * idx + 1] = top;
+            runs[3 * idx + 2] = a.height - 1;
+        } else {
+            runs[3 * (idx - 1) + 2] = a.height - 1;
+        }
+    } else if (top >= 0) {  // still open: a later band writes y_bot
+        runs[3 * idx + 0] = c;
+        runs[3 * idx + 1] = top;
+    }
+}
+
 }  // namespace
 
 extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t width, int32_t height,
                                    uint32_t* d_band_counts, int32_t* d_counts, int64_t* d_col_off,
-                                   int64_t* d_n_runs, int32_t* d_runs, int phase, cudaStream_t stream) {
+                                   int64_t* d_n_runs, int32_t* d_runs, int phase, int64_t n_runs_hint,
+                                   cudaStream_t stream) {
     ProfileArgs a{};
     a.bits = d_bits;
     a.pitch = pitch;
@@ -227,8 +367,31 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
         profile_colscan_kernel<<<(width + 255) / 256, 256, 0, stream>>>(a, d_band_counts, d_counts);
         profile_offsets_kernel<<<1, 1024, 0, stream>>>(width, d_counts, d_col_off, d_n_runs);
     } else {  // fill
-        profile_fill_kernel<<<static_cast<unsigned>((fill_warps + 7) / 8), 256, 0, stream>>>(a, d_band_counts,
-                                                                                           d_col_off, d_runs);
+        // Fill kernel by run density rho = runs per pixel, known from the count
+        // pass (measured on 21000^2, profiles/r01_fill_variants.md): the
+        // transposed walk wins on sparse masks (hbands rho 0.007: 96 vs 544 us), the
+        // row-stepping kernel on mid densities (checker(7) rho 0.071: 608 vs 779 /
+        // 957 us) and the staged coalesced write-out on dense ones (random rho
+        // 0.25: 1144 vs 2344 us).  YCHG_FILL_KERNEL=direct|rowwise|staged forces one.
+        const double rho = static_cast<double>(n_runs_hint) / (static_cast<double>(width) * height);
+        int kind = rho < 0.02 ? 0 : (rho < 0.13 ? 1 : 2);
+        if (const char* f = std::getenv("YCHG_FILL_KERNEL")) {
+            if (!std::strcmp(f, "direct")) kind = 0;
+            else if (!std::strcmp(f, "rowwise")) kind = 1;
+            else if (!std::strcmp(f, "staged")) kind = 2;
+        }
+        if (kind == 0) {
+            constexpr int wpc = fill_warps_per_cta<false>();
+            profile_fill_kernel<false><<<static_cast<unsigned>((fill_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
+                a, d_band_counts, d_col_off, d_runs);
+        } else if (kind == 1) {
+            profile_fill_rowwise_kernel<<<static_cast<unsigned>((fill_warps + 7) / 8), 256, 0, stream>>>(
+                a, d_band_counts, d_col_off, d_runs);
+        } else {
+            constexpr int wpc = fill_warps_per_cta<true>();
+            profile_fill_kernel<true><<<static_cast<unsigned>((fill_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
+                a, d_band_counts, d_col_off, d_runs);
+        }
     }
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);

@@ -294,6 +294,25 @@ def test_build_profile_invariants_and_large(gpu, orc):
             assert np.array_equal(y.column_runs(y.BinaryImage(sp.width, sp.height, bits), c), p.runs(c)), (sp, c)
 
 
+@pytest.mark.parametrize("kind", ["direct", "rowwise", "staged"])
+def test_build_profile_each_fill_kernel(gpu, orc, monkeypatch, kind):
+    """The three fill kernels (chosen by run density; YCHG_FILL_KERNEL forces one)
+    on the golden corpus and on band / width / height edges: 255/256/257 and
+    511/513 rows (partial bands and chunks), widths off the 32-column word and the
+    8-column byte, runs crossing bands, open at the last row, one-row masks."""
+    y = gpu
+    monkeypatch.setenv("YCHG_FILL_KERNEL", kind)
+    specs = [spec_of(row["spec"]) for row in corpus()]
+    specs += [Spec.random(1000, 257, 0.5, 5), Spec.random(37, 256, 0.7, 6), Spec.random(65, 255, 0.3, 7),
+              Spec.random(1031, 513, 0.95, 8), Spec.random(9, 511, 0.05, 9), Spec.hbands(100, 1000, 3),
+              Spec.checker(301, 700, 1), Spec.checker(64, 600, 300), Spec.random(257, 1, 0.5, 10),
+              Spec.random(3000, 2000, 0.5, 11)]
+    for sp in specs:
+        bits = orc.synth(sp)
+        p = y.build_profile(y.BinaryImage(sp.width, sp.height, bits))
+        assert np.array_equal(p.runs_flat, orc.profile(bits, sp.width)), (kind, sp)
+
+
 def test_reference_acceptance_on_gpu_library(gpu):
     """The reference's own acceptance suite (tests/acceptance.cpp), compiled from the
     reference sources and headers with libychg.so linked in place of runscan.cpp
