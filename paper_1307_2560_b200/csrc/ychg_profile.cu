@@ -314,16 +314,44 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
         if (rs) top = yb + 31 - __clz(rs);  // a run left open (at most one rise after the last fall)
         if (kStaged) {
         __syncwarp();
-        // Coalesced write-out: lane l's n_l records go to runs[3*idx_l ...].
-        uint32_t pending = __ballot_sync(0xFFFFFFFFu, n > 0);
-        while (pending) {
-            const int l = __ffs(pending) - 1;
-            pending &= pending - 1;
-            const int nl = __shfl_sync(0xFFFFFFFFu, n, l);
+        // Coalesced write-out of the chunk's records (T ints in total, warp-
+        // uniform).  T <= 512: one warp-wide segmented copy -- item t belongs to
+        // the last lane l whose exclusive offset is <= t (5 shuffles) and goes to
+        // runs[3*idx_l + t - off_l]; fewer, independent iterations win at mid
+        // densities.  Larger T: lane by lane, each segment one coalesced store
+        // per 32 ints (measured, profiles/r01_fill_variants.md).
+        const int m3 = 3 * n;
+        int inc = m3;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+        const int off = inc - m3;
+        if (total > 512) {
+            uint32_t pending = __ballot_sync(0xFFFFFFFFu, n > 0);
+            while (pending) {
+                const int l = __ffs(pending) - 1;
+                pending &= pending - 1;
+                const int ml = __shfl_sync(0xFFFFFFFFu, m3, l);
+                const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
+                const int32_t* src = &stage[wib][l * kLaneSlot];
+                int32_t* dst = runs + 3 * base;
+                for (int t = lane; t < ml; t += 32) dst[t] = src[t];
+            }
+        } else
+        for (int b0 = 0; b0 < total; b0 += 32) {
+            const int t = b0 + lane;
+            int l = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int e = __shfl_sync(0xFFFFFFFFu, off, l + step);
+                if (e <= t) l += step;
+            }
+            const int ol = __shfl_sync(0xFFFFFFFFu, off, l);
             const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
-            const int32_t* src = &stage[wib][l * kLaneSlot];
-            int32_t* dst = runs + 3 * base;
-            for (int t = lane; t < 3 * nl; t += 32) dst[t] = src[t];
+            if (t < total) runs[3 * base + (t - ol)] = stage[wib][l * kLaneSlot + (t - ol)];
         }
         __syncwarp();
         }
@@ -368,13 +396,13 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
         profile_offsets_kernel<<<1, 1024, 0, stream>>>(width, d_counts, d_col_off, d_n_runs);
     } else {  // fill
         // Fill kernel by run density rho = runs per pixel, known from the count
-        // pass (measured on 21000^2, profiles/r01_fill_variants.md): the
-        // transposed walk wins on sparse masks (hbands rho 0.007: 96 vs 544 us), the
-        // row-stepping kernel on mid densities (checker(7) rho 0.071: 608 vs 779 /
-        // 957 us) and the staged coalesced write-out on dense ones (random rho
-        // 0.25: 1144 vs 2344 us).  YCHG_FILL_KERNEL=direct|rowwise|staged forces one.
+        // pass (measured on 21000^2, profiles/r01_fill_variants.md): the direct
+        // transposed walk wins on sparse masks (hbands rho 0.007, checker(21)
+        // 0.024), the staged coalesced write-out on denser ones (checker(7) 0.071,
+        // random 0.25).  The row-stepping kernel is kept for A/B.
+        // YCHG_FILL_KERNEL=direct|rowwise|staged forces one.
         const double rho = static_cast<double>(n_runs_hint) / (static_cast<double>(width) * height);
-        int kind = rho < 0.02 ? 0 : (rho < 0.13 ? 1 : 2);
+        int kind = rho < 0.04 ? 0 : 2;
         if (const char* f = std::getenv("YCHG_FILL_KERNEL")) {
             if (!std::strcmp(f, "direct")) kind = 0;
             else if (!std::strcmp(f, "rowwise")) kind = 1;

@@ -11,7 +11,7 @@ import numpy as np  # noqa: E402
 import paper_1307_2560_b200 as y  # noqa: E402
 
 for pat, w, h, kw in [("checker", 21000, 21000, dict(cell=7)), ("random", 21000, 21000, dict(density=0.5, seed=1307)),
-                      ("hbands", 21000, 21000, dict(bands=147))]:
+                      ("hbands", 21000, 21000, dict(bands=147)), ("checker", 21000, 21000, dict(cell=21))]:
     img = y.synth(pat, w, h, **kw)
     prof = y.build_profile(img)
     runs = np.ascontiguousarray(prof.runs_flat)
