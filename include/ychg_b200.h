@@ -140,6 +140,13 @@ YCHG_API int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_t 
 YCHG_API int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
                                      int32_t strategy_kind, int32_t threads, int32_t* counts_out,
                                      int32_t* runs_out, int64_t runs_capacity, int64_t* n_runs_out);
+/* The same in ONE call (one upload, one count pass): after phase 0 the library
+ * calls alloc(alloc_ctx, n_runs) for a host buffer of 3*n_runs int32 (NULL ->
+ * YCHG_ERR_OOM) and fills it.  Not called when the image has no runs. */
+typedef void* (*ychg_alloc_fn)(void* alloc_ctx, int64_t n_runs);
+YCHG_API int ychg_build_profile_host_alloc(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                           int32_t strategy_kind, int32_t threads, int32_t* counts_out,
+                                           ychg_alloc_fn alloc, void* alloc_ctx, int64_t* n_runs_out);
 /* Runs of one column (runscan.cpp:104-120); YCHG_ERR_INVALID if col is out of range. */
 YCHG_API int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
                                    int32_t col, int32_t* runs_out, int64_t runs_capacity, int64_t* n_out);
@@ -190,9 +197,9 @@ YCHG_API int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, i
  * (multi-GPU column strips).  A plan is not safe for concurrent use. */
 YCHG_API int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t height,
                      ychg_plan** out);
-/* Plan flags: YCHG_PLAN_LATENCY sizes the launch for one isolated scan (all SMs
- * busy) instead of back-to-back pipelined scans (the default: fewer, longer CTAs
- * for large masks so consecutive scans overlap). */
+/* Plan flags.  YCHG_PLAN_LATENCY is accepted for compatibility and has no
+ * effect: every plan sizes one scan to fill all resident CTA slots of the GPU,
+ * which serves isolated and back-to-back scans alike. */
 #define YCHG_PLAN_LATENCY 1
 /* YCHG_PLAN_SYNC_INPUTS: the streaming kernel waits (griddepcontrol.wait) for the
  * kernel launched just before it on the stream to complete and flush before it
@@ -202,6 +209,11 @@ YCHG_API int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, 
  * stream, or any earlier kernel -- as in back-to-back scans of resident images).
  * Set it when a kernel of yours writes d_bits right before ychg_scan_device. */
 #define YCHG_PLAN_SYNC_INPUTS 2
+/* YCHG_PLAN_NO_SKIP: always run the full per-row step.  By default a 32-row block
+ * whose rows all equal the row above (every word of the warp's 1024 columns, plus
+ * the right-halo bit) is skipped: it changes no count, flag or K3 state.  The
+ * results are identical either way; the flag exists for A/B timing. */
+#define YCHG_PLAN_NO_SKIP 4
 YCHG_API int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_t height, int32_t flags,
                                  ychg_plan** out);
 YCHG_API void ychg_plan_destroy(ychg_plan* plan);

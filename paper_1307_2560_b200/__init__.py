@@ -67,6 +67,8 @@ _SIGS = {
                                               ctypes.POINTER(Totals)]),
     "ychg_build_profile_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _i64, ctypes.POINTER(_i64)]),
     "ychg_column_runs_host": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _i64, ctypes.POINTER(_i64)]),
+    "ychg_build_profile_host_alloc": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, _vp, _vp, _vp,
+                                                     ctypes.POINTER(_i64)]),
     "ychg_decompose_image": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _i32, ctypes.POINTER(_vp)]),
     "ychg_decompose_profile": (ctypes.c_int, [_i32, _i32, _vp, _vp, _i64, ctypes.POINTER(_vp)]),
     "ychg_hypergraph_info": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
@@ -328,28 +330,38 @@ class ColumnProfile:
         return int(self.counts.sum())
 
 
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64)
+
+
 def build_profile(image: BinaryImage, strategy: ScanStrategy = ScanStrategy.serial()) -> ColumnProfile:
-    """build_profile (runscan.cpp:130-143) on the GPU: count -> scan -> fill."""
+    """build_profile (runscan.cpp:130-143) on the GPU: count -> scan -> fill, in ONE
+    library call (the run buffer is requested once the total is known)."""
     counts = np.zeros(max(image.width, 1), dtype=np.int32)
     n = _i64(0)
-    _check(_lib.ychg_build_profile_host(image._ptr(), image.width, image.height, image.row_stride, strategy.kind,
-                                        strategy.threads, counts.ctypes.data_as(_vp), None, 0, ctypes.byref(n)),
-           "build_profile")
-    runs = np.zeros((max(n.value, 1), 3), dtype=np.int32)
-    if n.value > 0:
-        _check(_lib.ychg_build_profile_host(image._ptr(), image.width, image.height, image.row_stride,
-                                            strategy.kind, strategy.threads, counts.ctypes.data_as(_vp),
-                                            runs.ctypes.data_as(_vp), n.value, ctypes.byref(n)), "build_profile")
-    return ColumnProfile(image.width, image.height, counts[: image.width].copy(), runs[: n.value].copy())
+    holder = []
+
+    def alloc(_ctx, n_runs):
+        holder.append(np.empty((n_runs, 3), dtype=np.int32))
+        return holder[-1].ctypes.data
+
+    cb = _ALLOC_FN(alloc)
+    _check(_lib.ychg_build_profile_host_alloc(image._ptr(), image.width, image.height, image.row_stride,
+                                              strategy.kind, strategy.threads, counts.ctypes.data_as(_vp),
+                                              ctypes.cast(cb, _vp), None, ctypes.byref(n)), "build_profile")
+    runs = holder[-1] if holder else np.zeros((0, 3), dtype=np.int32)
+    return ColumnProfile(image.width, image.height, counts[: image.width].copy(), runs[: n.value])
 
 
 def column_runs(image: BinaryImage, col: int) -> np.ndarray:
-    """column_runs (runscan.cpp:104-120): (n, 3) int32 {col, y_top, y_bot}."""
+    """column_runs (runscan.cpp:104-120): (n, 3) int32 {col, y_top, y_bot}; moves one
+    byte column (O(height)) to the device, one call for columns of <= 65536 runs."""
     n = _i64(0)
-    _check(_lib.ychg_column_runs_host(image._ptr(), image.width, image.height, image.row_stride, int(col), None, 0,
-                                      ctypes.byref(n)), "column_runs")
-    out = np.zeros((max(n.value, 1), 3), dtype=np.int32)
-    if n.value > 0:
+    cap = max(1, min(image.height // 2 + 1, 1 << 16))
+    out = np.zeros((cap, 3), dtype=np.int32)
+    _check(_lib.ychg_column_runs_host(image._ptr(), image.width, image.height, image.row_stride, int(col),
+                                      out.ctypes.data_as(_vp), cap, ctypes.byref(n)), "column_runs")
+    if n.value > cap:
+        out = np.zeros((n.value, 3), dtype=np.int32)
         _check(_lib.ychg_column_runs_host(image._ptr(), image.width, image.height, image.row_stride, int(col),
                                           out.ctypes.data_as(_vp), n.value, ctypes.byref(n)), "column_runs")
     return out[: n.value].copy()
@@ -455,21 +467,25 @@ def decompose(source, strategy: ScanStrategy = ScanStrategy.serial(),
 
 
 # ---------------------------------------------------------------- device-resident plumbing
+STAMP_RING = 64  # ychg_device.cuh kStampRing: scans kept in the diagnostics stamp ring
+
+
 class Plan:
     """Geometry-specific launch plan + workspace on one device (ychg_plan_*)."""
 
     def __init__(self, width_img: int, height: int, width_cnt: int | None = None, device: int = 0,
-                 latency: bool = False, sync_inputs: bool = False):
-        """latency=True sizes the launch for isolated scans (YCHG_PLAN_LATENCY); the
-        default favours back-to-back (pipelined / graph-captured) scans.
-        sync_inputs=True (YCHG_PLAN_SYNC_INPUTS): the streaming kernel waits for the
-        kernel launched just before it, for images written by that kernel."""
+                 latency: bool = False, sync_inputs: bool = False, skip: bool = True):
+        """latency is accepted for compatibility (YCHG_PLAN_LATENCY, no effect: every
+        plan fills the GPU with one scan).  sync_inputs=True (YCHG_PLAN_SYNC_INPUTS):
+        the scan kernel waits for the kernel launched just before it, for images
+        written by that kernel.  skip=False (YCHG_PLAN_NO_SKIP): never skip 32-row
+        blocks identical to the row above (same results; A/B timing)."""
         self.device = device
         self.width_img, self.height = int(width_img), int(height)
         self.width_cnt = self.width_img if width_cnt is None else int(width_cnt)
         h = _vp()
         _check(_lib.ychg_plan_create_ex(device, self.width_img, self.width_cnt, self.height,
-                                        int(bool(latency)) | 2 * int(bool(sync_inputs)),
+                                        int(bool(latency)) | 2 * int(bool(sync_inputs)) | 4 * int(not skip),
                                         ctypes.byref(h)), "plan_create")
         self._h = h
 
@@ -494,21 +510,21 @@ class Plan:
         return a.value, b.value
 
     def debug_stamps(self, enable: bool = True):
-        """Per-CTA %globaltimer stamps (ns) of the last 4 scans, shape (4, grid, 32), indexed by
-        scan number % 4; see ychg_b200.h."""
+        """Per-CTA %globaltimer stamps (ns) of the last STAMP_RING scans, shape (STAMP_RING, grid, 32),
+        indexed by scan number % STAMP_RING; slots in ychg_scan.cu."""
         n = _i32(0)
         _check(_lib.ychg_plan_debug_stamps(self._h, int(enable), None, 0, ctypes.byref(n)), "debug_stamps")
         if not enable:
             return None
-        out = np.zeros((4, max(n.value, 1), 32), dtype=np.uint64)
+        out = np.zeros((STAMP_RING, max(n.value, 1), 32), dtype=np.uint64)
         _check(_lib.ychg_plan_debug_stamps(self._h, 1, out.ctypes.data_as(_vp), out.size, ctypes.byref(n)),
                "debug_stamps")
         return out[:, : n.value]
 
     def debug_peek(self):
-        """The stamp ring (4, max(grid, n_strips), 32) read without synchronising (diagnostics)."""
+        """The stamp ring (STAMP_RING, max(grid, n_strips), 32) read without synchronising (diagnostics)."""
         rows = max(self.info().grid, self.info().n_strips)
-        out = np.zeros((4, rows, 32), dtype=np.uint64)
+        out = np.zeros((STAMP_RING, rows, 32), dtype=np.uint64)
         _check(_lib.ychg_plan_debug_peek(self._h, out.ctypes.data_as(_vp), out.size), "debug_peek")
         return out
 

@@ -104,53 +104,21 @@ struct ychg_plan {
 
 namespace {
 
-// Pick the number of row segments per strip minimising the modelled makespan of
-// the persistent streaming kernel: waves of segments over the SMs, 8 warp bands
-// per segment, +1 block-time per segment for pipeline fill and the CTA merge.
-int choose_segments(int n_strips, int n_blocks, int sms, int* grid_out, bool latency = false) {
+// Row segments per strip: about one CTA per SM for one scan.  Each SM then
+// streams one segment of every scan, back-to-back scans interleave their CTAs on
+// the SM's three slots (PDL), and every segment is long enough to amortise its
+// ramp (first TMA round trip) and merge; measured at 21000^2 hbands(147), K=100
+// graph: 1 CTA/SM (k=7) 9.1 us/scan, 1.4/SM (k=10) 9.9, 3/SM (k=21) 14.8.
+// Bounds: a segment holds <= kMaxSegmentRows rows (u16 partials), every warp band
+// gets >= 2 blocks (tiny masks: fewer, fuller segments), k <= kMaxSegPerStrip.
+int choose_segments(int n_strips, int n_blocks, int sms, int warps) {
     const int max_seg_blocks = ychg_dev::kMaxSegmentRows / ychg_dev::kBlockRows;
-    int kmin = (n_blocks + max_seg_blocks - 1) / max_seg_blocks;
-    if (kmin < 1) kmin = 1;
-    // Large masks: few long CTAs, about half an SM's worth per scan.  Each CTA pays
-    // a fixed ramp + merge (~5 us) and back-to-back scans fill the other half of the
-    // SMs (two streaming CTAs per SM, programmatic dependent launch), so fewer,
-    // longer CTAs amortise it: measured at 21000^2 (21 strips, K=100 graph),
-    // k = 3/4/5/6/7/8 -> 12.7/12.8/13.2/13.3/13.6/14.0 us per scan.
-    // (A plan made for one isolated scan at a time -- the host entry points --
-    // keeps every SM busy instead: YCHG_PLAN_LATENCY.)
-    if (!latency && static_cast<long long>(n_strips) * n_blocks >= 8LL * sms * ychg_dev::kWarps) {
-        int k = std::max(1, (sms / 2 + std::max(1, n_strips) / 2) / std::max(1, n_strips));  // round(sms/2 / strips)
-        // ... but segments of at most 16384 rows: a very tall mask is better served by
-        // two resident CTAs per SM than by few extremely long ones (65536^2, K=30:
-        // k=2/128 CTAs -> 110 us full, 140 us counts-only; k=4/256 CTAs -> 110 / 110-119)
-        k = std::max(k, (n_blocks + 255) / 256);  // <= 8192 rows: 2048 rows per warp of a 4-warp CTA
-        k = std::max(k, kmin);
-        k = std::min(k, std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip)));
-        // all segments resident at once when they fit (plan_create clamps per path)
-        *grid_out = static_cast<int>(std::min<long long>(8LL * sms, static_cast<long long>(n_strips) * k));
-        return k;
-    }
-    double best = 1e300;
-    int best_k = kmin;
-    const int kmax = std::max(kmin, std::min(n_blocks, ychg_dev::kMaxSegPerStrip));
-    for (int k = kmin; k <= kmax; ++k) {
-        const long long segs = static_cast<long long>(n_strips) * k;
-        const long long G = std::min<long long>(sms, segs);
-        const long long waves = (segs + G - 1) / G;
-        const long long segb = (n_blocks + k - 1) / k;
-        const long long bpw = (segb + ychg_dev::kWarps - 1) / ychg_dev::kWarps;
-        const double cost = static_cast<double>(waves) * static_cast<double>(bpw + 1);
-        if (cost < best - 1e-9) {
-            best = cost;
-            best_k = k;
-        }
-        if (segs > 64LL * sms) break;
-    }
-    const long long segs = static_cast<long long>(n_strips) * best_k;
-    *grid_out = static_cast<int>(std::min<long long>(sms, segs));
-    return best_k;
+    const int kmin = std::max(1, (n_blocks + max_seg_blocks - 1) / max_seg_blocks);
+    int k = std::max(1, sms / std::max(1, n_strips));
+    k = std::min(k, std::max(1, n_blocks / (2 * warps)));
+    k = std::min(k, ychg_dev::kMaxSegPerStrip);
+    return std::max(k, kmin);
 }
-
 }  // namespace
 
 extern "C" {
@@ -200,55 +168,56 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
     p.n_strips = (width_cnt + ychg_dev::kStripCols - 1) / ychg_dev::kStripCols;
     p.n_blocks = (height + ychg_dev::kBlockRows - 1) / ychg_dev::kBlockRows;
     if (p.n_strips > 0 && p.n_blocks > 0) {
-        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, &plan->grid, (flags & YCHG_PLAN_LATENCY) != 0);
         p.wait_inputs = (flags & YCHG_PLAN_SYNC_INPUTS) ? 1 : 0;
-        // experiment hooks (benchmarking only): force the segments per strip / grid
-        if (const char* v = getenv("YCHG_SEGMENTS"); v && *v) {
-            // (never more segments than 32-row blocks: a segment must not be empty)
-            p.seg_per_strip = std::max(1, std::min(atoi(v), p.n_blocks));
-            plan->grid = static_cast<int>(std::min<long long>(8LL * sms, 1LL * p.n_strips * p.seg_per_strip));
+        p.skip_same = (flags & YCHG_PLAN_NO_SKIP) ? 0 : 1;
+        if (const char* v = getenv("YCHG_NO_SKIP"); v && v[0] == '1') p.skip_same = 0;  // A/B timing hook
+        // Resident CTAs per SM of each path's kernel (its grid is capped to what is
+        // resident: a strip finisher may wait on other CTAs of the same scan).
+        if (const int rc2 = ychg_scan_kernel_prepare())
+            return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
+        int per_path[2] = {0, 0}, warps[2] = {0, 0};
+        for (int path = 0; path < 2; ++path) {
+            int thr = 0, smem = 0;
+            ychg_scan_kernel_shape(path, &thr, &smem);
+            warps[path] = thr / 32;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_path[path], ychg_scan_kernel_ptr(path), thr, smem));
+            if (per_path[path] < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
         }
-        if (const char* v = getenv("YCHG_GRID"); v && *v)
-            plan->grid = std::max(1, std::min(atoi(v), p.n_strips * p.seg_per_strip));
+        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, warps[1]);
+        // experiment hook (benchmarking only): force the segments per strip
+        if (const char* v = getenv("YCHG_SEGMENTS"); v && *v)
+            p.seg_per_strip = std::max(1, std::min(atoi(v), p.n_blocks));  // a segment must not be empty
         p.n_segments = p.n_strips * p.seg_per_strip;
         if (p.seg_per_strip > ychg_dev::kMaxSegPerStrip)
             return fail(YCHG_ERR_INVALID, "plan_create: height %d needs more than %d row segments per strip",
                         height, ychg_dev::kMaxSegPerStrip);
-        // Occupancy of each path's streaming kernel (its grid is capped to what is resident).
-        if (const int rc2 = ychg_scan_kernel_prepare())
-            return cuda_fail(static_cast<cudaError_t>(rc2), "scan kernel smem opt-in");
-        // Each path's streaming kernel has its own CTA width, hence its own grid:
-        // up to what is resident at once (streaming CTAs never wait on each other;
-        // a CTA takes several segments when the grid is smaller).
-        int per_path[2] = {0, 0};
-        for (int path = 0; path < 2; ++path) {
-            int thr = 0, smem = 0;
-            ychg_scan_kernel_shape(path, &thr, &smem);
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_path[path], ychg_scan_kernel_ptr(path), thr, smem));
-            if (per_path[path] < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
+        plan->grid = std::min(p.n_segments, per_path[1] * sms);
+        plan->grid_counts = std::min(p.n_segments, per_path[0] * sms);
+        if (const char* v = getenv("YCHG_GRID"); v && *v) {
+            plan->grid = std::max(1, std::min(atoi(v), plan->grid));
+            plan->grid_counts = std::max(1, std::min(atoi(v), plan->grid_counts));
         }
-        const int want = plan->grid;
-        plan->grid = std::min(want, per_path[1] * sms);
-        plan->grid_counts = std::min(want, per_path[0] * sms);
         for (const int g : {plan->grid, plan->grid_counts})
             if ((p.n_segments + g - 1) / g > ychg_dev::kMaxSegPerCta)
                 return fail(YCHG_ERR_INVALID, "plan_create: %d segments over %d CTAs exceed %d per CTA",
                             p.n_segments, g, ychg_dev::kMaxSegPerCta);
         const int64_t S = p.n_strips, G = p.n_segments;
-        // part / sums / seg_links / seg_status are double-buffered by scan parity
-        const int64_t sz_part = 2 * G * 512 * 4, sz_sums = 2 * G * ychg_dev::kSumPlanes * 32 * 4, sz_seg = 2 * G * 8;
+        // part / sums / seg_links / rec are double-buffered by scan parity
+        const int64_t sz_part = 2 * G * 512 * 4, sz_sums = 2 * G * ychg_dev::kSumPlanes * 32 * 4;
         // strip records pack column counts (<= ceil(height/2)) in 21 bits
         if (height > (1 << 22) - 2)
             return fail(YCHG_ERR_INVALID, "plan_create: height %d > 2^22-2 rows is not supported", height);
-        const int64_t sz_rec = S * int64_t(sizeof(ychg_dev::StripRecord));
-        // order: part | sums | seg_links | seg_ticket | seg_status | fin_ticket | fin_all | fin_loaded[2][S] | rec
-        plan->ws_bytes = sz_part + sz_sums + 3 * sz_seg + 3 * S * 8 + 64 + sz_rec + 64;
+        const int64_t sz_rec = 2 * S * int64_t(sizeof(ychg_dev::StripRecord));
+        // order: part | sums | seg_links[2][G] | seg_ticket[G] | arrive[2][S] | fin_all | fin_loaded[2][S] | rec[2][S]
+        plan->ws_bytes = sz_part + sz_sums + 2 * G * 8 + G * 8 + 2 * S * 8 + 64 + 2 * S * 8 + sz_rec + 64;
         cudaError_t e = cudaMalloc(&plan->ws, plan->ws_bytes);
         if (e != cudaSuccess) {
             plan->ws = nullptr;
             return cuda_fail(e, "plan workspace cudaMalloc");
         }
+        // zeroed before any stream can use the plan (the counters are never reset)
         e = cudaMemset(plan->ws, 0, plan->ws_bytes);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
             cudaFree(plan->ws);
             plan->ws = nullptr;
@@ -260,13 +229,11 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         p.sums = reinterpret_cast<uint32_t*>(w);
         w += sz_sums;
         p.seg_links = reinterpret_cast<unsigned long long*>(w);
-        w += sz_seg;
+        w += 2 * G * 8;
         p.seg_ticket = reinterpret_cast<unsigned long long*>(w);
-        w += sz_seg;
-        p.seg_status = reinterpret_cast<unsigned long long*>(w);
-        w += sz_seg;
-        p.fin_ticket = reinterpret_cast<unsigned long long*>(w);
-        w += S * 8;
+        w += G * 8;
+        p.arrive = reinterpret_cast<unsigned long long*>(w);
+        w += 2 * S * 8;
         p.fin_all = reinterpret_cast<unsigned long long*>(w);
         w += 64;
         p.fin_loaded = reinterpret_cast<unsigned long long*>(w);
@@ -297,7 +264,7 @@ int ychg_plan_get_info(const ychg_plan* plan, ychg_plan_info* out) {
     out->seg_per_strip = plan->prm.seg_per_strip;
     out->n_segments = plan->prm.n_segments;
     out->grid = plan->grid;
-    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 2 : 0;
+    out->kernels_per_scan = (plan->prm.n_strips > 0 && plan->prm.n_blocks > 0) ? 1 : 0;
     out->workspace_bytes = plan->ws_bytes;
     return YCHG_OK;
 }
@@ -326,7 +293,7 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
                            int32_t* n_ctas) {
     if (!plan) return fail(YCHG_ERR_INVALID, "plan_debug_stamps: NULL plan");
     CK(cudaSetDevice(plan->device));
-    const int64_t bytes = int64_t(std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips)) * 32 * 8 * 4;
+    const int64_t bytes = int64_t(std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips)) * 32 * 8 * ychg_dev::kStampRing;
     if (enable && !plan->dbg && plan->grid > 0) {
         // zero-copy host memory, so a stalled pipeline can still be inspected (debug_peek)
         CK(cudaHostAlloc(reinterpret_cast<void**>(&plan->dbg_host), bytes, cudaHostAllocMapped));
@@ -350,7 +317,7 @@ int ychg_plan_debug_stamps(ychg_plan* plan, int32_t enable, uint64_t* host_out, 
 // Diagnostics: copy the stamp ring without synchronising (works while kernels stall).
 int ychg_plan_debug_peek(ychg_plan* plan, uint64_t* host_out, int32_t capacity) {
     if (!plan || !plan->dbg_host) return fail(YCHG_ERR_INVALID, "plan_debug_peek: stamps not enabled");
-    const int64_t bytes = int64_t(std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips)) * 32 * 8 * 4;
+    const int64_t bytes = int64_t(std::max(std::max(plan->grid, plan->grid_counts), plan->prm.n_strips)) * 32 * 8 * ychg_dev::kStampRing;
     std::memcpy(host_out, const_cast<const unsigned long long*>(plan->dbg_host),
                 size_t(std::min<int64_t>(capacity, bytes / 8)) * 8);
     return YCHG_OK;
@@ -409,6 +376,7 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     p.dbg_rows = std::max(std::max(plan->grid, plan->grid_counts), p.n_strips);
     p.mul2 = 2u;
     p.mul1 = 1u;
+    p.mulm1 = 0xFFFFFFFFu;
     p.mulnb = 1u << 25;
 
     if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
@@ -556,6 +524,8 @@ struct HostContext {
     uint8_t* h_stage[kStageSlots] = {};
     int64_t stage_bytes = 0;
     cudaEvent_t stage_ev[kStageSlots] = {};
+    uint8_t* h_col_stage = nullptr;  // column_runs: one byte column at a 16-byte pitch (pinned)
+    int64_t col_stage_cap = 0;
 };
 
 HostContext& host_context(int device) {
@@ -968,10 +938,9 @@ extern "C" int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, in
 // ---------------------------------------------------------------------------- run materialisation
 namespace {
 
-// Uploads the image and runs profile phase 0 (counts, column offsets, run total).
-int profile_phase0(HostContext& c, const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
-                   int64_t* n_runs) {
-    if (const int rc = upload_image(c, bits, width, height, row_stride)) return rc;
+// Profile phase 0 on the image already in c.d_bits (pitched for `width`): band
+// counts, column totals, column offsets and the run total (read back).
+int profile_count(HostContext& c, int32_t width, int32_t height, int64_t* n_runs) {
     if (const int rc = ensure_columns(c, width)) return rc;
     const int64_t pitch = ((int64_t(width) + 7) / 8 + 15) / 16 * 16;
     const int64_t bw = ychg_profile_band_words(width, height);
@@ -996,6 +965,13 @@ int profile_phase0(HostContext& c, const uint8_t* bits, int32_t width, int32_t h
     CK(cudaStreamSynchronize(c.stream));
     *n_runs = c.h_totals->total_runs;
     return YCHG_OK;
+}
+
+// Uploads the image and runs profile phase 0 (counts, column offsets, run total).
+int profile_phase0(HostContext& c, const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                   int64_t* n_runs) {
+    if (const int rc = upload_image(c, bits, width, height, row_stride)) return rc;
+    return profile_count(c, width, height, n_runs);
 }
 
 int profile_fill(HostContext& c, int32_t width, int32_t height, int64_t n_runs) {
@@ -1024,9 +1000,14 @@ int check_profile_args(const uint8_t* bits, int32_t width, int32_t height, int64
 
 }  // namespace
 
-extern "C" int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
-                                       int32_t strategy_kind, int32_t threads, int32_t* counts_out,
-                                       int32_t* runs_out, int64_t runs_capacity, int64_t* n_runs_out) {
+namespace {
+
+// build_profile body: phase 0, then `dest(n)` names the host buffer for the n
+// run triples (or nullptr: counts only); the image is uploaded and counted once.
+template <typename Dest>
+int build_profile_locked(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                         int32_t strategy_kind, int32_t threads, int32_t* counts_out, int64_t* n_runs_out,
+                         Dest&& dest) {
     // Same strategy validation as the scan (runscan.cpp:24-26); build_profile is strategy-independent.
     if (strategy_kind != YCHG_STRATEGY_SERIAL && strategy_kind != YCHG_STRATEGY_PARALLEL)
         return fail(YCHG_ERR_INVALID, "scan: unknown strategy kind %d", strategy_kind);
@@ -1047,7 +1028,8 @@ extern "C" int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32
     if (const int rc = profile_phase0(c, bits, width, height, row_stride, &n_runs)) return rc;
     if (n_runs_out) *n_runs_out = n_runs;
     if (counts_out) CK(cudaMemcpyAsync(counts_out, c.d_counts, int64_t(width) * 4, cudaMemcpyDeviceToHost, c.stream));
-    if (runs_out && runs_capacity >= n_runs && n_runs > 0) {
+    int32_t* runs_out = n_runs > 0 ? dest(n_runs) : nullptr;
+    if (runs_out) {
         if (const int rc = profile_fill(c, width, height, n_runs)) return rc;
         CK(cudaMemcpyAsync(runs_out, c.d_runs, n_runs * 12, cudaMemcpyDeviceToHost, c.stream));
     }
@@ -1055,6 +1037,34 @@ extern "C" int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32
     return YCHG_OK;
 }
 
+}  // namespace
+
+extern "C" int ychg_build_profile_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                       int32_t strategy_kind, int32_t threads, int32_t* counts_out,
+                                       int32_t* runs_out, int64_t runs_capacity, int64_t* n_runs_out) {
+    return build_profile_locked(bits, width, height, row_stride, strategy_kind, threads, counts_out, n_runs_out,
+                                [&](int64_t n) { return runs_capacity >= n ? runs_out : nullptr; });
+}
+
+extern "C" int ychg_build_profile_host_alloc(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
+                                             int32_t strategy_kind, int32_t threads, int32_t* counts_out,
+                                             ychg_alloc_fn alloc, void* alloc_ctx, int64_t* n_runs_out) {
+    if (!alloc) return fail(YCHG_ERR_INVALID, "build_profile: NULL allocator");
+    bool oom = false;
+    const int rc = build_profile_locked(bits, width, height, row_stride, strategy_kind, threads, counts_out,
+                                        n_runs_out, [&](int64_t n) {
+                                            auto* p = static_cast<int32_t*>(alloc(alloc_ctx, n));
+                                            oom = (p == nullptr);
+                                            return p;
+                                        });
+    if (rc == YCHG_OK && oom) return fail(YCHG_ERR_OOM, "build_profile: allocator returned NULL");
+    return rc;
+}
+
+// column_runs (runscan.cpp:104-120) moves O(height) bytes, not the image: only the
+// byte column holding `col` is gathered (pinned staging, one byte per row at a
+// 16-byte device pitch) and uploaded as an image of <= 8 columns, whose runs the
+// profile kernels materialise; Run.col is rebased on the returned triples.
 extern "C" int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
                                      int32_t col, int32_t* runs_out, int64_t runs_capacity, int64_t* n_out) {
     // runscan.cpp:105-107
@@ -1066,22 +1076,43 @@ extern "C" int ychg_column_runs_host(const uint8_t* bits, int32_t width, int32_t
     HostContext& c = host_context(device);
     std::lock_guard<std::mutex> lock(c.mu);
     if (const int rc = ensure_context(c)) return rc;
-    if (height == 0) {
-        if (n_out) *n_out = 0;
-        return YCHG_OK;
+    if (n_out) *n_out = 0;
+    if (height == 0) return YCHG_OK;
+    const int32_t xb = col / 8, j = col - 8 * xb;
+    const int32_t sub_w = std::min(8, width - 8 * xb);
+    const int64_t need = 16 * int64_t(height);
+    if (need > c.bits_cap) {
+        cudaFree(c.d_bits);
+        c.d_bits = nullptr;
+        c.bits_cap = 0;
+        CK(cudaMalloc(&c.d_bits, need));
+        c.bits_cap = need;
     }
+    if (need > c.col_stage_cap) {
+        if (c.h_col_stage) cudaFreeHost(c.h_col_stage);
+        c.h_col_stage = nullptr;
+        c.col_stage_cap = 0;
+        CK(cudaMallocHost(&c.h_col_stage, need));
+        std::memset(c.h_col_stage, 0, size_t(need));
+        c.col_stage_cap = need;
+    }
+    CK(cudaStreamSynchronize(c.stream));  // the staging buffer may still feed an earlier upload
+    const uint8_t* src = bits + xb;
+    for (int64_t y = 0; y < height; ++y) c.h_col_stage[16 * y] = src[y * row_stride];
+    CK(cudaMemcpyAsync(c.d_bits, c.h_col_stage, need, cudaMemcpyHostToDevice, c.stream));
     int64_t n_runs = 0;
-    if (const int rc = profile_phase0(c, bits, width, height, row_stride, &n_runs)) return rc;
+    if (const int rc = profile_count(c, sub_w, height, &n_runs)) return rc;
     int64_t off = 0;
     int32_t cnt = 0;
-    CK(cudaMemcpyAsync(&off, c.d_col_off + col, 8, cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaMemcpyAsync(&cnt, c.d_counts + col, 4, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&off, c.d_col_off + j, 8, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(&cnt, c.d_counts + j, 4, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     if (n_out) *n_out = cnt;
     if (runs_out && runs_capacity >= cnt && cnt > 0) {
-        if (const int rc = profile_fill(c, width, height, n_runs)) return rc;
+        if (const int rc = profile_fill(c, sub_w, height, n_runs)) return rc;
         CK(cudaMemcpyAsync(runs_out, c.d_runs + 3 * off, int64_t(cnt) * 12, cudaMemcpyDeviceToHost, c.stream));
         CK(cudaStreamSynchronize(c.stream));
+        for (int64_t i = 0; i < cnt; ++i) runs_out[3 * i] = col;  // sub-image column j -> image column col
     }
     return YCHG_OK;
 }

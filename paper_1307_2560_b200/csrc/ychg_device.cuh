@@ -15,62 +15,54 @@
 namespace ychg_dev {
 
 #ifndef YCHG_WARPS
-#define YCHG_WARPS 8
+#define YCHG_WARPS 4
 #endif
 #ifndef YCHG_STAGES
 #define YCHG_STAGES 3
 #endif
-constexpr int kWarps = YCHG_WARPS;               // warps per CTA
-constexpr int kThreads = kWarps * 32;
 constexpr int kStripWords = 32;                  // one warp lane per 32-column word
 constexpr int kStripCols = kStripWords * 32;     // 1024 columns per strip
 constexpr int kStripBytes = kStripWords * 4;     // 128 B of every row
 constexpr int kBoxBytes = kStripBytes + 16;      // + 16 B right halo (next strip's first word)
 constexpr int kBlockRows = 32;                   // rows per TMA stage / per Harley-Seal block
-constexpr int kStages = YCHG_STAGES;             // TMA ring depth per warp
 constexpr int kStageBytes = kBoxBytes * kBlockRows;   // 4608 B
 constexpr int kFlushBlocks = 15;                 // 8-bit bit-sliced counters: <= 15*16+15 = 255
 constexpr int kSumPlanes = 7;                    // K3 band summary planes (see BandSummary)
 constexpr int kMaxSegmentRows = 65504;           // u16 SWAR accumulators: counts <= rows/2 < 2^15
 
-constexpr int kMaxSegPerStrip = 128;            // the finisher keeps k summaries in smem
+constexpr int kMaxSegPerStrip = 128;            // row segments per strip (partials per strip finish)
 constexpr int kMaxSegPerCta = 64;               // segments one streaming CTA processes per scan
+constexpr int kFinishChunk = 16;                // K3 summaries loaded + composed per chunk by a strip finisher
+constexpr int kStampRing = 64;                  // diagnostics: scans kept in the per-CTA stamp ring
 
-// Shared-memory layout of an 8-warp scan CTA (bytes; see ScanSmem<NW> below).
-constexpr int kSmemStages = kWarps * kStages * kStageBytes;
-constexpr int kSmemBar = kWarps * kStages * 8;                         // mbarriers
-constexpr int kSmemAcc = kWarps * 16 * 32 * 4;                         // per-warp u16x2 counts
-constexpr int kSmemSum = kWarps * kSumPlanes * 32 * 4;                 // per-warp K3 summaries
-constexpr int kSmemMisc = kWarps * 24 + 48;                            // links, tree scratch, flags
-constexpr int kSmemTotal = kSmemStages + kSmemBar + kSmemAcc + kSmemSum + kSmemMisc;
-
-// The streaming kernel is instantiated per path with its own CTA width: the
-// ALU-bound full path (K1+K3) runs 4-warp CTAs (more CTAs per SM, so more
-// consecutive scans overlap and each CTA's merge is cheaper: 12.2 vs 13.0 us per
-// scan at 21000^2), the HBM-bound counts path 8-warp CTAs (more loads in flight
-// per scan: 10.0 vs 11.5 us with 2-stage rings; 9.0-9.4 us with 3).  Shared-memory layout of an NW-warp CTA:
+// The streaming kernel is instantiated per path (full: K1+K2+K3, counts: K1+K2)
+// with its own CTA width and TMA ring depth (YCHG_WARPS[_LINKS] / YCHG_STAGES[_LINKS]
+// build variants).  Both default to 4-warp CTAs with 3-stage rings (67 KB of
+// shared memory): three CTAs per SM, so one scan fills the GPU and the CTAs of
+// back-to-back scans interleave on an SM as they come and go.
 #ifndef YCHG_WARPS_LINKS
 #define YCHG_WARPS_LINKS 4
 #endif
-constexpr int kWarpsLinks = YCHG_WARPS_LINKS;
-constexpr int kWarpsCounts = kWarps;
 #ifndef YCHG_STAGES_LINKS
 #define YCHG_STAGES_LINKS YCHG_STAGES
 #endif
-constexpr int kStagesLinks = YCHG_STAGES_LINKS;  // TMA ring depth per warp of the full path
-template <int NW, int ST = kStages>
+constexpr int kWarpsLinks = YCHG_WARPS_LINKS;
+constexpr int kWarpsCounts = YCHG_WARPS;
+constexpr int kStagesLinks = YCHG_STAGES_LINKS;
+constexpr int kStagesCounts = YCHG_STAGES;
+template <int NW, int ST>
 struct ScanSmem {
     static constexpr int kStagesB = NW * ST * kStageBytes;
     static constexpr int kBar = NW * ST * 8;
     static constexpr int kAcc = NW * 16 * 32 * 4;
     static constexpr int kSum = NW * kSumPlanes * 32 * 4;
-    static constexpr int kMisc = NW * 24 + 48;
+    static constexpr int kMisc = NW * 24 + 64;
     static constexpr int kTotal = kStagesB + kBar + kAcc + kSum + kMisc;
 };
 template <bool kLinks>
 __host__ __device__ constexpr int scan_warps() { return kLinks ? kWarpsLinks : kWarpsCounts; }
 template <bool kLinks>
-__host__ __device__ constexpr int scan_stages() { return kLinks ? kStagesLinks : kStages; }
+__host__ __device__ constexpr int scan_stages() { return kLinks ? kStagesLinks : kStagesCounts; }
 template <bool kLinks>
 __host__ __device__ constexpr int scan_smem() { return ScanSmem<scan_warps<kLinks>(), scan_stages<kLinks>()>::kTotal; }
 
@@ -86,10 +78,10 @@ struct StripRecord {
 };
 
 // ----------------------------------------------------------------------------
-// Launch parameters of one scan.  Cross-CTA bookkeeping (segment flags, strip
-// records) is epoch-tagged -- each segment and each strip finisher numbers its
-// scans with its own monotonic ticket, so both sides agree -- it never needs
-// resetting between scans and the launches are CUDA-graph replayable.
+// Launch parameters of one scan.  Cross-CTA bookkeeping is epoch-tagged or
+// monotonic -- every segment numbers its scans with its own ticket, and all k
+// segments of a strip agree on it -- so nothing is reset between scans and the
+// launches are CUDA-graph replayable.
 struct ScanParams {
     const uint8_t* bits;      // device image base (row-major packed bits)
     int64_t pitch;            // bytes between rows (multiple of 16 for TMA)
@@ -102,17 +94,18 @@ struct ScanParams {
     int32_t seg_per_strip;    // k: row segments per strip
     int32_t n_segments;       // n_strips * k
     uint32_t mul2, mulnb;     // 2 and 1 << 25 as runtime values: keeps the b-word shifts on IMAD
-    uint32_t mul1;            // 1 as a runtime value: keeps the link adds on IMAD
-    uint32_t* part;           // [n_segments][512] per-segment u16x2 column counts
-    uint32_t* sums;           // [n_segments][7][32] K3 band summaries
-    unsigned long long* seg_links;    // [n_segments] links closed inside each segment
+    uint32_t mul1, mulm1;     // 1 and -1 as runtime values: keeps disjoint adds / subset subtracts on IMAD
+    int32_t skip_same;        // 1: skip 32-row blocks identical to the row above (state is unchanged)
+    // per scan parity (two halves: scan t+1 fills one while scan t's finishers read the other)
+    uint32_t* part;           // [2][n_segments][512] per-segment u16x2 column counts
+    uint32_t* sums;           // [2][n_segments][7][32] K3 band summaries (one per segment)
+    unsigned long long* seg_links;    // [2][n_segments] links closed inside each segment
     unsigned long long* seg_ticket;   // [n_segments] scans started per segment (monotonic)
-    unsigned long long* seg_status;   // [n_segments] epoch tag of the last merged segment (release)
-    unsigned long long* fin_ticket;   // [n_strips] scans started per strip finisher (monotonic)
-    unsigned long long* fin_all;      // [1] strip finishers completed (monotonic)
-    unsigned long long* fin_loaded;   // [2][n_strips] per buffer half: 1 + the last scan whose
-                                      // partials of that half the strip's finisher has loaded
-    struct StripRecord* rec;  // [n_strips] published by each strip's finisher
+    unsigned long long* arrive;       // [2][n_strips] segments of the strip merged (monotonic, +k per scan)
+    unsigned long long* fin_all;      // [1] strip finishes completed (monotonic)
+    unsigned long long* fin_loaded;   // [2][n_strips] per half: 1 + the last scan whose inputs of that
+                                      //   half the strip's finisher has read
+    struct StripRecord* rec;  // [2][n_strips] published by each strip's finisher
     long long* totals;        // ychg_totals {total_runs, links, hyperedges, n_boundaries}
     int32_t* counts;          // [width_cnt] final per-column counts
     uint32_t* flags;          // [ceil(width_cnt/32)] change flags, bit j = column 32w+j

@@ -2,6 +2,7 @@
 // ychg::detect_boundary_columns (reference runscan.hpp:59-71) implemented over
 // the C ABI of libychg_b200.so.  Status codes become the reference's exception
 // types (errors.hpp:11-40); there is no CPU fallback.
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -16,13 +17,16 @@ namespace ychg {
 
 namespace {
 
+// Validation messages of the C ABI are worded like the reference's own
+// (runscan.cpp:25-26,105-107: "scan: parallel strategy needs threads >= 1, got 0",
+// "column_runs: column 4 out of range [0, 4)") and pass through unprefixed, so
+// what() matches the reference; device/runtime failures get the entry point.
 void check(int rc, const char* what) {
     if (rc == YCHG_OK) return;
     if (rc == YCHG_ERR_PARSE)
         throw ParseError(ychg_last_error(), static_cast<std::size_t>(ychg_last_error_offset()));
-    const std::string msg = std::string(what) + ": " + ychg_last_error();
-    if (rc == YCHG_ERR_INVALID) throw ValidationError(msg);
-    throw Error(msg);
+    if (rc == YCHG_ERR_INVALID) throw ValidationError(ychg_last_error());
+    throw Error(std::string(what) + ": " + ychg_last_error());
 }
 
 // The PNM loader's messages are the reference's own (pnm.cpp), unprefixed.
@@ -104,15 +108,20 @@ std::vector<int> cut_vertex_counts(const BinaryImage& image, ScanStrategy strate
 }
 
 std::vector<Run> column_runs(const BinaryImage& image, int col) {
+    // a column holds at most ceil(height/2) runs; one call fills up to that many
+    std::vector<Run> runs(static_cast<std::size_t>(std::min(image.height() / 2 + 1, 1 << 16)));
     std::int64_t n = 0;
     check(ychg_column_runs_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), col,
-                                nullptr, 0, &n),
+                                reinterpret_cast<std::int32_t*>(runs.data()), static_cast<std::int64_t>(runs.size()),
+                                &n),
           "column_runs");
-    std::vector<Run> runs(static_cast<std::size_t>(n));
-    if (n > 0)
+    if (n > static_cast<std::int64_t>(runs.size())) {  // very tall column: second call at the exact size
+        runs.resize(static_cast<std::size_t>(n));
         check(ychg_column_runs_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), col,
                                     reinterpret_cast<std::int32_t*>(runs.data()), n, &n),
               "column_runs");
+    }
+    runs.resize(static_cast<std::size_t>(n));
     return runs;
 }
 
@@ -123,16 +132,17 @@ ColumnProfile build_profile(const BinaryImage& image, ScanStrategy strategy) {
     p.width = image.width();
     p.height = image.height();
     p.counts.assign(static_cast<std::size_t>(image.width()), 0);
+    std::vector<Run> flat;
     std::int64_t n = 0;
-    check(ychg_build_profile_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), kind,
-                                  strategy.threads, p.counts.data(), nullptr, 0, &n),
+    // one call: the library asks for the run buffer once it knows the total
+    auto alloc = [](void* ctx, std::int64_t n_runs) -> void* {
+        auto* v = static_cast<std::vector<Run>*>(ctx);
+        v->resize(static_cast<std::size_t>(n_runs));
+        return v->data();
+    };
+    check(ychg_build_profile_host_alloc(image.bytes().data(), image.width(), image.height(), image.row_stride(),
+                                        kind, strategy.threads, p.counts.data(), alloc, &flat, &n),
           "build_profile");
-    std::vector<Run> flat(static_cast<std::size_t>(n));
-    if (n > 0)
-        check(ychg_build_profile_host(image.bytes().data(), image.width(), image.height(), image.row_stride(), kind,
-                                      strategy.threads, p.counts.data(), reinterpret_cast<std::int32_t*>(flat.data()),
-                                      n, &n),
-              "build_profile");
     p.runs.resize(static_cast<std::size_t>(image.width()));
     std::size_t at = 0;
     for (int c = 0; c < image.width(); ++c) {

@@ -1,36 +1,39 @@
-// ychg_scan.cu -- the yCHG hot path on sm_100a: two kernels per scan, chained by
-// programmatic dependent launch (PDL), graph-capturable.
+// ychg_scan.cu -- the yCHG hot path on sm_100a: ONE kernel per scan, graph-
+// capturable, chained to the next scan by programmatic dependent launch (PDL).
 //
 //   K1  per-column cut-vertex counts      (reference runscan.cpp:41-74,122-128)
 //   K2  change flags + ascending boundary  (runscan.cpp:145-153)
 //   K3  hyperedge total = runs - links     (hypergraph.cpp:94-170,192)
 //
-// ychg_scan_kernel<with_links, NW> (streaming): the mask is cut into 1024-column
-// strips (one 32-bit word per lane) and every strip into k row segments; CTA g
-// owns segments g, g+G, ...  A segment is split into NW consecutive warp bands
-// (NW = 4 for the ALU-bound K1+K3 path, 8 for the HBM-bound counts path).  Each
-// warp streams its band through its own 3-stage TMA ring (cp.async.bulk.tensor,
-// 32 rows x 144 B per stage: 128 B of the strip + a 16 B right halo) and runs K1
-// + K3 bit-sliced in registers; the CTA merges its warps in shared memory and
-// writes one partial per segment (counts + K3 band summary + links, coalesced)
-// into a workspace double-buffered by scan parity, then release-stores an
-// epoch-tagged segment flag.
+// The mask is cut into 1024-column strips (one 32-bit word per lane) and every
+// strip into k row segments; CTA g owns segments g, g+G, ... (one each when the
+// grid covers them: the planner sizes k so one scan fills every resident CTA
+// slot of the GPU).  A segment is split into NW consecutive warp bands; each
+// warp streams its band through its own TMA ring (cp.async.bulk.tensor, 32 rows
+// x 144 B per stage: 128 B of the strip + a 16 B right halo) and runs K1 + K3
+// bit-sliced in registers.  The CTA merges its warps in shared memory, writes
+// one partial per segment (counts + K3 band summary + links) into a workspace
+// double-buffered by scan parity, and counts itself in on the strip's arrival
+// counter.  The LAST segment of a strip to arrive finishes the strip in the same
+// CTA (no second kernel, no CTA waiting on a segment): it sums the k partials,
+// composes the K3 summaries, publishes a strip record, derives its boundary
+// offset and first-column flag from every record to its left (warp-parallel
+// look-back), compacts the boundary list; the right-most strip writes totals.
 //
-// ychg_finish_kernel<with_links> (one small CTA per strip, co-resident with the
-// streaming CTAs): waits for its strip's k flags, loads the partials, releases
-// the buffer half, composes the K3 summaries, publishes a strip record and
-// derives its boundary offset and first-column flag from every record to its
-// left (warp-parallel look-back), compacts the boundary list; the right-most
-// strip writes the totals.
-//
-// Consecutive scans overlap (the finisher of scan t runs while scan t+1
-// streams).  The invariants that make this safe are listed in DESIGN.md §3
-// ("Cross-scan invariants"): per-half fin_loaded, every per-segment input read
-// before the half is released, scan tickets drawn before launch_dependents.
+// Consecutive scans overlap: every CTA triggers the next scan's launch at entry,
+// so the next scan's CTAs take SM slots as this scan's CTAs retire.  Invariants
+// (DESIGN.md §3): tickets drawn before the trigger (they then follow launch
+// order); a segment's partial half is reused only after the finisher of the
+// scan two back loaded it (fin_loaded); a strip finisher publishes nothing
+// before every finisher of the previous scan is done (fin_all).  Waits are
+// deadlock-free: all CTAs of a scan are resident before the next scan launches
+// (PDL trigger semantics), a CTA processes its segments in increasing order,
+// and a finisher only waits on strips to its left or on the previous scan.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "ychg_device.cuh"
 #include "ychg_kernels.h"
@@ -45,6 +48,7 @@ struct LaneState {
     uint32_t acc[16];          // u16x2 per-column totals (see acc_column)
     uint32_t pa, pb;           // previous row: column c and column c+1 bits
     uint32_t pab;              // pa & pb (K3)
+    uint32_t praw;             // previous row's raw (load-order) word: the skip test compares raw words
     uint32_t mk3;              // valid column pairs of this word
     // K3
     uint32_t G2, G3;           // open component holds >= 2 / >= 3 runs
@@ -74,11 +78,13 @@ __device__ __forceinline__ void flush_counts(LaneState& s) {
 // (hypergraph.cpp:137-143).  Head pairs (open across the band's top edge) start
 // "poisoned" at N >= 3 so their unknown-prefix component never counts here;
 // kHead additionally tracks their new runs (h1, h2) until they close (Hd <= G2,
-// so Hd & f == Hd & ab & ~pab likewise).
+// so Hd & f == Hd & ab & ~pab likewise).  `apa` (a & pa) is handed back: K1's
+// rise word a & ~pa is then a - apa, an IMAD.
 template <bool kHead>
-__device__ __forceinline__ uint32_t k3_step(uint32_t a, uint32_t b, LaneState& s) {
+__device__ __forceinline__ uint32_t k3_step(uint32_t a, uint32_t b, LaneState& s, uint32_t& apa) {
     const uint32_t ab = a & b;
-    const uint32_t cont = lop3<0xF8>(a & s.pa, b, s.pb);       // (a & pa) | (b & pb)
+    apa = a & s.pa;
+    const uint32_t cont = lop3<0xF8>(apa, b, s.pb);            // (a & pa) | (b & pb)
     const uint32_t lk = lop3<0x04>(cont, s.G2, s.G3);          // ~cont & G2 & ~G3
     if (kHead) {
         s.Hd &= cont;
@@ -96,66 +102,66 @@ __device__ __forceinline__ uint32_t k3_step(uint32_t a, uint32_t b, LaneState& s
     return lk;
 }
 
-// 32 rows from one TMA stage: 16 row pairs -> Harley-Seal tree -> ripple planes.
-// Rises of one column are never in consecutive rows, so a row pair contributes
-// (a0 & ~pa) | (a1 & ~a0) -- one LOP3.  Links of one pair are likewise never in
-// consecutive rows and are popcounted per row pair.
-// Right neighbour (column c+1 at column c's bit) of a raw little-endian word:
-// inside a byte it is one bit lower (raw << 1); bit 0 of byte L takes bit 7 of
-// byte L+1 (raw >> 15), byte 3 takes bit 7 of the next word's byte 0 (nb << 17).
-// The shifts run as IMAD / IMAD.HI on the FMA pipe (runtime multipliers keep
-// ptxas from turning them into ALU shifts); one LOP3 merges them.
-// (Raw-order variant, kept for the diagnostics microbenchmarks: mul = 1 << 17.)
-__device__ __forceinline__ uint32_t right_neighbour(uint32_t raw, uint32_t nb, uint32_t mul2, uint32_t mul17) {
-    const uint32_t t1 = raw * mul2;
-    const uint32_t t3 = nb * mul17 + __umulhi(raw, mul17);
-    return lop3<0xE2>(t1, 0xFEFEFEFEu, t3);  // (t1 & M) | (t3 & ~M): bit select, one LOP3
-}
-
 // The K3 path runs on MSB-first words (one PRMT per row): the right neighbour is
 // then a << 1 with the next word's first bit shifted in, i.e. the MSB of the
-// next byte nb -- IMAD(a, 2, umulhi(nb, 1 << 25)), no ALU op at all (the
-// raw-order merge above costs an extra LOP3 + IMAD; measured -4 % per row).
+// next byte nb -- IMAD(a, 2, umulhi(nb, 1 << 25)), no ALU op at all.
 __device__ __forceinline__ uint32_t right_neighbour_msb(uint32_t a, uint32_t nb, uint32_t mul2, uint32_t mul25) {
     return a * mul2 + __umulhi(nb, mul25);
 }
 
+struct Muls {
+    uint32_t m2, mnb, m1, mm1;  // 2, 1 << 25, 1, -1 (runtime values: ptxas keeps the IMADs)
+};
+
+// 32 rows from one TMA stage: 16 row pairs -> Harley-Seal tree -> ripple planes.
+// Rises of one column are never in consecutive rows, so a row pair contributes
+// (a0 & ~pa) | (a1 & ~a0): on the K3 path the two terms are a - (a & pa) from
+// k3_step's `apa`, disjoint, so the pair word is three IMADs on the FMA pipe
+// (the ALU pipe is the K3 path's bottleneck); the counts path keeps one LOP3.
+// Links of one pair are likewise never in consecutive rows and are popcounted
+// per row pair.
 // kMask (strips with invalid column pairs -- the image's last column, or a
 // multi-GPU strip's right halo): the right-hand column of an invalid pair is
 // zeroed, so its components hold one run and never link.  Full strips skip it,
 // which lets the two row links of a pair be added on the FMA pipe (they are
 // disjoint bit sets) instead of a masked LOP3.
-template <bool kLinks, bool kHead, bool kBs = kLinks, bool kMask = false>
-__device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage, int lane,
-                                              LaneState& s, uint32_t mul2, uint32_t mulnb, uint32_t mul1) {
+template <bool kLinks, bool kHead, bool kMask = false>
+__device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage, int lane, LaneState& s,
+                                              const Muls& mu) {
     const uint8_t* p = stage + 4 * lane;
     uint32_t Pprev = 0, tA = 0, fA = 0, eA = 0;
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         const uint8_t* r0 = p + (2 * q) * kBoxBytes;
         const uint8_t* r1 = r0 + kBoxBytes;
-        uint32_t a0 = *reinterpret_cast<const uint32_t*>(r0);
-        uint32_t a1 = *reinterpret_cast<const uint32_t*>(r1);
-        if (kBs) {  // MSB-first words (bit 31-j = column j): b = a << 1 | next byte's MSB, FMA pipe
-            a0 = __byte_perm(a0, 0u, 0x0123u);
-            a1 = __byte_perm(a1, 0u, 0x0123u);
-        }
-        const uint32_t P = lop3<0x3A>(a0, s.pa, a1);  // (a0 & ~pa) | (a1 & ~a0)
-        if (kLinks) {
-            uint32_t b0 = kBs ? right_neighbour_msb(a0, r0[4], mul2, mulnb)
-                              : right_neighbour(a0, r0[4], mul2, mulnb);
-            uint32_t b1 = kBs ? right_neighbour_msb(a1, r1[4], mul2, mulnb)
-                              : right_neighbour(a1, r1[4], mul2, mulnb);
+        const uint32_t raw0 = *reinterpret_cast<const uint32_t*>(r0);
+        const uint32_t raw1 = *reinterpret_cast<const uint32_t*>(r1);
+        uint32_t P;
+        if (kLinks) {  // MSB-first words (bit 31-j = column j): b = a << 1 | next byte's MSB, FMA pipe
+            const uint32_t a0 = __byte_perm(raw0, 0u, 0x0123u);
+            const uint32_t a1 = __byte_perm(raw1, 0u, 0x0123u);
+            uint32_t b0 = right_neighbour_msb(a0, r0[4], mu.m2, mu.mnb);
+            uint32_t b1 = right_neighbour_msb(a1, r1[4], mu.m2, mu.mnb);
             if (kMask) {
                 b0 &= s.mk3;
                 b1 &= s.mk3;
             }
-            const uint32_t l0 = k3_step<kHead>(a0, b0, s);
-            const uint32_t l1 = k3_step<kHead>(a1, b1, s);
+            uint32_t apa0, apa1;
+#ifdef YCHG_P_ALU  // A/B variant: the pair's rise word as one LOP3 (MSB-first words)
+            const uint32_t pa_old = s.pa;
+#endif
+            const uint32_t l0 = k3_step<kHead>(a0, b0, s, apa0);
+            const uint32_t l1 = k3_step<kHead>(a1, b1, s, apa1);
             // l0 | l1 == l0 + l1 (disjoint); IMADs keep both adds off the ALU pipe
-            s.links = __popc(l0 * mul1 + l1) * mul1 + s.links;
+            s.links = __popc(l0 * mu.m1 + l1) * mu.m1 + s.links;
+#ifdef YCHG_P_ALU
+            P = lop3<0x3A>(a0, pa_old, a1);
+#else
+            P = (apa0 * mu.mm1 + a0) * mu.m1 + (apa1 * mu.mm1 + a1);  // (a0 - a0&pa) + (a1 - a1&a0)
+#endif
         } else {
-            s.pa = a1;
+            P = lop3<0x3A>(raw0, s.pa, raw1);  // (a0 & ~pa) | (a1 & ~a0)
+            s.pa = raw1;
         }
 #ifdef YCHG_DIAG_NO_K1  // microbenchmark-only: K3 alone (counts wrong)
         s.ones ^= P;
@@ -195,6 +201,43 @@ __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage,
         s.u64 ^= c2;
         s.u128 ^= c3;
     }
+    if (kLinks) s.praw = *reinterpret_cast<const uint32_t*>(p + 31 * kBoxBytes);
+}
+
+// True (warp-uniform) iff every row of the stage equals the row above it for
+// every word of the warp AND for the right-halo bit lane 31's pairs read: then
+// K1 sees no rise, and every K3 plane (cont == a|b, G2, G3, Hd, h1, h2, pa, pb)
+// maps to itself, so the block is a no-op and is skipped.  Rows 0..7 are tested
+// first, so a block that changes early (random masks) pays ~8 compares.
+// `phalo` carries the halo byte of the row above (row 31 of the previous block).
+__device__ __forceinline__ bool block_unchanged(const uint8_t* __restrict__ stage, int lane, uint32_t praw,
+                                                uint32_t& phalo) {
+    const uint8_t* p = stage + 4 * lane;
+    uint32_t x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x[r] = *reinterpret_cast<const uint32_t*>(p + r * kBoxBytes);
+    // right halo column (bit 7 of the halo's first byte): lane L holds row L
+    const uint32_t hb = stage[lane * kBoxBytes + kStripBytes];
+    uint32_t hprev = __shfl_up_sync(0xFFFFFFFFu, hb, 1);
+    if (lane == 0) hprev = phalo;
+    // (x ^ y) | (z ^ x) = lop3 0x7E: two row compares per LOP3; 0xFE = 3-way OR
+    uint32_t d = lop3<0x28>(hb, hprev, 0x80u);  // (hb ^ hprev) & 0x80
+    d = lop3<0xFE>(d, lop3<0x7E>(x[0], praw, x[1]), lop3<0x7E>(x[2], x[1], x[3]));
+    d = lop3<0xFE>(d, lop3<0x7E>(x[4], x[3], x[5]), lop3<0x7E>(x[6], x[5], x[7]));
+    if (__any_sync(0xFFFFFFFFu, d != 0u)) return false;
+    uint32_t prev = x[7];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        uint32_t y[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) y[r] = *reinterpret_cast<const uint32_t*>(p + (8 + 8 * c + r) * kBoxBytes);
+        d = lop3<0xFE>(d, lop3<0x7E>(y[0], prev, y[1]), lop3<0x7E>(y[2], y[1], y[3]));
+        d = lop3<0xFE>(d, lop3<0x7E>(y[4], y[3], y[5]), lop3<0x7E>(y[6], y[5], y[7]));
+        prev = y[7];
+    }
+    const bool same = !__any_sync(0xFFFFFFFFu, d != 0u);
+    phalo = __shfl_sync(0xFFFFFFFFu, hb, 31);
+    return same;
 }
 
 // Valid-bit mask of word `gw` for `limit` columns: columns j < limit-32*gw, MSB-first.
@@ -211,13 +254,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// dbg layout: [scan index % 4][CTA][32 slots]; `ring` must be in scope.
-#define YCHG_STAMP_AT(slot, value)                                                                       \
-    do {                                                                                                 \
-        if (prm.dbg)                                                                                     \
-            prm.dbg[(static_cast<int64_t>(ring) * prm.dbg_rows + blockIdx.x) * 32 + (slot)] = (value);      \
-    } while (0)
-#define YCHG_STAMP(slot) YCHG_STAMP_AT(slot, globaltimer())
+// Diagnostics stamps: dbg layout [scan % kStampRing][CTA][32 slots] (ns, %globaltimer).
+//   0 CTA entry, 1 first segment streamed (all warps), 2 first segment arrived,
+//   3 strip finish entered, 4 strip finish left, 5 CTA exit, 6 first stage ready
+//   (warp 0), 7 warp 0's band streamed, 8 scan number + 1
+__device__ __forceinline__ void stamp(const ScanParams& prm, unsigned long long scan, int slot,
+                                      unsigned long long v) {
+    if (prm.dbg)
+        prm.dbg[(static_cast<int64_t>(scan % kStampRing) * prm.dbg_rows + blockIdx.x) * 32 + slot] = v;
+}
 
 __device__ __forceinline__ unsigned long long atom_add_acq_rel(unsigned long long* p, unsigned long long v) {
     unsigned long long old;
@@ -231,61 +276,102 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
     return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// In-place, order-preserving tree composition of n band summaries stored in
-// shared memory (slot i = 7 planes x 32 lanes at base + i*224), using every warp
-// of the CTA: level s composes slots (p*2s, p*2s+s) into p*2s.  Returns, in
-// every thread, the number of links resolved at the junctions.  Must be called
-// by the whole CTA (contains __syncthreads).
+__device__ __forceinline__ BandSummary load_summary(const uint32_t* a, int lane) {
+    return BandSummary{a[lane], a[32 + lane], a[64 + lane], a[96 + lane], a[128 + lane], a[160 + lane], a[192 + lane]};
+}
+
+__device__ __forceinline__ void store_summary(uint32_t* a, int lane, const BandSummary& C) {
+    a[lane] = C.O;
+    a[32 + lane] = C.E;
+    a[64 + lane] = C.h1;
+    a[96 + lane] = C.h2;
+    a[128 + lane] = C.OE;
+    a[160 + lane] = C.T2;
+    a[192 + lane] = C.T3;
+}
+
+// Order-preserving composition of n >= 1 band summaries stored in shared memory
+// (slot i = 7 planes x 32 lanes at base + i*224): warp w composes the slots of
+// its contiguous chunk in registers, one __syncthreads, then warp 0 composes the
+// chunk results.  A chain in registers beats a log-depth tree here: every tree
+// level would cost a CTA barrier, and one compose is ~30 ALU ops.  Returns, in
+// warp 0 only, the composite (every lane its word) and the number of links
+// resolved at the junctions (all lanes); `red` is NW scratch words.  Must be
+// called by the whole CTA.
 template <int NW>
-__device__ unsigned long long tree_compose(uint32_t* base, int n, unsigned long long* red) {
+__device__ BandSummary chain_compose(const uint32_t* base, int n, unsigned long long* red,
+                                     unsigned long long& links) {
     constexpr int kSW = kSumPlanes * 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long mine = 0;
-    for (int st = 1; st < n; st <<= 1) {
-        for (int p = warp; p * 2 * st + st < n; p += NW) {
-            uint32_t* a = base + (p * 2 * st) * kSW;
-            const uint32_t* b = base + (p * 2 * st + st) * kSW;
-            const BandSummary A{a[lane], a[32 + lane], a[64 + lane], a[96 + lane], a[128 + lane], a[160 + lane],
-                                a[192 + lane]};
-            const BandSummary B{b[lane], b[32 + lane], b[64 + lane], b[96 + lane], b[128 + lane], b[160 + lane],
-                                b[192 + lane]};
+    const int c0 = (warp * n) / NW, c1 = ((warp + 1) * n) / NW;
+    BandSummary A{};
+    if (c1 > c0) {
+        A = load_summary(base + c0 * kSW, lane);
+        for (int i = c0 + 1; i < c1; ++i) {
+            const BandSummary B = load_summary(base + i * kSW, lane);
             BandSummary C;
             mine += __popc(compose_summary(A, B, C));
-            a[lane] = C.O;
-            a[32 + lane] = C.E;
-            a[64 + lane] = C.h1;
-            a[96 + lane] = C.h2;
-            a[128 + lane] = C.OE;
-            a[160 + lane] = C.T2;
-            a[192 + lane] = C.T3;
+            A = C;
         }
-        __syncthreads();
     }
+    __shared__ uint32_t chunk[NW][kSumPlanes * 32];
+    if (c1 > c0) store_summary(chunk[warp], lane, A);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
     if (lane == 0) red[warp] = mine;
     __syncthreads();
-    unsigned long long t = 0;
-    for (int w = 0; w < NW; ++w) t += red[w];
-    __syncthreads();
-    return t;
+    links = 0;
+    if (warp == 0) {
+        bool first = true;
+        unsigned long long jl = 0;
+        for (int w = 0; w < NW; ++w) {
+            if (((w + 1) * n) / NW <= (w * n) / NW) continue;
+            const BandSummary B = load_summary(chunk[w], lane);
+            if (first) {
+                A = B;
+                first = false;
+            } else {
+                BandSummary C;
+                jl += __popc(compose_summary(A, B, C));
+                A = C;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) jl += __shfl_xor_sync(0xFFFFFFFFu, jl, o);
+        for (int w = 0; w < NW; ++w) jl += red[w];
+        links = jl;
+    }
+    return A;
 }
 
-// Shared-memory scratch of the strip finisher (lives in the idle TMA stage area).
+// Shared-memory scratch of a strip finish (overlaid on the CTA's idle TMA ring).
+template <int NW>
 struct FinishSmem {
     int32_t sc[kStripCols];       // counts of the strip's columns
     uint32_t fw[kStripWords];     // change-flag words of the strip (inside flags only)
     int wpre[kStripWords];        // exclusive prefix of popc(fw)
-    long long red[kWarps];
-    long long red2[kWarps];
+    long long red[NW];
+    unsigned long long red2[NW];
     long long base;
-    unsigned long long seglinks;  // links closed inside the strip's segments (loaded with the partials)
+    long long n_total;            // boundaries up to and including this strip (right-most: the total)
+    unsigned long long seglinks;  // links closed inside the strip's segments
     uint32_t edge;                // flag of the strip's first column
 };
+template <int NW>
+__host__ __device__ constexpr int finish_smem_bytes() {
+    return ((static_cast<int>(sizeof(FinishSmem<NW>)) + 127) / 128) * 128 + (kFinishChunk + 1) * kSumPlanes * 32 * 4;
+}
 
 __device__ __forceinline__ unsigned long long pack_strip_status(uint32_t epoch, uint32_t inside, int32_t first,
                                                                 int32_t last) {
@@ -295,153 +381,111 @@ __device__ __forceinline__ unsigned long long pack_strip_status(uint32_t epoch, 
            (static_cast<unsigned long long>(static_cast<uint32_t>(last) & 0x1FFFFFu));
 }
 
-// Warp-uniform wait until word p (per active lane) carries `epoch` in its top 12 bits.
-__device__ __forceinline__ unsigned long long warp_wait_epoch12(const unsigned long long* p, bool active,
-                                                               uint32_t epoch) {
-    unsigned long long v = 0;
-    bool ok = !active;
-    while (true) {
-        if (!ok) {
-            v = ld_acquire(p);
-            ok = static_cast<uint32_t>(v >> 52) == (epoch & 0xFFFu);
-        }
-        if (__all_sync(0xFFFFFFFFu, ok)) break;
-    }
-    return v;
-}
-
-// Finish strip s: counts, K3 stitch, flags, boundary compaction, totals.
-// This runs on the kernel's tail, so it is built around global round trips:
-// one batch of loads, one release of the strip record (flags strictly inside
-// the strip + counts of its first and last column), one warp-parallel acquire
-// of every record to the left -- from which the boundary offset AND this
-// strip's first-column flag (counts[c0] vs counts[c0-1], runscan.cpp:147)
-// follow -- then fire-and-forget writes.
-template <bool kLinks>
-__global__ void __launch_bounds__(kThreads)
-ychg_finish_kernel(const ScanParams prm) {
-    extern __shared__ __align__(128) uint8_t scratch[];
-    FinishSmem& fs = *reinterpret_cast<FinishSmem*>(scratch);
-    uint32_t* ssum = reinterpret_cast<uint32_t*>(scratch + ((sizeof(FinishSmem) + 127) / 128) * 128);
+// Finish strip s of scan `scan_no` (run by the CTA whose segment arrived last):
+// counts, K3 stitch, flags, boundary compaction, totals.  One batch of loads
+// (the k segment partials of the strip, their links and K3 summaries, all in
+// flight together), one release of the strip record (flags strictly inside the
+// strip + counts of its first and last column), one warp-parallel acquire of
+// every record to the left -- from which the boundary offset AND this strip's
+// first-column flag (counts[c0] vs counts[c0-1], runscan.cpp:147) follow -- then
+// fire-and-forget writes.  Records are double-buffered by scan parity (rewritten
+// only once the scan two back is done); only the output writes wait for the
+// previous scan's finishers (the outputs are shared by consecutive scans).
+template <bool kLinks, int NW>
+__device__ void finish_strip(const ScanParams& prm, int s, unsigned long long scan_no, uint8_t* scratch) {
+    constexpr int T = NW * 32;
+    FinishSmem<NW>& fs = *reinterpret_cast<FinishSmem<NW>*>(scratch);
+    uint32_t* ssum = reinterpret_cast<uint32_t*>(scratch + ((sizeof(FinishSmem<NW>) + 127) / 128) * 128);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int s = blockIdx.x;
     const int k = prm.seg_per_strip;
     const int g0 = s * k;
+    const int S = prm.n_strips;
     constexpr int kSumWords = kSumPlanes * 32;
-
-    // (0) this strip's scan number -- taken BEFORE releasing the next scan's
-    // streaming kernel, so tickets follow launch order (a later scan's finisher
-    // can never draw an earlier number) -- then let the next scan launch right
-    // away (it only needs SMs; it waits on fin_loaded before reusing this scan's
-    // workspace), then wait until all k segments of this scan merged.
-    unsigned long long scan_no = 0;
-    if (tid == 0) {
-        scan_no = atomicAdd(prm.fin_ticket + s, 1ull);
-        fs.base = static_cast<long long>(scan_no);
-    }
-    __syncthreads();
-    asm volatile("griddepcontrol.launch_dependents;");
-    scan_no = static_cast<unsigned long long>(fs.base);
+    constexpr int kSumVec = kSumWords / 4;  // uint4 per summary
     const uint32_t epoch = static_cast<uint32_t>(scan_no % 4095ull) + 1u;
-    const int ring = static_cast<int>(scan_no & 3ull);
-    if (tid == 0) YCHG_STAMP_AT(16, scan_no + 1);
-    // Segment partials are double-buffered by scan parity (the next scan's
-    // stream kernel writes the other half while this finisher reads).
     const int64_t par = static_cast<int64_t>(scan_no & 1ull);
     const int64_t G = prm.n_segments;
-    const uint32_t* part_p = prm.part + par * G * 512;
-    const uint32_t* sums_p = prm.sums + par * G * kSumWords;
-    const unsigned long long* seglinks_p = prm.seg_links + par * G;
-    const unsigned long long* segstat_p = prm.seg_status + par * G;
-    if (warp == 0) {
-        unsigned long long sl = 0;
-        for (int jb = 0; jb < k; jb += 32) {
-            const int j = jb + lane;
-            const bool act = j < k;
-            bool ok = !act;
-            while (true) {
-                if (!ok) ok = static_cast<uint32_t>(ld_acquire(segstat_p + g0 + (act ? j : 0))) == epoch;
-                if (__all_sync(0xFFFFFFFFu, ok)) break;
-            }
-            // every per-segment input must be read before fin_loaded releases this
-            // half to scan t+2 -- including the segment link counts
-            if (kLinks && act) sl += __ldcg(seglinks_p + g0 + j);
+    const uint32_t* part_p = prm.part + (par * G + g0) * 512;
+    const uint32_t* sums_p = prm.sums + (par * G + g0) * kSumWords;
+    StripRecord* recs = prm.rec + par * S;
+    if (tid == 0) {
+        stamp(prm, scan_no, 3, globaltimer());
+        stamp(prm, scan_no, 9, scan_no + 1);
+    }
+
+    // (1) one batch of loads: the k partials (128 uint4 each; thread t sums uint4 t
+    //     of every segment, kB segments in flight at once), the first chunk of K3
+    //     summaries (straight to smem) and the segment links; tid 0 also reads the
+    //     finish counter for the two waits below, overlapped with the batch.
+    static_assert(T == 128 || T == 256, "partial layout: 512 words over the CTA");
+    constexpr int kWPT = 512 / T;  // partial words per thread (one 16 B / 8 B load per segment)
+    using VecT = typename std::conditional<kWPT == 4, uint4, uint2>::type;
+    constexpr int kB = 8;          // segments per load batch
+    constexpr int kSV = (kFinishChunk * kSumVec + T - 1) / T;  // uint4 of the summary chunk per thread
+    uint32_t lo[kWPT], hi[kWPT];
+#pragma unroll
+    for (int q = 0; q < kWPT; ++q) lo[q] = hi[q] = 0;
+    const int n0 = k < kFinishChunk ? k : kFinishChunk;
+    uint4 sv[kSV];
+    if (kLinks) {  // all of the chunk's loads in flight before the first use
+        const uint4* src = reinterpret_cast<const uint4*>(sums_p);
+#pragma unroll
+        for (int r = 0; r < kSV; ++r) {
+            const int i = tid + r * T;
+            sv[r] = i < n0 * kSumVec ? __ldcg(src + i) : make_uint4(0u, 0u, 0u, 0u);
         }
+    }
+    unsigned long long sl = 0;
+    if (kLinks && warp == 0)
+        for (int j = lane; j < k; j += 32) sl += __ldcg(prm.seg_links + par * G + g0 + j);
+    const VecT* pv = reinterpret_cast<const VecT*>(part_p);
+    for (int g = 0; g < k; g += kB) {
+        VecT x[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) x[u] = (g + u < k) ? __ldcg(pv + (g + u) * T + tid) : VecT{};
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(&x[u]);
+#pragma unroll
+            for (int q = 0; q < kWPT; ++q) {
+                lo[q] += w[q] & 0xFFFFu;
+                hi[q] += w[q] >> 16;
+            }
+        }
+    }
+    if (kLinks) {
+#pragma unroll
+        for (int r = 0; r < kSV; ++r) {
+            const int i = tid + r * T;
+            if (i < n0 * kSumVec) reinterpret_cast<uint4*>(ssum)[i] = sv[r];
+        }
+    }
+    unsigned long long fa = 0;
+    if (tid == 0) fa = ld_acquire(prm.fin_all);
+    if (kLinks && warp == 0) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sl += __shfl_xor_sync(0xFFFFFFFFu, sl, o);
         if (lane == 0) fs.seglinks = sl;
     }
-    __syncthreads();
-    if (tid == 0) {
-        YCHG_STAMP(21);
-        YCHG_STAMP_AT(30, scan_no + 1);  // identity stamps: scan number (+1) at each stage
-    }
-
-    // (1) one batch of loads per 8 segments: partial counts (512 u16x2 words per
-    //     segment over the CTA) and the K3 summaries (8 x 224 words).
-    constexpr int kR = (512 + kThreads - 1) / kThreads;
-    constexpr int kY = (8 * kSumWords + kThreads - 1) / kThreads;
-    // Per-segment partials are u16x2 words (a segment has <= 65504 rows, so a
-    // column's count in it fits 16 bits); the strip total needs up to 21 bits
-    // (height < 2^22), so the two halves are summed separately.
-    uint32_t v[kR], vh[kR];
+    // partial word idx = 32 i + ln holds the u16 counters of columns 32 ln + acc_column(i, 0 / 1)
 #pragma unroll
-    for (int r = 0; r < kR; ++r) v[r] = vh[r] = 0;
-    for (int g = 0; g < k; g += 8) {
-        const int n = k - g < 8 ? k - g : 8;
-        uint32_t x[kR][8], y[kY];
-        const uint32_t* src = part_p + static_cast<int64_t>(g0 + g) * 512;
-#pragma unroll
-        for (int r = 0; r < kR; ++r) {
-            const int idx = tid + r * kThreads;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) x[r][u] = (u < n && idx < 512) ? __ldcg(src + u * 512 + idx) : 0u;
-        }
-        const uint32_t* ss = sums_p + static_cast<int64_t>(g0 + g) * kSumWords;
-        if (kLinks) {
-#pragma unroll
-            for (int u = 0; u < kY; ++u) {
-                const int i = tid + u * kThreads;
-                y[u] = i < n * kSumWords ? __ldcg(ss + i) : 0u;
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < kR; ++r)
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                v[r] += x[r][u] & 0xFFFFu;
-                vh[r] += x[r][u] >> 16;
-            }
-        if (kLinks) {
-#pragma unroll
-            for (int u = 0; u < kY; ++u) {
-                const int i = tid + u * kThreads;
-                if (i < n * kSumWords) ssum[g * kSumWords + i] = y[u];
-            }
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < kR; ++r) {
-        const int idx = tid + r * kThreads;
-        if (idx < 512) {
-            const int i = idx >> 5, ln = idx & 31;
-            fs.sc[32 * ln + acc_column<kLinks>(i, 0)] = static_cast<int32_t>(v[r]);
-            fs.sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(vh[r]);
-        }
+    for (int q = 0; q < kWPT; ++q) {
+        const int idx = kWPT * tid + q;
+        const int i = idx >> 5, ln = idx & 31;
+        fs.sc[32 * ln + acc_column<kLinks>(i, 0)] = static_cast<int32_t>(lo[q]);
+        fs.sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(hi[q]);
     }
     __syncthreads();
-    if (tid == 0) {
-        YCHG_STAMP(24);
-        YCHG_STAMP_AT(31, scan_no + 1);
-        // this scan's workspace for strip s is in smem: the next scan's stream
-        // kernel may overwrite it (it waits on this before its first partial write)
-        st_release(prm.fin_loaded + par * prm.n_strips + s, scan_no + 1);
+    if (tid == 0 && k <= kFinishChunk) {
+        // every input of this half is read: scan t+2 may overwrite it
+        st_release(prm.fin_loaded + par * S + s, scan_no + 1);
     }
+    if (tid == 0) stamp(prm, scan_no, 16, globaltimer());
 
-    // (2) flags strictly inside the strip (columns 1..1023), counts out, run total
+    // (2) flags strictly inside the strip (columns 1..1023), run total
     const int nwords = (prm.width_cnt + 31) >> 5;
     long long local_sum = 0;
-    for (int wi = warp; wi < kStripWords; wi += kWarps) {
+    for (int wi = warp; wi < kStripWords; wi += NW) {
         const int col = wi * 32 + lane;
         const int gc = s * kStripCols + col;
         const bool valid = gc < prm.width_cnt;
@@ -454,22 +498,18 @@ ychg_finish_kernel(const ScanParams prm) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local_sum += __shfl_xor_sync(0xFFFFFFFFu, local_sum, o);
     if (lane == 0) fs.red[warp] = local_sum;
-    __syncthreads();
-
-    // Strip records and the outputs are shared by consecutive scans: every
-    // finisher of the previous scan must be done before this one publishes or
-    // writes anything (normally long done by now).
-    if (tid == 0 && scan_no > 0) {
-        const unsigned long long need = scan_no * static_cast<unsigned long long>(prm.n_strips);
-        YCHG_STAMP_AT(28, scan_no);
-        while (ld_acquire(prm.fin_all) < need) {
-        }
-        YCHG_STAMP(29);
-        YCHG_STAMP_AT(19, scan_no + 1);
+    // This parity's records (status and tstat/runs/links) were last read by the
+    // scan two back: its finishers must all be done before any of them is
+    // rewritten (normally long ago).
+    if (tid == 0 && scan_no >= 2) {
+        const unsigned long long need = (scan_no - 1) * static_cast<unsigned long long>(S);
+        while (fa < need) fa = ld_acquire(prm.fin_all);
     }
     __syncthreads();
-    const bool last_strip = (s == prm.n_strips - 1);
-    StripRecord* rec = prm.rec + s;
+    if (tid == 0) stamp(prm, scan_no, 17, globaltimer());
+
+    const bool last_strip = (s == S - 1);
+    StripRecord* rec = recs + s;
     int inside = 0;
     const int32_t first = fs.sc[0];
     if (warp == 0) {
@@ -485,28 +525,69 @@ ychg_finish_kernel(const ScanParams prm) {
         inside = __shfl_sync(0xFFFFFFFFu, incl, 31);
         if (lane == 0) st_release(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
     }
-    // (2b) K3: stitch the strip's segment summaries top to bottom (tree, all warps)
+    // The look-back's first loads (records of up to 32 strips to the left) go out
+    // now and land while the K3 summaries are composed.  A record is one packed
+    // word validated by its epoch, so relaxed loads suffice.
+    unsigned long long lb = 0;
+    if (warp == 0 && lane < s) lb = ld_relaxed(&recs[lane].status);
+    // (2b) K3: stitch the strip's segment summaries top to bottom, kFinishChunk at
+    // a time (warp 0 carries the running composite between chunks); strip_links
+    // is complete in warp 0
     unsigned long long strip_links = 0;
     if (kLinks) {
-        strip_links = tree_compose<kWarps>(ssum, k, reinterpret_cast<unsigned long long*>(fs.red2));
-        if (tid == 0) YCHG_STAMP(26);
-        if (warp == 1) {
-            // close whatever is still open at row H (virtual background row)
-            unsigned long long c = __popc(ssum[4 * 32 + lane] & ssum[5 * 32 + lane] & ~ssum[6 * 32 + lane]);
+        unsigned long long jl = 0;
+        BandSummary R = chain_compose<NW>(ssum, n0, fs.red2, jl);
+        strip_links = jl;
+        for (int c0 = n0; c0 < k; c0 += kFinishChunk) {
+            const int n = k - c0 < kFinishChunk ? k - c0 : kFinishChunk;
+            __syncthreads();  // the previous chain_compose's readers are done
+            const uint4* src = reinterpret_cast<const uint4*>(sums_p + static_cast<int64_t>(c0) * kSumWords);
+            for (int i = tid; i < n * kSumVec; i += T) reinterpret_cast<uint4*>(ssum)[i] = __ldcg(src + i);
+            __syncthreads();
+            const BandSummary B = chain_compose<NW>(ssum, n, fs.red2, jl);
+            if (warp == 0) {
+                BandSummary C;
+                unsigned long long m = __popc(compose_summary(R, B, C));
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-            strip_links += c;
+                for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xFFFFFFFFu, m, o);
+                strip_links += jl + m;
+                R = C;
+            }
+        }
+        if (warp == 0) {
+            // close whatever is still open at row H (virtual background row)
+            unsigned long long m = __popc(R.OE & R.T2 & ~R.T3);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xFFFFFFFFu, m, o);
+            strip_links += m;
         }
     }
+    if (tid == 0 && k > kFinishChunk) st_release(prm.fin_loaded + par * S + s, scan_no + 1);
+    if (tid == 0) stamp(prm, scan_no, 18, globaltimer());
 
     if (warp == 0) {
-        // (4) acquire every record to the left: boundary offset + this strip's first-column flag
+        // (4) release (runs, links) for the totals, then acquire every record to
+        // the left: boundary offset + this strip's first-column flag
+        if (lane == 0) {
+            long long runs = 0;
+            for (int w = 0; w < NW; ++w) runs += fs.red[w];
+            rec->runs = runs;
+            rec->links = static_cast<long long>(strip_links + (kLinks ? fs.seglinks : 0ull));
+            st_release(&rec->tstat, static_cast<unsigned long long>(epoch));
+        }
         long long off = 0;
         int32_t carry_last = 0;  // last(j-1) entering each chunk; last(-1) := 0
         for (int jb = 0; jb < s; jb += 32) {
             const int j = jb + lane;
             const bool act = j < s;
-            const unsigned long long st = warp_wait_epoch12(&prm.rec[act ? j : 0].status, act, epoch);
+            unsigned long long st = jb == 0 ? lb : 0ull;
+            bool ok = !act || (jb == 0 && static_cast<uint32_t>(lb >> 52) == (epoch & 0xFFFu));
+            while (!__all_sync(0xFFFFFFFFu, ok)) {
+                if (!ok) {
+                    st = ld_relaxed(&recs[j].status);
+                    ok = static_cast<uint32_t>(st >> 52) == (epoch & 0xFFFu);
+                }
+            }
             const int32_t fj = static_cast<int32_t>((st >> 21) & 0x1FFFFFu);
             const int32_t lj = static_cast<int32_t>(st & 0x1FFFFFu);
             int32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, lj, 1);
@@ -517,37 +598,28 @@ ychg_finish_kernel(const ScanParams prm) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
         if (lane == 0) {
-            YCHG_STAMP(27);
-            YCHG_STAMP_AT(18, scan_no + 1);
+            stamp(prm, scan_no, 19, globaltimer());
             fs.edge = (first != carry_last) ? 1u : 0u;
             fs.base = off;
-            if (last_strip) prm.totals[3] = off + fs.edge + inside;
-        }
-    } else if (warp == 1) {
-        // (4) release (runs, links) for the totals
-        const unsigned long long links = strip_links;
-        const unsigned long long sl = fs.seglinks;  // read before fin_loaded was released
-        if (lane == 0) {
-            long long runs = 0;
-            for (int w = 0; w < kWarps; ++w) runs += fs.red[w];
-            rec->runs = runs;
-            rec->links = static_cast<long long>(links + sl);
-            st_release(&rec->tstat, static_cast<unsigned long long>(epoch));
-        }
-    } else {
-        // counts out (fire and forget)
-        for (int col = tid - 64; col < kStripCols; col += kThreads - 64) {
-            const int gc = s * kStripCols + col;
-            if (gc < prm.width_cnt) prm.counts[gc] = fs.sc[col];
+            fs.n_total = off + static_cast<long long>(first != carry_last) + inside;
         }
     }
+    // (5) the outputs are shared with the previous scan: its finishers must be done
+    if (tid == 0 && scan_no >= 1) {
+        const unsigned long long need = scan_no * static_cast<unsigned long long>(S);
+        while (fa < need) fa = ld_acquire(prm.fin_all);
+    }
     __syncthreads();
-    if (tid == 0) YCHG_STAMP(25);
-
-    // (5) flags out + ordered compaction (the first-column flag, if set, comes first)
+    if (tid == 0) stamp(prm, scan_no, 20, globaltimer());
+    if (tid == 0 && last_strip) prm.totals[3] = fs.n_total;
+    for (int col = tid; col < kStripCols; col += T) {
+        const int gc = s * kStripCols + col;
+        if (gc < prm.width_cnt) prm.counts[gc] = fs.sc[col];
+    }
+    // flags out + ordered compaction (the first-column flag, if set, comes first)
     const uint32_t e = fs.edge;
     if (tid == 0 && e) prm.boundaries[fs.base] = s * kStripCols;
-    for (int wi = warp; wi < kStripWords; wi += kWarps) {
+    for (int wi = warp; wi < kStripWords; wi += NW) {
         const int w = s * kStripWords + wi;
         const uint32_t m = fs.fw[wi];
         if (lane == 0 && w < nwords) prm.flags[w] = m | (wi == 0 ? e : 0u);
@@ -558,21 +630,21 @@ ychg_finish_kernel(const ScanParams prm) {
     // (6) the right-most strip also writes run/link totals once every strip released them
     if (last_strip && warp == 0) {
         long long runs = 0, links = 0;
-        for (int jb = 0; jb < prm.n_strips; jb += 32) {
+        for (int jb = 0; jb < S; jb += 32) {
             const int j = jb + lane;
-            const bool act = j < prm.n_strips;
-            unsigned long long v = 0;
+            const bool act = j < S;
+            unsigned long long vv = 0;
             bool ok = !act;
             while (true) {
                 if (!ok) {
-                    v = ld_acquire(&prm.rec[j].tstat);
-                    ok = static_cast<uint32_t>(v) == epoch;
+                    vv = ld_acquire(&recs[j].tstat);
+                    ok = static_cast<uint32_t>(vv) == epoch;
                 }
                 if (__all_sync(0xFFFFFFFFu, ok)) break;
             }
             if (act) {
-                runs += __ldcg(&prm.rec[j].runs);
-                links += __ldcg(&prm.rec[j].links);
+                runs += __ldcg(&recs[j].runs);
+                links += __ldcg(&recs[j].links);
             }
         }
 #pragma unroll
@@ -586,83 +658,113 @@ ychg_finish_kernel(const ScanParams prm) {
             prm.totals[2] = kLinks ? runs - links : -1;
         }
     }
+    if (tid == 0) stamp(prm, scan_no, 21, globaltimer());
     __syncthreads();
     if (tid == 0) {
-        YCHG_STAMP(22);
-        YCHG_STAMP_AT(17, scan_no + 1);
+        stamp(prm, scan_no, 4, globaltimer());
+        stamp(prm, scan_no, 10, scan_no + 1);
         __threadfence();
         atomicAdd(prm.fin_all, 1ull);
     }
 }
 
 // ----------------------------------------------------------------------------
+// Row-block range [wb0, wb0 + nb) of warp `warp`'s band in segment `seg`.
+template <int NW>
+__device__ __forceinline__ void band_of(const ScanParams& prm, int seg, int warp, int& strip, int& nseg, int& wb0,
+                                        int& nb) {
+    const int k = prm.seg_per_strip;
+    strip = seg / k;
+    const int j = seg - strip * k;
+    const int sb0 = seg_first_block(j, k, prm.n_blocks);
+    nseg = seg_first_block(j + 1, k, prm.n_blocks) - sb0;
+    wb0 = sb0 + (warp * nseg) / NW;
+    nb = sb0 + ((warp + 1) * nseg) / NW - wb0;
+}
+
+// Lane 0: fill the first stages of the warp's TMA ring for a band.
+template <int kS>
+__device__ __forceinline__ void kick_ring(const CUtensorMap* tmap, uint8_t* my_stages, uint64_t* my_bars,
+                                          uint32_t it, int x0, int wb0, int nb) {
+    const int npre = nb < kS ? nb : kS;
+    for (int i = 0; i < npre; ++i) {
+        const int st = (it + i) % kS;
+        mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
+        tma_load_2d(my_stages + st * kStageBytes, tmap, &my_bars[st], x0, (wb0 + i) * kBlockRows);
+    }
+}
+
 template <bool kLinks, int NW = scan_warps<kLinks>()>
 __global__ void __launch_bounds__(NW * 32, 1)
 ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm) {
     constexpr int kS = scan_stages<kLinks>();  // TMA ring depth of this path
+    constexpr int T = NW * 32;
     using L = ScanSmem<NW, kS>;
+    static_assert(finish_smem_bytes<NW>() <= L::kStagesB, "strip finish scratch must fit in the TMA ring");
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stages = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kStagesB);
     uint32_t* accs = reinterpret_cast<uint32_t*>(smem + L::kStagesB + L::kBar);
     uint32_t* sums = accs + NW * 16 * 32;
     unsigned long long* wlinks = reinterpret_cast<unsigned long long*>(sums + NW * kSumPlanes * 32);
-    int* misc = reinterpret_cast<int*>(wlinks + 2 * NW);  // [0..W) warp empty, [W+1] epoch, [W+2] scan index
+    int* misc = reinterpret_cast<int*>(wlinks + 2 * NW);  // [0] last-arrival flag
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
-
-    // This CTA's scan number for each of its segments, drawn BEFORE releasing the
-    // finisher (and, through it, the next scan): tickets then follow launch order
-    // even when consecutive scans' CTAs overlap.
-    __shared__ unsigned long long seg_tick[kMaxSegPerCta];
     const unsigned long long t_entry = globaltimer();
+    uint8_t* my_stages = stages + warp * kS * kStageBytes;
+    uint64_t* my_bars = bars + warp * kS;
+    const bool have_seg = static_cast<int>(blockIdx.x) < prm.n_segments;
+
+    // Each warp owns its ring: lane 0 initialises the warp's barriers and -- unless
+    // the image is still being written by the preceding kernel -- starts the first
+    // band's loads right away, so the TMA round trip overlaps the ticket draw.
+    if (lane == 0) {
+        for (int i = 0; i < kS; ++i) mbar_init(&my_bars[i], 1);
+        fence_proxy_async();
+        if (have_seg && !prm.wait_inputs) {
+            int strip, nseg, wb0, nb;
+            band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
+            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb);
+        }
+    }
+    // This CTA's scan number for each of its segments, drawn BEFORE triggering the
+    // next scan's launch: tickets then follow launch order even when consecutive
+    // scans' CTAs overlap.
+    __shared__ unsigned long long seg_tick[kMaxSegPerCta];
     if (tid == 0) {
-        for (int i = 0; i < NW * kS; ++i) mbar_init(&bars[i], 1);
         int i = 0;
         for (int sg = blockIdx.x; sg < prm.n_segments && i < kMaxSegPerCta; sg += gridDim.x, ++i)
             seg_tick[i] = atomicAdd(prm.seg_ticket + sg, 1ull);
     }
-    fence_proxy_async();
     __syncthreads();
-    // Let this scan's finisher kernel launch now: its CTAs are small, co-reside
-    // with ours and wait on the per-segment flags (programmatic dependent launch).
+    // Let the next scan launch now: its CTAs take SM slots as ours retire.
     asm volatile("griddepcontrol.launch_dependents;");
-    // The streaming kernel is a programmatic dependent of whatever kernel precedes
-    // it on the stream.  Back-to-back scans need no wait (the image was written
-    // before the previous scan's finisher ran); a plan whose image is written by
-    // the immediately preceding kernel (host path: re-pitch / PNM pack) waits for
-    // that grid's completion and memory flush here.
-    if (prm.wait_inputs) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // A plan whose image is written by the immediately preceding kernel (host
+    // path: re-pitch / PNM pack) waits for that grid's completion and memory
+    // flush before its first load; back-to-back scans read images written long before.
+    if (prm.wait_inputs) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lane == 0 && have_seg) {
+            int strip, nseg, wb0, nb;
+            band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
+            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb);
+        }
+    }
+    if (tid == 0 && have_seg) stamp(prm, seg_tick[0], 0, t_entry);
 
-    uint8_t* my_stages = stages + warp * kS * kStageBytes;
-    uint64_t* my_bars = bars + warp * kS;
     uint32_t it = 0;  // blocks consumed by this warp so far (stage = it % kS)
+    const Muls mu{prm.mul2, prm.mulnb, prm.mul1, prm.mulm1};
 
-    const int k = prm.seg_per_strip;
     int seg_i = 0;
     for (int seg = blockIdx.x; seg < prm.n_segments; seg += gridDim.x, ++seg_i) {
-        const int strip = seg / k;
-        const int j = seg - strip * k;
-        const int sb0 = seg_first_block(j, k, prm.n_blocks);
-        const int sb1 = seg_first_block(j + 1, k, prm.n_blocks);
-        const int nseg = sb1 - sb0;
-        const int wb0 = sb0 + (warp * nseg) / NW;
-        const int wb1 = sb0 + ((warp + 1) * nseg) / NW;
-        const int nb = wb1 - wb0;
+        int strip, nseg, wb0, nb;
+        band_of<NW>(prm, seg, warp, strip, nseg, wb0, nb);
         const int x0 = strip * kStripBytes;
         const int gw = strip * kStripWords + lane;
+        const unsigned long long scan_idx = seg_tick[seg_i];
 
-        // this segment's scan number (agrees with the finisher's strip ticket)
-        if (tid == 0) {
-            const unsigned long long t = seg_tick[seg_i];
-            misc[NW + 1] = static_cast<int>(t % 4095ull) + 1;
-            misc[NW + 2] = static_cast<int>(t);  // scans before this one (< 2^31 per plan)
-            const int ring = static_cast<int>(t & 3ull);
-            YCHG_STAMP_AT(0, t_entry);
-            YCHG_STAMP_AT(15, t + 1);
-        }
         LaneState s;
         s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
 #pragma unroll
@@ -672,20 +774,11 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         const bool full = !kLinks || __all_sync(0xFFFFFFFFu, s.mk3 == 0xFFFFFFFFu);
         s.h1 = s.h2 = 0;
         s.links = 0;
-        s.pa = s.pb = s.pab = 0;
+        s.pa = s.pb = s.pab = s.praw = 0;
         uint32_t O = 0;
 
         if (nb > 0) {
-            // Kick off the ring first so the halo-row load overlaps it.
-            if (lane == 0) {
-                const int npre = nb < kS ? nb : kS;
-                for (int i = 0; i < npre; ++i) {
-                    const int st = (it + i) % kS;
-                    mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
-                    tma_load_2d(my_stages + st * kStageBytes, &tmap, &my_bars[st], x0,
-                                (wb0 + i) * kBlockRows);
-                }
-            }
+            if (seg_i > 0 && lane == 0) kick_ring<kS>(&tmap, my_stages, my_bars, it, x0, wb0, nb);
             // Halo row y0-1 (the reference's prev row, runscan.cpp:45; zero above row 0).
             const int y0 = wb0 * kBlockRows;
             uint32_t raw = 0, nbyte = 0;
@@ -697,7 +790,9 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                     if (c + q < prm.row_bytes) raw |= static_cast<uint32_t>(__ldg(row + c + q)) << (8 * q);
                 if (c + 4 < prm.row_bytes) nbyte = __ldg(row + c + 4);
             }
-            s.pa = kLinks ? __byte_perm(raw, 0u, 0x0123u) : raw;  // word order of process_block<kLinks>
+            s.praw = raw;
+            uint32_t phalo = __shfl_sync(0xFFFFFFFFu, nbyte, 31);  // right-halo byte of the row above
+            s.pa = kLinks ? __byte_perm(raw, 0u, 0x0123u) : raw;     // word order of process_block<kLinks>
             s.pb = right_neighbour_msb(s.pa, nbyte, prm.mul2, prm.mulnb);
             O = kLinks ? (s.pa | s.pb) : 0u;
             s.Hd = O;
@@ -707,34 +802,30 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             int since_flush = 0;
             for (int bi = 0; bi < nb; ++bi) {
                 const int st = it % kS;
-#ifdef YCHG_COMPUTE_ONLY  // diagnostics build: reuse the first kS blocks, no TMA after the fill
-                if (bi < kS) mbar_wait(&my_bars[st], (it / kS) & 1u);
-#else
                 mbar_wait(&my_bars[st], (it / kS) & 1u);
-#endif
+                if (bi == 0 && tid == 0 && seg_i == 0) stamp(prm, scan_idx, 6, globaltimer());
                 const uint8_t* sp = my_stages + st * kStageBytes;
+                const bool skip = kLinks && prm.skip_same && block_unchanged(sp, lane, s.praw, phalo);
+                if (!skip) {
 #ifdef YCHG_NO_HEAD  // diagnostics build: never take the head-mode block (wrong results, timing only)
-                if (false)
+                    if (false)
 #else
-                if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u))
+                    if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u))
 #endif
-                {
-                    if (full) process_block<kLinks, true, kLinks, false>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
-                    else process_block<kLinks, true, kLinks, true>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
-                } else {
-                    if (full) process_block<kLinks, false, kLinks, false>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
-                    else process_block<kLinks, false, kLinks, true>(sp, lane, s, prm.mul2, prm.mulnb, prm.mul1);
+                    {
+                        if (full) process_block<kLinks, true, false>(sp, lane, s, mu);
+                        else process_block<kLinks, true, true>(sp, lane, s, mu);
+                    } else {
+                        if (full) process_block<kLinks, false, false>(sp, lane, s, mu);
+                        else process_block<kLinks, false, true>(sp, lane, s, mu);
+                    }
+                    if (kLinks && prm.skip_same) phalo = sp[31 * kBoxBytes + kStripBytes];
                 }
                 __syncwarp();
-#ifdef YCHG_COMPUTE_ONLY
-                if (false) {
-#else
                 if (lane == 0 && bi + kS < nb) {
-#endif
                     fence_proxy_async();
                     mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
-                    tma_load_2d(my_stages + st * kStageBytes, &tmap, &my_bars[st], x0,
-                                (wb0 + bi + kS) * kBlockRows);
+                    tma_load_2d(my_stages + st * kStageBytes, &tmap, &my_bars[st], x0, (wb0 + bi + kS) * kBlockRows);
                 }
                 ++it;
                 if (++since_flush == kFlushBlocks) {
@@ -743,6 +834,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
                 }
             }
             flush_counts(s);
+            if (tid == 0 && seg_i == 0) stamp(prm, scan_idx, 7, globaltimer());
 
             if (kLinks) {
                 const uint32_t m = s.mk3;
@@ -767,32 +859,19 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         uint32_t* wa = accs + warp * 16 * 32;
 #pragma unroll
         for (int i = 0; i < 16; ++i) wa[i * 32 + lane] = s.acc[i];
-        if (lane == 0) {
-            misc[warp] = (nb == 0);
-            const int ring = misc[NW + 2] & 3;
-            if (warp < 16) YCHG_STAMP(1 + warp);
-        }
-        __syncthreads();
 
         // ---- partials are double-buffered by scan parity: the finisher of the scan
-        // two back (same half) must have loaded this strip before we overwrite it
-        const unsigned long long scan_idx = static_cast<unsigned long long>(misc[NW + 2]);
+        // two back (same half) must have loaded this strip's before we overwrite them
         const int64_t par = static_cast<int64_t>(scan_idx & 1ull);
         if (tid == 0 && scan_idx >= 2) {
-            const int ring = static_cast<int>(scan_idx & 3ull);
-            YCHG_STAMP_AT(9, scan_idx);
-            YCHG_STAMP(10);
-            // per half: the NEXT scan's finisher (other half) may load first, so a
-            // single per-strip counter could release us before scan_idx-2's
-            // finisher has read this half (then its flags would be overwritten).
             while (ld_acquire(prm.fin_loaded + par * prm.n_strips + strip) < scan_idx - 1) {
             }
-            YCHG_STAMP(11);
-            YCHG_STAMP_AT(12, scan_idx + 1);
         }
         __syncthreads();
-        // ---- CTA merge: counts (sum over warps, coalesced u16x2 words), K3 (compose in row order).
-        for (int idx = tid; idx < 16 * 32; idx += (NW * 32)) {
+        if (tid == 0 && seg_i == 0) stamp(prm, scan_idx, 1, globaltimer());
+        // ---- CTA merge: counts (sum over warps, one coalesced 2 KB partial of u16x2
+        // words per segment), K3 (compose the warps' band summaries in row order).
+        for (int idx = tid; idx < 16 * 32; idx += T) {
             uint32_t v = 0;
 #pragma unroll
             for (int w = 0; w < NW; ++w) v += accs[w * 16 * 32 + idx];
@@ -802,33 +881,36 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             // non-empty warp bands were written to consecutive slots (row order)
             int nfull = 0;
             for (int w = 0; w < NW; ++w) nfull += ((w + 1) * nseg) / NW > (w * nseg) / NW;
-            const unsigned long long jl = tree_compose<NW>(sums, nfull, wlinks + NW);
+            unsigned long long jl = 0;
+            const BandSummary C = chain_compose<NW>(sums, nfull, wlinks + NW, jl);  // (contains __syncthreads)
             if (warp == 0) {
                 unsigned long long links = lane < NW ? wlinks[lane] : 0ull;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
                 uint32_t* gs = prm.sums + (par * prm.n_segments + seg) * kSumPlanes * 32;
-#pragma unroll
-                for (int q = 0; q < kSumPlanes; ++q) gs[q * 32 + lane] = sums[q * 32 + lane];
+                store_summary(gs, lane, C);
                 if (lane == 0) prm.seg_links[par * prm.n_segments + seg] = links + jl;
             }
         }
-        // ---- publish the segment: the barrier orders every thread's partial
-        // writes before tid 0's release store of the epoch-tagged flag.
+        // ---- arrive on the strip: the barrier orders every thread's partial
+        // writes before tid 0's release; the last of the k arrivals acquires them all.
         __syncthreads();
         if (tid == 0) {
-            const int ring = misc[NW + 2] & 3;
-            YCHG_STAMP(20);
-            YCHG_STAMP_AT(13, static_cast<unsigned long long>(misc[NW + 2]) + 1);
-            st_release(prm.seg_status + par * prm.n_segments + seg, static_cast<unsigned long long>(misc[NW + 1]));
+            if (seg_i == 0) stamp(prm, scan_idx, 2, globaltimer());
+            const unsigned long long old = atom_add_acq_rel(prm.arrive + par * prm.n_strips + strip, 1ull);
+            misc[0] = ((old + 1ull) % static_cast<unsigned long long>(prm.seg_per_strip)) == 0ull;
+            stamp(prm, scan_idx, 8, scan_idx + 1);
+            stamp(prm, scan_idx, 14, old + 1);
+            stamp(prm, scan_idx, 15, static_cast<unsigned long long>(seg) + 1);
         }
         __syncthreads();
+        if (misc[0]) finish_strip<kLinks, NW>(prm, strip, scan_idx, stages);
+        // the merge / finish used the TMA ring as scratch (generic writes): order
+        // them before the async-proxy writes of the next segment's loads
+        fence_proxy_async();
+        __syncthreads();
     }
-    if (tid == 0 && prm.n_segments > 0) {
-        const int ring = misc[NW + 2] & 3;
-        YCHG_STAMP(23);
-        YCHG_STAMP_AT(14, static_cast<unsigned long long>(misc[NW + 2]) + 1);
-    }
+    if (tid == 0 && have_seg) stamp(prm, seg_tick[0], 5, globaltimer());
 }
 
 }  // namespace ychg_dev
@@ -848,9 +930,7 @@ extern "C" void ychg_scan_kernel_shape(int with_links, int* threads, int* smem_b
     *smem_bytes = with_links ? scan_smem<true>() : scan_smem<false>();
 }
 
-constexpr int kFinishSmemMax = 160 * 1024;
-
-// Opt-in to >48 KB dynamic shared memory (per device, all kernels and variants).
+// Opt-in to >48 KB dynamic shared memory (per device, both paths).
 extern "C" int ychg_scan_kernel_prepare(void) {
     static bool done[64] = {};
     int dev = 0;
@@ -861,19 +941,8 @@ extern "C" int ychg_scan_kernel_prepare(void) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(&ychg_scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  scan_smem<false>());
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(&ychg_finish_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kFinishSmemMax);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(&ychg_finish_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kFinishSmemMax);
-    // Same (maximum) shared-memory carveout for every kernel of a scan: an SM only
-    // co-schedules CTAs whose carveout matches, and the finisher must co-reside
-    // with the streaming CTAs it waits on.
-    const void* fns[4] = {reinterpret_cast<const void*>(&ychg_scan_kernel<true>),
-                          reinterpret_cast<const void*>(&ychg_scan_kernel<false>),
-                          reinterpret_cast<const void*>(&ychg_finish_kernel<true>),
-                          reinterpret_cast<const void*>(&ychg_finish_kernel<false>)};
+    const void* fns[2] = {reinterpret_cast<const void*>(&ychg_scan_kernel<true>),
+                          reinterpret_cast<const void*>(&ychg_scan_kernel<false>)};
     for (const void* f : fns)
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -883,21 +952,15 @@ extern "C" int ychg_scan_kernel_prepare(void) {
     return 0;
 }
 
-// Two launches per scan, both programmatic dependent launches: the streaming
-// kernel triggers its finisher at entry (the finisher CTAs are small and wait on
-// per-segment flags while the stream runs), and the finisher triggers the NEXT
-// scan's streaming kernel as soon as it holds this scan's workspace in smem, so
-// back-to-back scans (e.g. one CUDA graph) overlap each finish with the next
-// stream.  Every CTA of the finisher grid waits only on work that is already
-// launched; the streaming kernel never waits.
+// One launch per scan, a programmatic dependent launch: the kernel triggers the
+// next launch at CTA entry, so back-to-back scans (e.g. one CUDA graph) overlap
+// the tail of one scan with the start of the next.
 extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int grid, int with_links,
                                 cudaStream_t stream, cudaEvent_t ev_mid) {
     (void)ev_mid;
     if (const int rc = ychg_scan_kernel_prepare()) return rc;
     const void* fa = with_links ? reinterpret_cast<const void*>(&ychg_scan_kernel<true>)
                                 : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
-    const void* fb = with_links ? reinterpret_cast<const void*>(&ychg_finish_kernel<true>)
-                                : reinterpret_cast<const void*>(&ychg_finish_kernel<false>);
     static const bool no_pdl = [] {
         const char* v = getenv("YCHG_NO_PDL");
         return v && v[0] == '1';
@@ -916,20 +979,6 @@ extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int gri
     ca.stream = stream;
     ca.attrs = attr;
     ca.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelExC(&ca, fa, args_a);
-    if (e != cudaSuccess) return static_cast<int>(e);
-
-    const size_t fsm = ((sizeof(FinishSmem) + 127) / 128) * 128 +
-                       static_cast<size_t>(prm->seg_per_strip) * kSumPlanes * 32 * 4;
-    if (fsm > static_cast<size_t>(kFinishSmemMax)) return static_cast<int>(cudaErrorInvalidValue);
-    void* args_b[1] = {&p};
-    cudaLaunchConfig_t cb{};
-    cb.gridDim = dim3(prm->n_strips);
-    cb.blockDim = dim3(kThreads);
-    cb.dynamicSmemBytes = fsm;
-    cb.stream = stream;
-    cb.attrs = attr;
-    cb.numAttrs = 1;
-    e = cudaLaunchKernelExC(&cb, fb, args_b);
+    const cudaError_t e = cudaLaunchKernelExC(&ca, fa, args_a);
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }

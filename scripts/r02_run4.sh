@@ -1,0 +1,5 @@
+timeout 100 python scripts/stall_probe.py 2000 2000 24 50 | tail -1
+timeout 100 python scripts/stall_probe.py 3100 2600 24 50 | tail -1
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 300 python scripts/pipe_timeline.py 21000 hbands "" 10 7 2>&1 | tail -40
+timeout 300 python scripts/pipe_timeline.py 21000 random 10 2>&1 | tail -10

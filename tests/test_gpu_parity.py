@@ -193,9 +193,9 @@ def test_timing_hooks(gpu):
     plan.set_timing(True)
     plan.scan_device(d.ptr, pitch, dc.ptr, df.ptr, db.ptr, dt.ptr)
     a, b = plan.last_ms()
-    assert a > 0 and b == 0.0  # reported as one scan (stream + finish kernels)
+    assert a > 0 and b == 0.0  # one kernel per scan (the strip finish is fused)
     info = plan.info()
-    assert info.kernels_per_scan == 2 and info.grid >= 1
+    assert info.kernels_per_scan == 1 and info.grid >= 1
 
 
 def test_cxx_dropin_binary(gpu):
@@ -595,3 +595,87 @@ def test_host_path_output_buffers_grow_and_shrink(gpu, orc):
             if links:
                 assert r.hyperedges == orc.hyperedges(bits, W)[0], (W, H)
         assert np.array_equal(y.cut_vertex_counts(img), want_c)
+
+
+def _scan_plan(y, bits, W, H, skip=True, links=True):
+    """One device scan of host rows `bits` through a fresh plan -> (counts, boundaries, totals)."""
+    import torch
+    pitch = y.pitch_for(W)
+    dev = np.zeros((H, pitch), np.uint8)
+    dev[:, : bits.shape[1]] = bits
+    d = torch.from_numpy(dev).cuda()
+    c = torch.full((W,), -7, dtype=torch.int32, device="cuda")
+    f = torch.zeros(W // 32 + 64, dtype=torch.int32, device="cuda")
+    b = torch.full((W,), -7, dtype=torch.int32, device="cuda")
+    t = torch.zeros(4, dtype=torch.int64, device="cuda")
+    plan = y.Plan(W, H, skip=skip)
+    plan.scan_device(d.data_ptr(), pitch, c.data_ptr(), f.data_ptr(), b.data_ptr(), t.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream, links)
+    torch.cuda.synchronize()
+    tt = t.cpu().tolist()
+    plan.close()
+    return c.cpu().numpy(), b.cpu().numpy()[: tt[3]], tt
+
+
+def _row_image(W, H, row_fn):
+    """Rows built column-wise: row_fn(y) -> bool array of W columns."""
+    px = np.stack([row_fn(yy) for yy in range(H)]).astype(np.uint8)
+    return np.packbits(px, axis=1)
+
+
+@pytest.mark.parametrize("case", ["halo_only", "lane_edge", "sparse_rows", "one_pixel", "strip_edge_pair"])
+def test_skip_unchanged_blocks_exact(gpu, orc, case):
+    """The skip of 32-row blocks equal to the row above (default on) must be exact,
+    including changes that only the right-halo bit of lane 31 sees (column 1024k,
+    the next strip's first column), changes at lane (32-column) edges, and single
+    changed pixels; compared with the oracle and with YCHG_PLAN_NO_SKIP."""
+    y = gpu
+    W, H = 3100, 2100
+    rng = np.random.default_rng(hash(case) & 0xFFFF)
+    base = rng.random(W) < 0.5
+    if case == "halo_only":          # only columns 1024 and 2048 ever change
+        toggles = set(int(v) for v in rng.integers(0, H, 120))
+        state = {1024: False, 2048: True}
+        rows = []
+        for yy in range(H):
+            if yy in toggles:
+                for c in state:
+                    state[c] = not state[c]
+            r = base.copy()
+            for c, v in state.items():
+                r[c] = v
+            rows.append(r)
+        bits = np.packbits(np.stack(rows).astype(np.uint8), axis=1)
+    elif case == "lane_edge":        # only columns 31/32 and 1023 change, at random rows
+        cols = [31, 32, 1023]
+        bits = _row_image(W, H, lambda yy: np.where(np.isin(np.arange(W), cols), (yy * 7919 % 97) < 40, base))
+    elif case == "sparse_rows":      # a handful of changing rows, everything else constant
+        change = set(int(v) for v in rng.integers(0, H, 9))
+        rows, cur = [], base.copy()
+        for yy in range(H):
+            if yy in change:
+                cur = rng.random(W) < 0.5
+            rows.append(cur.copy())
+        bits = np.packbits(np.stack(rows).astype(np.uint8), axis=1)
+    elif case == "one_pixel":        # constant rows + single isolated pixels
+        px = np.tile(base, (H, 1))
+        for _ in range(40):
+            px[int(rng.integers(0, H)), int(rng.integers(0, W))] ^= True
+        bits = np.packbits(px.astype(np.uint8), axis=1)
+    else:                            # vertical pairs straddling the strip edge, toggled together
+        px = np.zeros((H, W), bool)
+        on = False
+        for yy in range(H):
+            if yy % 61 == 0:
+                on = not on
+            px[yy, 1023] = on
+            px[yy, 1024] = (yy % 13) < 9
+        bits = np.packbits(px.astype(np.uint8), axis=1)
+    want_c = orc.counts(bits, W)
+    want_b = orc.boundaries(want_c)
+    he, runs, links = orc.hyperedges(bits, W)
+    for skip in (True, False):
+        c, b, t = _scan_plan(y, bits, W, H, skip=skip)
+        assert np.array_equal(c, want_c), (case, skip)
+        assert np.array_equal(b, want_b), (case, skip)
+        assert t[:3] == [runs, links, he], (case, skip)
