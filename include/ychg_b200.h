@@ -115,6 +115,13 @@ YCHG_API int ychg_cut_vertex_counts(const uint8_t* bits, int32_t width, int32_t 
 /* boundaries_out must hold n entries; *n_out receives the number written. */
 YCHG_API int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, int32_t* boundaries_out,
                                  int64_t* n_out);
+/* The same on device-resident counts (e.g. counts all-gathered from column
+ * strips on several GPUs), asynchronous on `stream`:
+ * d_flags needs ychg_boundary_flag_words(n) words (flags + scratch),
+ * d_boundaries n ints, *d_n (device) receives the boundary count. */
+YCHG_API int64_t ychg_boundary_flag_words(int64_t n);
+YCHG_API int ychg_detect_boundaries_device(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
+                                           int32_t* d_boundaries, int64_t* d_n, void* stream);
 
 /* Fused pass.  counts_out[width] (may be NULL), boundaries_out[width] (may be NULL),
  * totals_out (may be NULL).  with_hyperedges = 0 skips K3 (hyperedges = -1). */
@@ -250,6 +257,12 @@ YCHG_API int ychg_plan_debug_peek(ychg_plan* plan, uint64_t* host_out, int32_t c
  * writes height rows of `pitch` bytes, padding bytes and bits zeroed. */
 YCHG_API int ychg_synth_device(int32_t pattern, int32_t width, int32_t height, int32_t bands, int32_t cell,
                       double density, uint64_t seed, uint8_t* d_bits, int64_t pitch, void* stream);
+/* Columns [x0, x0 + win) of the same width x height image (x0 a multiple of 8),
+ * packed from bit 7 of each row's byte 0: a multi-GPU column strip generated in
+ * place, bit-exact with those columns of the whole image. */
+YCHG_API int ychg_synth_device_window(int32_t pattern, int32_t width, int32_t height, int32_t x0, int32_t win,
+                                      int32_t bands, int32_t cell, double density, uint64_t seed, uint8_t* d_bits,
+                                      int64_t pitch, void* stream);
 
 /* Device memory helpers so hosts without a CUDA runtime binding can drive the
  * device API (tests, ctypes). */

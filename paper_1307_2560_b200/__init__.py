@@ -85,6 +85,10 @@ _SIGS = {
     "ychg_plan_debug_stamps": (ctypes.c_int, [_vp, _i32, _vp, _i32, ctypes.POINTER(_i32)]),
     "ychg_plan_debug_peek": (ctypes.c_int, [_vp, _vp, _i32]),
     "ychg_synth_device": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64, _vp, _i64, _vp]),
+    "ychg_boundary_flag_words": (_i64, [_i64]),
+    "ychg_detect_boundaries_device": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
+    "ychg_synth_device_window": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64,
+                                                _vp, _i64, _vp]),
     "ychg_device_alloc": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.POINTER(_vp)]),
     "ychg_device_free": (ctypes.c_int, [ctypes.c_int, _vp]),
     "ychg_host_alloc_pinned": (ctypes.c_int, [_i64, ctypes.POINTER(_vp)]),
@@ -535,17 +539,39 @@ class Plan:
                                      d_boundaries, d_totals, stream or None), "scan_device")
 
 
+def boundary_flag_words(n: int) -> int:
+    """uint32 words of flags + scratch that detect_boundaries_device needs for n columns."""
+    return int(_lib.ychg_boundary_flag_words(int(n)))
+
+
+def detect_boundaries_device(d_counts: int, n: int, d_flags: int, d_boundaries: int, d_n: int,
+                             stream: int = 0) -> None:
+    """detect_boundary_columns (runscan.cpp:145-153) on device-resident counts (e.g. all-gathered
+    from column strips), asynchronous on `stream`; *d_n (int64, device) = boundary count."""
+    _check(_lib.ychg_detect_boundaries_device(d_counts, int(n), d_flags, d_boundaries, d_n, stream or None),
+           "detect_boundaries_device")
+
+
 def pitch_for(width: int) -> int:
     """Device row pitch used by the library: ceil(width/8) rounded up to 16 B (TMA stride rule)."""
     return ((width + 7) // 8 + 15) // 16 * 16
 
 
 def synth_device(pattern: str, width: int, height: int, d_bits: int, pitch: int, *, bands: int = 0,
-                 cell: int = 0, density: float = 0.0, seed: int = 0, stream: int = 0) -> None:
-    """K0: bit-exact reference synth() (synth.cpp:38-104) written straight into device memory."""
-    _check(_lib.ychg_synth_device(PATTERNS[pattern], width, height, bands, cell, float(density),
-                                  int(seed) & 0xFFFFFFFFFFFFFFFF, d_bits, int(pitch), stream or None),
-           "synth_device")
+                 cell: int = 0, density: float = 0.0, seed: int = 0, stream: int = 0,
+                 x0: int = 0, win: int | None = None) -> None:
+    """K0: bit-exact reference synth() (synth.cpp:38-104) written straight into device memory;
+    with x0 / win only the column window [x0, x0 + win) of the width x height image
+    (a multi-GPU column strip, x0 a multiple of 8)."""
+    if x0 == 0 and win is None:
+        _check(_lib.ychg_synth_device(PATTERNS[pattern], width, height, bands, cell, float(density),
+                                      int(seed) & 0xFFFFFFFFFFFFFFFF, d_bits, int(pitch), stream or None),
+               "synth_device")
+        return
+    win = width - x0 if win is None else int(win)
+    _check(_lib.ychg_synth_device_window(PATTERNS[pattern], width, height, int(x0), win, bands, cell, float(density),
+                                         int(seed) & 0xFFFFFFFFFFFFFFFF, d_bits, int(pitch), stream or None),
+           "synth_device_window")
 
 
 class DeviceBuffer:

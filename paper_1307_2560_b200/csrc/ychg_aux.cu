@@ -24,6 +24,7 @@ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
 
 struct SynthArgs {
     int pattern, width, height, bands, cell, all;
+    int x0, win;  // the buffer holds columns [x0, x0 + win) of the width x height image
     uint64_t seed, threshold;
     int64_t pitch;
     int row_bytes, band_h;
@@ -59,8 +60,9 @@ __global__ void synth_kernel(const SynthArgs a, uint8_t* __restrict__ out) {
         if (xb < a.row_bytes && !(a.pattern == 5 && a.threshold == 0 && !a.all)) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int x = xb * 8 + i;
-                if (x < a.width && synth_pixel(a, x, y)) v |= 0x80u >> i;
+                const int xl = xb * 8 + i;
+                const int x = a.x0 + xl;
+                if (xl < a.win && x < a.width && synth_pixel(a, x, y)) v |= 0x80u >> i;
             }
         }
         out[idx] = static_cast<uint8_t>(v);
@@ -136,18 +138,24 @@ __global__ void bcompact_kernel(const uint32_t* __restrict__ flags, int64_t n,
 
 }  // namespace
 
-extern "C" int ychg_launch_synth(int pattern, int width, int height, int bands, int cell,
-                                 double density, uint64_t seed, uint8_t* d_bits, int64_t pitch,
-                                 cudaStream_t stream) {
+// Columns [x0, x0 + win) of the width x height reference image (x0 a multiple of
+// 8), packed from bit 7 of byte 0: a multi-GPU column strip generated in place,
+// bit-exact with the same columns of the whole image (random draws are indexed
+// by the global pixel index y * width + x).
+extern "C" int ychg_launch_synth_window(int pattern, int width, int height, int x0, int win, int bands, int cell,
+                                        double density, uint64_t seed, uint8_t* d_bits, int64_t pitch,
+                                        cudaStream_t stream) {
     SynthArgs a{};
     a.pattern = pattern;
     a.width = width;
     a.height = height;
+    a.x0 = x0;
+    a.win = win;
     a.bands = bands;
     a.cell = cell < 1 ? 1 : cell;
     a.seed = seed;
     a.pitch = pitch;
-    a.row_bytes = (width + 7) / 8;
+    a.row_bytes = (win + 7) / 8;
     a.band_h = (pattern == 3 && bands > 0) ? (height - (bands - 1)) / bands : 0;
     if (pattern == 5) {
         // synth.cpp:76-79: threshold = (uint64)(density * 2^64), "all" when it saturates.
@@ -167,6 +175,13 @@ extern "C" int ychg_launch_synth(int pattern, int width, int height, int bands, 
     synth_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(a, d_bits);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+extern "C" int ychg_launch_synth(int pattern, int width, int height, int bands, int cell,
+                                 double density, uint64_t seed, uint8_t* d_bits, int64_t pitch,
+                                 cudaStream_t stream) {
+    return ychg_launch_synth_window(pattern, width, height, 0, width, bands, cell, density, seed, d_bits, pitch,
+                                    stream);
 }
 
 // d_flags needs ceil(n/32) words rounded up to a multiple of 32; d_n is one long long.

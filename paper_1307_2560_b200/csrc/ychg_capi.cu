@@ -392,6 +392,13 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
 
 int ychg_synth_device(int32_t pattern, int32_t width, int32_t height, int32_t bands, int32_t cell,
                       double density, uint64_t seed, uint8_t* d_bits, int64_t pitch, void* stream) {
+    return ychg_synth_device_window(pattern, width, height, 0, width, bands, cell, density, seed, d_bits, pitch,
+                                    stream);
+}
+
+int ychg_synth_device_window(int32_t pattern, int32_t width, int32_t height, int32_t x0, int32_t win,
+                             int32_t bands, int32_t cell, double density, uint64_t seed, uint8_t* d_bits,
+                             int64_t pitch, void* stream) {
     // Validation as synth.cpp:10-34.
     if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "synth: negative dimensions %dx%d", width, height);
     if (pattern < 0 || pattern > 5) return fail(YCHG_ERR_INVALID, "synth: unknown pattern %d", pattern);
@@ -401,12 +408,14 @@ int ychg_synth_device(int32_t pattern, int32_t width, int32_t height, int32_t ba
         return fail(YCHG_ERR_INVALID, "synth: checker cell must be >= 1, got %d", cell);
     if (pattern == YCHG_PATTERN_RANDOM && !(density >= 0.0 && density <= 1.0))
         return fail(YCHG_ERR_INVALID, "synth: random density must lie in [0, 1], got %f", density);
-    if (pitch < (width + 7) / 8) return fail(YCHG_ERR_INVALID, "synth: pitch too small");
+    if (x0 < 0 || x0 % 8 != 0 || win < 0 || x0 > width)
+        return fail(YCHG_ERR_INVALID, "synth: window x0=%d (a multiple of 8 in [0, %d]) width %d", x0, width, win);
+    if (pitch < (win + 7) / 8) return fail(YCHG_ERR_INVALID, "synth: pitch too small");
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (const int rc = require_device(dev)) return rc;
-    const int rc = ychg_launch_synth(pattern, width, height, bands, cell, density, seed, d_bits, pitch,
-                                     static_cast<cudaStream_t>(stream));
+    const int rc = ychg_launch_synth_window(pattern, width, height, x0, win, bands, cell, density, seed, d_bits,
+                                            pitch, static_cast<cudaStream_t>(stream));
     if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "synth kernel launch");
     return YCHG_OK;
 }
@@ -642,6 +651,17 @@ int h2d_staged(HostContext& c, uint8_t* d_dst, const uint8_t* src, int64_t bytes
         c.stage_bytes = 0;
         for (auto& p : c.h_stage) CK(cudaMallocHost(&p, chunk));
         c.stage_bytes = chunk;
+    }
+    static const int64_t direct_max = [] {
+        // small inputs: the driver's own staged copy has no pool hand-off and a
+        // steadier latency (4096^2, 2 MB: 150 us vs a bimodal 250/430 us through
+        // the pool on a 16-core host, scripts/host_counts_probe.py)
+        const char* v = getenv("YCHG_PAGEABLE_DIRECT_MB");
+        return (v && *v ? atoll(v) : 4) << 20;
+    }();
+    if (bytes <= direct_max) {
+        CK(cudaMemcpyAsync(d_dst, src, bytes, cudaMemcpyHostToDevice, c.stream));
+        return YCHG_OK;
     }
     // the copy stream must not overwrite device memory still read by earlier work on c.stream
     CK(cudaEventRecord(c.chunk_ev[0], c.stream));
@@ -932,6 +952,23 @@ extern "C" int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, in
         CK(cudaStreamSynchronize(c.stream));
     }
     if (n_out) *n_out = nb;
+    return YCHG_OK;
+}
+
+extern "C" int64_t ychg_boundary_flag_words(int64_t n) {
+    // flags: one word per 32 columns, rounded to whole 1024-column blocks, + per-block counts
+    return ((n + 1023) / 1024) * 32 + (n + 1023) / 1024 + 32;
+}
+
+extern "C" int ychg_detect_boundaries_device(const int32_t* d_counts, int64_t n, uint32_t* d_flags, int32_t* d_boundaries,
+                                  int64_t* d_n, void* stream) {
+    if (n < 0) return fail(YCHG_ERR_INVALID, "detect_boundary_columns: negative length");
+    if (!d_n || (n > 0 && (!d_counts || !d_flags || !d_boundaries)))
+        return fail(YCHG_ERR_INVALID, "detect_boundary_columns: NULL device buffer");
+    if (n > INT32_MAX) return fail(YCHG_ERR_INVALID, "detect_boundary_columns: more than 2^31-1 columns");
+    const int rc = ychg_launch_boundaries(d_counts, n, d_flags, d_boundaries, reinterpret_cast<long long*>(d_n),
+                                          static_cast<cudaStream_t>(stream));
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "boundary kernels launch");
     return YCHG_OK;
 }
 

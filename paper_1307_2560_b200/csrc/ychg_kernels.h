@@ -22,6 +22,8 @@ void ychg_scan_kernel_shape(int with_links, int* threads, int* smem_bytes);
 
 int ychg_launch_synth(int pattern, int width, int height, int bands, int cell, double density,
                       uint64_t seed, uint8_t* d_bits, int64_t pitch, cudaStream_t stream);
+int ychg_launch_synth_window(int pattern, int width, int height, int x0, int win, int bands, int cell,
+                             double density, uint64_t seed, uint8_t* d_bits, int64_t pitch, cudaStream_t stream);
 
 int ychg_launch_repitch(const uint8_t* d_src, int64_t row_bytes, uint8_t* d_dst, int64_t pitch, int y0, int y1,
                         cudaStream_t stream);

@@ -1,6 +1,6 @@
-"""CPU: the column-strip sharding host logic (paper_1307_2560_b200/sharded.py) over
-torch.distributed gloo with world_size 2 and 3, strips computed by the oracle
-(on GPUs the same logic drives the C ABI per rank and NCCL)."""
+"""CPU: the column-strip sharding host logic (paper_1307_2560_b200/multigpu.py: plan_strips,
+StripExchange) over torch.distributed gloo with world_size 2 and 3, strips computed by the
+oracle; bench.py drives the same StripExchange with NCCL and the C ABI per GPU."""
 import os
 import socket
 
@@ -10,7 +10,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import Oracle, Spec
-from paper_1307_2560_b200.sharded import merge_boundaries, plan_strips, run_sharded, strip_bits
+from paper_1307_2560_b200.multigpu import merge_boundaries, plan_strips, run_sharded, strip_bits
 
 
 def oracle_strip(orc):
