@@ -108,6 +108,8 @@ class Oracle:
         L.yo_hyperedge_count.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i64p, _i64p]
         L.yo_pair_link_counts.restype = ctypes.c_int
         L.yo_pair_link_counts.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i32p]
+        L.yo_a7_links.restype = ctypes.c_int64
+        L.yo_a7_links.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64]
         L.yo_profile.restype = ctypes.c_int64
         L.yo_profile.argtypes = [_u8p, ctypes.c_int, ctypes.c_int, ctypes.c_int64, _i32p, ctypes.c_int64, _i32p]
         L.yo_foreground_count.restype = ctypes.c_int64
@@ -186,6 +188,15 @@ class Oracle:
         counts = np.bincount(runs[:, 0], minlength=w).astype(np.int32) if len(runs) else np.zeros(w, np.int32)
         return self.decompose_profile(runs, counts)
 
+    def a7_links(self, bits: np.ndarray, w: int) -> int:
+        """Link total by the streaming a7 rule (yo_a7_links, OpenMP over column pairs):
+        independent of decompose's run lists, so it reaches 65536^2."""
+        h = bits.shape[0]
+        if w < 2 or h == 0:
+            return 0
+        bits = np.ascontiguousarray(bits)
+        return int(self.lib.yo_a7_links(_ptr(bits, _u8p), w, h, bits.shape[1]))
+
     def pair_links(self, bits: np.ndarray, w: int) -> np.ndarray:
         h = bits.shape[0]
         out = np.zeros(max(w - 1, 0), dtype=np.int32)
@@ -218,6 +229,8 @@ class Reference:
         L.yr_image_bytes.argtypes = [ctypes.c_void_p]
         L.yr_counts.restype = ctypes.c_int
         L.yr_counts.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _i32p]
+        L.yr_column_runs.restype = ctypes.c_int64
+        L.yr_column_runs.argtypes = [ctypes.c_void_p, ctypes.c_int, _i32p, ctypes.c_int64]
         L.yr_boundaries.restype = ctypes.c_int64
         L.yr_boundaries.argtypes = [_i32p, ctypes.c_int64, _i32p]
         L.yr_hyperedges.restype = ctypes.c_int64
@@ -319,6 +332,15 @@ class RefImage:
             raise RuntimeError(self.ref.last_error())
         out = np.zeros((max(n, 1), 3), dtype=np.int32)
         self.ref.lib.yr_profile(self.handle, kind, threads, _ptr(out, _i32p), n)
+        return out[:n]
+
+    def column_runs(self, col: int) -> np.ndarray:
+        """column_runs(img, col) by the reference: (n, 3) int32; ValueError(what()) when it throws."""
+        n = self.ref.lib.yr_column_runs(self.handle, int(col), None, 0)
+        if n < 0:
+            raise ValueError(self.ref.last_error())
+        out = np.zeros((max(n, 1), 3), dtype=np.int32)
+        self.ref.lib.yr_column_runs(self.handle, int(col), _ptr(out, _i32p), n)
         return out[:n]
 
     def hyperedges(self, kind: int = 0, threads: int = 1) -> int:

@@ -111,6 +111,24 @@ YR_EXPORT int yr_counts(void* img, int kind, int threads, int32_t* out) {
     }
 }
 
+// column_runs(image, col) (runscan.cpp:104-120): returns the run count (triples
+// {col, y_top, y_bot} into runs when capacity allows), -1 on a reference exception.
+YR_EXPORT int64_t yr_column_runs(void* img, int col, int32_t* runs, int64_t capacity) {
+    try {
+        const auto r = ychg::column_runs(*static_cast<ychg::BinaryImage*>(img), col);
+        if (runs && capacity >= static_cast<int64_t>(r.size()))
+            for (std::size_t i = 0; i < r.size(); ++i) {
+                runs[3 * i] = r[i].col;
+                runs[3 * i + 1] = r[i].y_top;
+                runs[3 * i + 2] = r[i].y_bot;
+            }
+        return static_cast<int64_t>(r.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 YR_EXPORT int64_t yr_boundaries(const int32_t* counts, int64_t n, int32_t* out) {
     const auto b = ychg::detect_boundary_columns(std::span<const int>(counts, static_cast<size_t>(n)));
     if (out && !b.empty()) std::memcpy(out, b.data(), b.size() * sizeof(int));

@@ -18,9 +18,11 @@
  * MSB-first in each byte (x = 0 is bit 0x80), rows padded to stride = (w+7)/8 bytes,
  * padding bits zero.  All entry points take (bits, w, h, stride).
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #define YO_EXPORT __attribute__((visibility("default")))
 
@@ -55,50 +57,114 @@ YO_EXPORT int yo_synth_validate(int pattern, int w, int h, int bands, int cell, 
     return 0;
 }
 
+/* ---------------------------------------------------------------- threads
+ * Row / column ranges split over the host's cores (pthreads; no OpenMP runtime in
+ * this image).  Only the large-image parity tests need it; results are identical
+ * to the serial loops. */
+typedef void (*yo_range_fn)(void* ctx, int64_t lo, int64_t hi);
+typedef struct {
+    yo_range_fn fn;
+    void* ctx;
+    int64_t lo, hi;
+} yo_job;
+
+static void* yo_job_run(void* p) {
+    yo_job* j = (yo_job*)p;
+    if (j->hi > j->lo) j->fn(j->ctx, j->lo, j->hi);
+    return NULL;
+}
+
+static void yo_parallel(int64_t n, yo_range_fn fn, void* ctx) {
+    long t = sysconf(_SC_NPROCESSORS_ONLN);
+    if (t < 1) t = 1;
+    if (t > 64) t = 64;
+    if (n < 4096 || t == 1) {
+        fn(ctx, 0, n);
+        return;
+    }
+    pthread_t th[64];
+    yo_job jobs[64];
+    for (long i = 0; i < t; ++i) {
+        jobs[i].fn = fn;
+        jobs[i].ctx = ctx;
+        jobs[i].lo = n * i / t;
+        jobs[i].hi = n * (i + 1) / t;
+        if (i > 0 && pthread_create(&th[i], NULL, yo_job_run, &jobs[i]) != 0) yo_job_run(&jobs[i]), th[i] = 0;
+    }
+    yo_job_run(&jobs[0]);
+    for (long i = 1; i < t; ++i)
+        if (th[i]) pthread_join(th[i], NULL);
+}
+
+typedef struct {
+    int pattern, w, h, bands, cell, all;
+    uint64_t seed, threshold;
+    int64_t stride;
+    uint8_t* out;
+} yo_synth_args;
+
+static void yo_synth_rows(void* p, int64_t y0, int64_t y1) {
+    const yo_synth_args* a = (const yo_synth_args*)p;
+    const int w = a->w, h = a->h;
+    const int bh = a->pattern == YO_HBANDS ? (h - (a->bands - 1)) / a->bands : 0;
+    for (int64_t yy = y0; yy < y1; ++yy) {
+        const int y = (int)yy;
+        switch (a->pattern) {
+        case YO_FULL: /* synth.cpp:38-43 */
+            for (int x = 0; x < w; ++x) yo_set(a->out, a->stride, x, y);
+            break;
+        case YO_FRAME: /* synth.cpp:45-51 */
+            for (int x = 0; x < w; ++x)
+                if (x == 0 || y == 0 || x == w - 1 || y == h - 1) yo_set(a->out, a->stride, x, y);
+            break;
+        case YO_HBANDS: { /* synth.cpp:55-64: equal maximal bands from the top, 1-row gaps */
+            const int b = y / (bh + 1);
+            if (b < a->bands && y - b * (bh + 1) < bh)
+                for (int x = 0; x < w; ++x) yo_set(a->out, a->stride, x, y);
+            break;
+        }
+        case YO_CHECKER: /* synth.cpp:66-72 */
+            for (int x = 0; x < w; ++x)
+                if (((x / a->cell) + (y / a->cell)) % 2 == 0) yo_set(a->out, a->stride, x, y);
+            break;
+        case YO_RANDOM: { /* synth.cpp:74-87: one draw per pixel, row-major, draw < density*2^64;
+                           * draw i of the sequential generator mixes state seed + (i+1)*golden,
+                           * so every row starts from seed + y*w*golden */
+            uint64_t st = a->seed + (uint64_t)y * (uint64_t)w * 0x9e3779b97f4a7c15ull;
+            for (int x = 0; x < w; ++x) {
+                const uint64_t draw = yo_splitmix64_next(&st);
+                if (a->all || draw < a->threshold) yo_set(a->out, a->stride, x, y);
+            }
+            break;
+        }
+        default:
+            break;
+        }
+    }
+}
+
 /* out must hold h * ((w+7)/8) bytes; it is fully overwritten. */
 YO_EXPORT int yo_synth(int pattern, int w, int h, int bands, int cell, double density,
                        uint64_t seed, uint8_t* out) {
     if (yo_synth_validate(pattern, w, h, bands, cell, density) != 0) return -1;
-    const int64_t stride = (w + 7) / 8;
-    memset(out, 0, (size_t)(stride * h));
-    switch (pattern) {
-    case YO_FULL: /* synth.cpp:38-43 */
-        for (int y = 0; y < h; ++y)
-            for (int x = 0; x < w; ++x) yo_set(out, stride, x, y);
-        break;
-    case YO_EMPTY:
-        break;
-    case YO_FRAME: /* synth.cpp:45-51 */
-        for (int y = 0; y < h; ++y)
-            for (int x = 0; x < w; ++x)
-                if (x == 0 || y == 0 || x == w - 1 || y == h - 1) yo_set(out, stride, x, y);
-        break;
-    case YO_HBANDS: { /* synth.cpp:55-64: equal maximal bands from the top, 1-row gaps */
-        const int bh = (h - (bands - 1)) / bands;
-        for (int b = 0; b < bands; ++b)
-            for (int y = b * (bh + 1); y < b * (bh + 1) + bh; ++y)
-                for (int x = 0; x < w; ++x) yo_set(out, stride, x, y);
-        break;
-    }
-    case YO_CHECKER: /* synth.cpp:66-72 */
-        for (int y = 0; y < h; ++y)
-            for (int x = 0; x < w; ++x)
-                if (((x / cell) + (y / cell)) % 2 == 0) yo_set(out, stride, x, y);
-        break;
-    case YO_RANDOM: { /* synth.cpp:74-87: one draw per pixel, row-major, draw < density*2^64 */
-        if (density <= 0.0) break;
+    yo_synth_args a;
+    memset(&a, 0, sizeof(a));
+    a.pattern = pattern;
+    a.w = w;
+    a.h = h;
+    a.bands = bands;
+    a.cell = cell;
+    a.seed = seed;
+    a.stride = (w + 7) / 8;
+    a.out = out;
+    memset(out, 0, (size_t)(a.stride * h));
+    if (pattern == YO_EMPTY || (pattern == YO_RANDOM && density <= 0.0)) return 0;
+    if (pattern == YO_RANDOM) {
         const double scaled = density * 18446744073709551616.0; /* 0x1p64 */
-        const int all = scaled >= 18446744073709551616.0;
-        const uint64_t threshold = all ? 0 : (uint64_t)scaled;
-        uint64_t st = seed;
-        for (int y = 0; y < h; ++y)
-            for (int x = 0; x < w; ++x) {
-                const uint64_t draw = yo_splitmix64_next(&st);
-                if (all || draw < threshold) yo_set(out, stride, x, y);
-            }
-        break;
+        a.all = scaled >= 18446744073709551616.0;
+        a.threshold = a.all ? 0 : (uint64_t)scaled;
     }
-    }
+    yo_parallel(h, yo_synth_rows, &a);
     return 0;
 }
 
@@ -107,17 +173,30 @@ YO_EXPORT int yo_synth(int pattern, int w, int h, int bands, int cell, double de
  * counted per pixel as background->foreground transitions scanning down with a
  * virtual background row -1 (runscan.cpp:41-74 semantics; the per-pixel form is
  * the reference's own independent checker corpus.hpp:91-102). */
-YO_EXPORT void yo_cut_vertex_counts(const uint8_t* bits, int w, int h, int64_t stride,
-                                    int32_t* counts) {
-    for (int c = 0; c < w; ++c) {
+typedef struct {
+    const uint8_t* bits;
+    int w, h;
+    int64_t stride;
+    int32_t* counts;
+} yo_counts_args;
+
+static void yo_counts_cols(void* p, int64_t c0, int64_t c1) {
+    const yo_counts_args* a = (const yo_counts_args*)p;
+    for (int64_t c = c0; c < c1; ++c) {
         int prev = 0, n = 0;
-        for (int y = 0; y < h; ++y) {
-            const int cur = yo_get(bits, stride, c, y);
+        for (int y = 0; y < a->h; ++y) {
+            const int cur = yo_get(a->bits, a->stride, (int)c, y);
             n += cur & !prev;
             prev = cur;
         }
-        counts[c] = n;
+        a->counts[c] = n;
     }
+}
+
+YO_EXPORT void yo_cut_vertex_counts(const uint8_t* bits, int w, int h, int64_t stride,
+                                    int32_t* counts) {
+    yo_counts_args a = {bits, w, h, stride, counts};
+    yo_parallel(w, yo_counts_cols, &a);
 }
 
 /* ---------------------------------------------------------------- step 2
@@ -330,4 +409,72 @@ YO_EXPORT int64_t yo_decompose(const int32_t* runs, const int32_t* counts, int w
     }
     free(off); free(right); free(has_left); free(scratch); free(ra); free(rb);
     return e;
+}
+
+/* ---------------------------------------------------------------- a7, streaming form
+ * The link count of decompose() (hypergraph.cpp:108-143) restated as a row scan per
+ * column pair: the 4-connected components of the 2-column strip
+ * {c, c+1} are row intervals; a row continues the open component iff
+ * (a & pa) | (b & pb); a component is a link iff it holds exactly two runs (one per
+ * column, mutually unique).  n counts the runs of the open component (saturating
+ * at 3); virtual empty rows -1 and h close everything.  Independent of the GPU's
+ * bit-sliced formulation; pinned to the decompose-based count above by
+ * tests/test_oracle.py.  Column pairs are split over the host cores (the 65536^2
+ * parity test, where decompose itself needs tens of GB).  Returns the link total;
+ * hyperedges = total runs - links. */
+typedef struct {
+    const uint8_t* bits;
+    int h, pairs;
+    int64_t stride;
+    int64_t links[1];  /* total, atomically accumulated by the ranges */
+} yo_a7_args;
+
+static void yo_a7_range(void* p, int64_t lo, int64_t hi) {
+    yo_a7_args* a = (yo_a7_args*)p;
+    const int chunk = 512;
+    int64_t links = 0;
+    unsigned char* n = (unsigned char*)calloc(chunk, 1);
+    unsigned char* pa = (unsigned char*)calloc(chunk + 1, 1);
+    unsigned char* cur = (unsigned char*)calloc(chunk + 1, 1);
+    for (int64_t c0 = lo; c0 < hi; c0 += chunk) {
+        const int np = (int)(hi - c0 < chunk ? hi - c0 : chunk);
+        memset(n, 0, (size_t)chunk);
+        memset(pa, 0, (size_t)chunk + 1);
+        for (int y = 0; y <= a->h; ++y) {
+            /* bits of columns c0 .. c0+np (np + 1 columns) of row y; row h is empty */
+            for (int i = 0; i <= np; ++i)
+                cur[i] = y < a->h ? (unsigned char)yo_get(a->bits, a->stride, (int)c0 + i, y) : 0;
+            for (int i = 0; i < np; ++i) {
+                const int av = cur[i], bv = cur[i + 1], pav = pa[i], pbv = pa[i + 1];
+                const int cont = (av & pav) | (bv & pbv);
+                if (!cont) {
+                    if ((pav | pbv) && n[i] == 2) ++links;
+                    n[i] = (unsigned char)(av + bv);
+                } else {
+                    const int m = n[i] + (av & !pav) + (bv & !pbv);
+                    n[i] = (unsigned char)(m > 3 ? 3 : m);
+                }
+            }
+            unsigned char* t = pa;
+            pa = cur;
+            cur = t;
+        }
+    }
+    free(n);
+    free(pa);
+    free(cur);
+    __atomic_fetch_add(&a->links[0], links, __ATOMIC_RELAXED);
+}
+
+YO_EXPORT int64_t yo_a7_links(const uint8_t* bits, int w, int h, int64_t stride) {
+    if (w < 2 || h <= 0) return 0;
+    yo_a7_args* a = (yo_a7_args*)calloc(1, sizeof(yo_a7_args));
+    a->bits = bits;
+    a->h = h;
+    a->pairs = w - 1;
+    a->stride = stride;
+    yo_parallel(w - 1, yo_a7_range, a);
+    const int64_t links = a->links[0];
+    free(a);
+    return links;
 }

@@ -63,20 +63,24 @@ int main() {
         CHECK(cut_vertex_counts(frame(5, 5), ScanStrategy::parallel(t)) ==
               (std::vector<int>{1, 2, 2, 2, 1}));
 
-    bool threw = false;
-    try {
-        cut_vertex_counts(full(3, 50), ScanStrategy::parallel(0));
-    } catch (const ValidationError&) {
-        threw = true;
-    }
-    CHECK(threw);
-    threw = false;
-    try {
-        cut_vertex_counts(full(3, 50), ScanStrategy::parallel(-2));
-    } catch (const ValidationError&) {
-        threw = true;
-    }
-    CHECK(threw);
+    // Validation: the exception type AND its what() (runscan.cpp:25-26, 105-107).
+    // The messages are printed as "WHAT\t<case>\t<what()>" for tests/test_gpu_parity.py,
+    // which compares them with the live reference's own messages.
+    auto expect_validation = [&](const char* name, auto&& fn) {
+        bool threw = false;
+        try {
+            fn();
+        } catch (const ValidationError& e) {
+            threw = true;
+            std::printf("WHAT\t%s\t%s\n", name, e.what());
+        }
+        CHECK(threw);
+    };
+    expect_validation("parallel0", [&] { cut_vertex_counts(full(3, 50), ScanStrategy::parallel(0)); });
+    expect_validation("parallel-2", [&] { cut_vertex_counts(full(3, 50), ScanStrategy::parallel(-2)); });
+    expect_validation("column_runs4", [&] { column_runs(full(4, 4), 4); });
+    expect_validation("column_runs-1", [&] { column_runs(full(4, 4), -1); });
+    expect_validation("build_profile_parallel0", [&] { build_profile(full(3, 5), ScanStrategy::parallel(0)); });
 
     CHECK(detect_boundary_columns(std::vector<int>{1, 2, 2, 2, 1}) == (std::vector<int>{0, 1, 4}));
     CHECK(detect_boundary_columns(std::vector<int>{0, 0, 0}).empty());

@@ -198,12 +198,33 @@ def test_timing_hooks(gpu):
     assert info.kernels_per_scan == 1 and info.grid >= 1
 
 
-def test_cxx_dropin_binary(gpu):
+def test_cxx_dropin_binary(gpu, ref):
+    """The reference's test_runscan.cpp vectors through the C++ drop-in, and its
+    ValidationError::what() texts equal to the live reference's (runscan.cpp:25-26,
+    105-107): no prefix added by the shim."""
     exe = os.path.join(ROOT, "tests", "cpp", "dropin_test")
     if not os.path.exists(exe):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
+    ours = dict(ln.split("\t")[1:3] for ln in out.stdout.splitlines() if ln.startswith("WHAT\t"))
+    full3 = ref.image(np.full((50, 1), 0xE0, np.uint8), 3)
+    full4 = ref.image(np.full((4, 1), 0xF0, np.uint8), 4)
+
+    def ref_what(fn):
+        with pytest.raises(ValueError) as e:
+            fn()
+        return str(e.value)
+
+    want = {"parallel0": ref_what(lambda: full3.counts(1, 0)),
+            "parallel-2": ref_what(lambda: full3.counts(1, -2)),
+            "column_runs4": ref_what(lambda: full4.column_runs(4)),
+            "column_runs-1": ref_what(lambda: full4.column_runs(-1))}
+    assert want["parallel0"] == "scan: parallel strategy needs threads >= 1, got 0"
+    assert want["column_runs4"] == "column_runs: column 4 out of range [0, 4)"
+    for k, v in want.items():
+        assert ours[k] == v, (k, ours[k], v)
+    assert ours["build_profile_parallel0"] == want["parallel0"]
 
 
 def test_back_to_back_scans_pipelined(gpu, orc):
@@ -679,3 +700,26 @@ def test_skip_unchanged_blocks_exact(gpu, orc, case):
         assert np.array_equal(c, want_c), (case, skip)
         assert np.array_equal(b, want_b), (case, skip)
         assert t[:3] == [runs, links, he], (case, skip)
+
+
+def test_column_runs_byte_column_path(gpu, orc, ref):
+    """column_runs moves one byte column (O(height)) and rebases Run.col: every
+    column of odd widths (partial last byte, garbage padding bits), and a column of
+    > 65536 runs (the second, exact-size call), against the live reference."""
+    y = gpu
+    for sp in (Spec.random(37, 301, 0.5, 5), Spec.random(1031, 77, 0.3, 6), Spec.checker(19, 40, 3)):
+        bits = orc.synth(sp)
+        rimg = ref.image(bits, sp.width)
+        noisy = bits.copy()
+        if sp.width % 8:
+            noisy[:, -1] |= np.uint8((1 << (8 - sp.width % 8)) - 1)  # padding bits set: must be ignored
+        for img in (y.BinaryImage(sp.width, sp.height, bits), y.BinaryImage(sp.width, sp.height, noisy)):
+            for col in range(sp.width):
+                assert np.array_equal(y.column_runs(img, col), rimg.column_runs(col)), (sp, col)
+    tall = Spec.random(9, 300_000, 0.5, 7)
+    bits = orc.synth(tall)
+    rimg = ref.image(bits, 9)
+    img = y.BinaryImage(9, tall.height, bits)
+    for col in (0, 4, 8):
+        got = y.column_runs(img, col)
+        assert got.shape[0] > 65536 and np.array_equal(got, rimg.column_runs(col)), col

@@ -98,6 +98,39 @@ def test_a7_streaming_rule_equals_decompose(orc):
         assert a7_links(bits, sp.width) == links, name
 
 
+def test_c_a7_restatement_pinned(orc):
+    """yo_a7_links (the C streaming restatement the 65536^2 parity test relies on,
+    where decompose does not fit) equals the decompose-based link count on the whole
+    corpus and on the reference-pinned large fixtures, whose hyperedge totals come
+    from the reference's own decompose (tests/golden/large_ref.json)."""
+    for name, sp in full_corpus():
+        bits = orc.synth(sp)
+        he, runs, links = orc.hyperedges(bits, sp.width)
+        assert orc.a7_links(bits, sp.width) == links, name
+    for row in large():
+        sp = spec_of(row["spec"])
+        bits = orc.synth(sp)
+        runs = int(orc.counts(bits, sp.width).astype(np.int64).sum())
+        assert runs - orc.a7_links(bits, sp.width) == row["hyperedges"], row["spec"]
+
+
+def test_threaded_synth_matches_serial_draws(orc):
+    """yo_synth splits rows over threads; the random pattern's row start state
+    seed + y*w*golden must reproduce the sequential SplitMix64 stream exactly."""
+    sp = Spec.random(5003, 900, 0.37, 987654321)
+    bits = orc.synth(sp)
+    draws = orc.splitmix64(sp.seed, 3 * sp.width)   # the first three rows, sequentially
+    thr = int(0.37 * 2.0 ** 64)
+    for y in range(3):
+        row = np.array([d < thr for d in draws[y * sp.width:(y + 1) * sp.width]], dtype=np.uint8)
+        assert np.array_equal(np.packbits(row), bits[y]), y
+    tall = Spec.random(40, 9000, 0.5, 11)   # > 4096 rows: the threaded path
+    tb = orc.synth(tall)
+    dr = orc.splitmix64(tall.seed, 40 * 9000)
+    want = np.packbits(np.array([d < 2 ** 63 for d in dr], dtype=np.uint8).reshape(9000, 40), axis=1)
+    assert np.array_equal(tb, want)
+
+
 def test_oracle_against_live_reference(orc, ref):
     # When oracle/_ref is present: random geometries straddling byte/word edges.
     rng = np.random.default_rng(5)
