@@ -462,14 +462,19 @@ def run_ours(a):
                   "value": round(W * H / (ms3 / a.steps * 1e-3) / 1e9, 3),
                   "note": "the same graph with the unchanged-block skip " + ("on" if a.no_skip else "off")}
         other.close()
-        # one scan on an idle stream (CUDA events around the single launch)
-        plan.set_timing(True)
+        # one scan on an idle stream (CUDA events around the single launch), through a
+        # latency plan (YCHG_PLAN_LATENCY: one CTA per SM, what an isolated caller uses)
+        lp = y.Plan(Wimg, H, width_cnt=Ws, device=local, latency=True, skip=not a.no_skip)
+        lp.set_timing(True)
         isl = []
         for i in range(25):
-            scan(i, stream, sl=slots[1])
-            isl.append(plan.last_ms()[0] * 1e3)
-        plan.set_timing(False)
-        iso = round(sorted(isl[5:])[len(isl[5:]) // 2], 2)
+            b = bufs[i % nbuf]
+            lp.scan_device(b.data_ptr(), pitch, osl["counts"].data_ptr(), osl["flags"].data_ptr(),
+                           osl["bounds"].data_ptr(), osl["totals"].data_ptr(), stream.cuda_stream, with_links)
+            isl.append(lp.last_ms()[0] * 1e3)
+        iso = {"us": round(sorted(isl[5:])[len(isl[5:]) // 2], 2), "plan": "YCHG_PLAN_LATENCY",
+               "grid": lp.info().grid, "timing": "CUDA events around one launch on an idle stream, median of 20"}
+        lp.close()
     clk = clocks.stop()
 
     tot = last["totals"].cpu().tolist()
@@ -624,7 +629,7 @@ def run_ours(a):
                          "peak_source": peak_src,
                          "timing": ("CUDA events around a K-step CUDA graph replay" if graphed
                                     else "CUDA events around K eager steps") + (f"; a {HOLD_NOTE}" if held else "")},
-            "isolated_us": iso, "north_star_subset": alt, "skip_ab": noskip, "multi_gpu": comm,
+            "isolated_us": iso["us"] if iso else None, "isolated": iso, "north_star_subset": alt, "skip_ab": noskip, "multi_gpu": comm,
             "e2e": e2e, "e2e_dropin": e2e_dropin, "cpu_baseline": cpu, "parity": parity, "clocks": clk,
             "gpu_launches": info.kernels_per_scan * a.steps + (4 * a.steps if world > 1 else 0),  # + NCCL x2, K2 x2
             "totals": totals_json,

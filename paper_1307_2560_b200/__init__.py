@@ -101,6 +101,8 @@ _SIGS = {
     "ychg_stream_synchronize": (ctypes.c_int, [_vp]),
 }
 for _name, (_res, _args) in _SIGS.items():
+    if not hasattr(_lib, _name) and os.environ.get("YCHG_LIB"):
+        continue  # an older experimental build (A/B timing): only the entry points it has
     _fn = getattr(_lib, _name)
     _fn.restype = _res
     _fn.argtypes = _args
@@ -479,8 +481,8 @@ class Plan:
 
     def __init__(self, width_img: int, height: int, width_cnt: int | None = None, device: int = 0,
                  latency: bool = False, sync_inputs: bool = False, skip: bool = True):
-        """latency is accepted for compatibility (YCHG_PLAN_LATENCY, no effect: every
-        plan fills the GPU with one scan).  sync_inputs=True (YCHG_PLAN_SYNC_INPUTS):
+        """latency=True (YCHG_PLAN_LATENCY) sizes the launch for isolated scans (one CTA
+        per SM); the default favours back-to-back scans.  sync_inputs=True (YCHG_PLAN_SYNC_INPUTS):
         the scan kernel waits for the kernel launched just before it, for images
         written by that kernel.  skip=False (YCHG_PLAN_NO_SKIP): never skip 32-row
         blocks identical to the row above (same results; A/B timing)."""

@@ -104,17 +104,22 @@ struct ychg_plan {
 
 namespace {
 
-// Row segments per strip: about one CTA per SM for one scan.  Each SM then
-// streams one segment of every scan, back-to-back scans interleave their CTAs on
-// the SM's three slots (PDL), and every segment is long enough to amortise its
-// ramp (first TMA round trip) and merge; measured at 21000^2 hbands(147), K=100
-// graph: 1 CTA/SM (k=7) 9.1 us/scan, 1.4/SM (k=10) 9.9, 3/SM (k=21) 14.8.
+// Row segments per strip.  Back-to-back scans (the default plan, e.g. graph-
+// captured pipelines): about half a CTA per SM per scan -- consecutive scans then
+// interleave their CTAs on the SMs' three slots (PDL), every segment is long enough
+// to amortise its ramp (first TMA round trip), merge and strip finish, and ~5
+// scans are in flight (measured at 21000^2, K=100 graph, us/scan hbands(147) /
+// random(0.5): 0.57 CTA/SM (k=4) 9.05 / 11.9; 1 CTA/SM (k=7) 9.2 / 12.5; 3 CTA/SM
+// (k=21) 14.8 / 18).  An isolated scan (YCHG_PLAN_LATENCY, the host entry points)
+// instead wants one CTA per SM, all SMs streaming at once (25 vs 33 us at 21000^2).
 // Bounds: a segment holds <= kMaxSegmentRows rows (u16 partials), every warp band
 // gets >= 2 blocks (tiny masks: fewer, fuller segments), k <= kMaxSegPerStrip.
-int choose_segments(int n_strips, int n_blocks, int sms, int warps) {
+int choose_segments(int n_strips, int n_blocks, int sms, int warps, bool latency) {
     const int max_seg_blocks = ychg_dev::kMaxSegmentRows / ychg_dev::kBlockRows;
     const int kmin = std::max(1, (n_blocks + max_seg_blocks - 1) / max_seg_blocks);
-    int k = std::max(1, sms / std::max(1, n_strips));
+    const int ns = std::max(1, n_strips);
+    int k = latency ? sms / ns : (sms + ns) / (2 * ns);  // floor(sms / S) | round(sms / 2S)
+    k = std::max(1, k);
     k = std::min(k, std::max(1, n_blocks / (2 * warps)));
     k = std::min(k, ychg_dev::kMaxSegPerStrip);
     return std::max(k, kmin);
@@ -183,7 +188,7 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_path[path], ychg_scan_kernel_ptr(path), thr, smem));
             if (per_path[path] < 1) return fail(YCHG_ERR_CUDA, "scan kernel does not fit on an SM");
         }
-        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, warps[1]);
+        p.seg_per_strip = choose_segments(p.n_strips, p.n_blocks, sms, warps[1], (flags & YCHG_PLAN_LATENCY) != 0);
         // experiment hook (benchmarking only): force the segments per strip
         if (const char* v = getenv("YCHG_SEGMENTS"); v && *v)
             p.seg_per_strip = std::max(1, std::min(atoi(v), p.n_blocks));  // a segment must not be empty

@@ -68,11 +68,11 @@ __host__ __device__ constexpr int scan_smem() { return ScanSmem<scan_warps<kLink
 
 // What a strip's finisher publishes for the strips to its right: `status`
 // packs the epoch, the number of change flags strictly inside the strip and the
-// counts of its first and last column (counts < 2^21, i.e. height < 2^22);
-// `tstat` releases the strip's run and link totals.
+// counts of its first and last column (counts < 2^21, i.e. height < 2^22); it is
+// release-stored after the strip's run and link totals.
 struct StripRecord {
     unsigned long long status;  // epoch:12 | inside:10 | first:21 | last:21 (release-published)
-    unsigned long long tstat;   // epoch, release-published after runs/links
+    unsigned long long pad;
     long long runs;             // sum of the strip's counts
     long long links;            // K3 links of the strip's column pairs
 };

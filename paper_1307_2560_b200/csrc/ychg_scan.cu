@@ -115,9 +115,8 @@ struct Muls {
 
 // 32 rows from one TMA stage: 16 row pairs -> Harley-Seal tree -> ripple planes.
 // Rises of one column are never in consecutive rows, so a row pair contributes
-// (a0 & ~pa) | (a1 & ~a0): on the K3 path the two terms are a - (a & pa) from
-// k3_step's `apa`, disjoint, so the pair word is three IMADs on the FMA pipe
-// (the ALU pipe is the K3 path's bottleneck); the counts path keeps one LOP3.
+// (a0 & ~pa) | (a1 & ~a0) -- one LOP3 (moving it to the FMA pipe as
+// (a0 - a0&pa) + (a1 - a1&a0) with k3_step's `apa` measured 1 % slower: -DYCHG_P_FMA).
 // Links of one pair are likewise never in consecutive rows and are popcounted
 // per row pair.
 // kMask (strips with invalid column pairs -- the image's last column, or a
@@ -147,17 +146,15 @@ __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage,
                 b1 &= s.mk3;
             }
             uint32_t apa0, apa1;
-#ifdef YCHG_P_ALU  // A/B variant: the pair's rise word as one LOP3 (MSB-first words)
             const uint32_t pa_old = s.pa;
-#endif
             const uint32_t l0 = k3_step<kHead>(a0, b0, s, apa0);
             const uint32_t l1 = k3_step<kHead>(a1, b1, s, apa1);
             // l0 | l1 == l0 + l1 (disjoint); IMADs keep both adds off the ALU pipe
             s.links = __popc(l0 * mu.m1 + l1) * mu.m1 + s.links;
-#ifdef YCHG_P_ALU
-            P = lop3<0x3A>(a0, pa_old, a1);
+#ifdef YCHG_P_FMA  // A/B variant: the rise word as (a0 - a0&pa) + (a1 - a1&a0), 3 IMADs (1 % slower)
+            P = (apa0 * mu.mm1 + a0) * mu.m1 + (apa1 * mu.mm1 + a1);
 #else
-            P = (apa0 * mu.mm1 + a0) * mu.m1 + (apa1 * mu.mm1 + a1);  // (a0 - a0&pa) + (a1 - a1&a0)
+            P = lop3<0x3A>(a0, pa_old, a1);  // (a0 & ~pa) | (a1 & ~a0)
 #endif
         } else {
             P = lop3<0x3A>(raw0, s.pa, raw1);  // (a0 & ~pa) | (a1 & ~a0)
@@ -207,33 +204,31 @@ __device__ __forceinline__ void process_block(const uint8_t* __restrict__ stage,
 // True (warp-uniform) iff every row of the stage equals the row above it for
 // every word of the warp AND for the right-halo bit lane 31's pairs read: then
 // K1 sees no rise, and every K3 plane (cont == a|b, G2, G3, Hd, h1, h2, pa, pb)
-// maps to itself, so the block is a no-op and is skipped.  Rows 0..7 are tested
-// first, so a block that changes early (random masks) pays ~8 compares.
+// maps to itself, so the block is a no-op and is skipped.  Rows 0..1 are tested
+// first, so a block that changes early (dense content) pays two compares.
 // `phalo` carries the halo byte of the row above (row 31 of the previous block).
 __device__ __forceinline__ bool block_unchanged(const uint8_t* __restrict__ stage, int lane, uint32_t praw,
                                                 uint32_t& phalo) {
     const uint8_t* p = stage + 4 * lane;
-    uint32_t x[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) x[r] = *reinterpret_cast<const uint32_t*>(p + r * kBoxBytes);
     // right halo column (bit 7 of the halo's first byte): lane L holds row L
     const uint32_t hb = stage[lane * kBoxBytes + kStripBytes];
     uint32_t hprev = __shfl_up_sync(0xFFFFFFFFu, hb, 1);
     if (lane == 0) hprev = phalo;
-    // (x ^ y) | (z ^ x) = lop3 0x7E: two row compares per LOP3; 0xFE = 3-way OR
-    uint32_t d = lop3<0x28>(hb, hprev, 0x80u);  // (hb ^ hprev) & 0x80
-    d = lop3<0xFE>(d, lop3<0x7E>(x[0], praw, x[1]), lop3<0x7E>(x[2], x[1], x[3]));
-    d = lop3<0xFE>(d, lop3<0x7E>(x[4], x[3], x[5]), lop3<0x7E>(x[6], x[5], x[7]));
+    // (x ^ y) | (z ^ x) = lop3 0x7E: two row compares per LOP3; 0xFE = 3-way OR.
+    // Rows 0..1 first: a block that changes there (random masks) pays 2 loads + 2 LOP3.
+    const uint32_t x0 = *reinterpret_cast<const uint32_t*>(p);
+    const uint32_t x1 = *reinterpret_cast<const uint32_t*>(p + kBoxBytes);
+    uint32_t d = lop3<0xFE>(lop3<0x28>(hb, hprev, 0x80u), lop3<0x7E>(x0, praw, x1), 0u);
     if (__any_sync(0xFFFFFFFFu, d != 0u)) return false;
-    uint32_t prev = x[7];
+    uint32_t prev = x1;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        uint32_t y[8];
+    for (int c = 0; c < 5; ++c) {
+        uint32_t y[6];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) y[r] = *reinterpret_cast<const uint32_t*>(p + (8 + 8 * c + r) * kBoxBytes);
+        for (int r = 0; r < 6; ++r) y[r] = *reinterpret_cast<const uint32_t*>(p + (2 + 6 * c + r) * kBoxBytes);
         d = lop3<0xFE>(d, lop3<0x7E>(y[0], prev, y[1]), lop3<0x7E>(y[2], y[1], y[3]));
-        d = lop3<0xFE>(d, lop3<0x7E>(y[4], y[3], y[5]), lop3<0x7E>(y[6], y[5], y[7]));
-        prev = y[7];
+        d = lop3<0xFE>(d, lop3<0x7E>(y[4], y[3], y[5]), 0u);
+        prev = y[5];
     }
     const bool same = !__any_sync(0xFFFFFFFFu, d != 0u);
     phalo = __shfl_sync(0xFFFFFFFFu, hb, 31);
@@ -365,6 +360,7 @@ struct FinishSmem {
     unsigned long long red2[NW];
     long long base;
     long long n_total;            // boundaries up to and including this strip (right-most: the total)
+    long long tot_runs, tot_links;  // right-most strip: totals over every strip
     unsigned long long seglinks;  // links closed inside the strip's segments
     uint32_t edge;                // flag of the strip's first column
 };
@@ -498,7 +494,7 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local_sum += __shfl_xor_sync(0xFFFFFFFFu, local_sum, o);
     if (lane == 0) fs.red[warp] = local_sum;
-    // This parity's records (status and tstat/runs/links) were last read by the
+    // This parity's records (status, runs, links) were last read by the
     // scan two back: its finishers must all be done before any of them is
     // rewritten (normally long ago).
     if (tid == 0 && scan_no >= 2) {
@@ -513,7 +509,7 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
     int inside = 0;
     const int32_t first = fs.sc[0];
     if (warp == 0) {
-        // (3) publish this strip's record early: the strips to the right wait on it
+        // (3) boundary prefix of the strip's flag words
         const int c = __popc(fs.fw[lane]);
         int incl = c;
 #pragma unroll
@@ -523,11 +519,10 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
         }
         fs.wpre[lane] = incl - c;
         inside = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        if (lane == 0) st_release(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
     }
     // The look-back's first loads (records of up to 32 strips to the left) go out
-    // now and land while the K3 summaries are composed.  A record is one packed
-    // word validated by its epoch, so relaxed loads suffice.
+    // now and land while the K3 summaries are composed.  The status word is one
+    // packed value validated by its epoch, so relaxed loads suffice for it.
     unsigned long long lb = 0;
     if (warp == 0 && lane < s) lb = ld_relaxed(&recs[lane].status);
     // (2b) K3: stitch the strip's segment summaries top to bottom, kFinishChunk at
@@ -566,16 +561,18 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
     if (tid == 0) stamp(prm, scan_no, 18, globaltimer());
 
     if (warp == 0) {
-        // (4) release (runs, links) for the totals, then acquire every record to
-        // the left: boundary offset + this strip's first-column flag
+        // (4) publish the strip record -- runs and links, then the status word with
+        // one release (the strips to the right wait on it; the right-most strip
+        // reads every record's runs / links after acquiring its status) -- and
+        // acquire every record to the left: boundary offset + first-column flag
         if (lane == 0) {
             long long runs = 0;
             for (int w = 0; w < NW; ++w) runs += fs.red[w];
             rec->runs = runs;
             rec->links = static_cast<long long>(strip_links + (kLinks ? fs.seglinks : 0ull));
-            st_release(&rec->tstat, static_cast<unsigned long long>(epoch));
+            st_release(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
         }
-        long long off = 0;
+        long long off = 0, runs_l = 0, links_l = 0;
         int32_t carry_last = 0;  // last(j-1) entering each chunk; last(-1) := 0
         for (int jb = 0; jb < s; jb += 32) {
             const int j = jb + lane;
@@ -594,14 +591,33 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
             if (lane == 0) prev_last = carry_last;
             if (act) off += static_cast<long long>((st >> 42) & 0x3FFu) + (fj != prev_last ? 1 : 0);
             carry_last = __shfl_sync(0xFFFFFFFFu, lj, (s - 1 - jb) < 31 ? (s - 1 - jb) : 31);
+            if (last_strip) {
+                // the statuses were observed with relaxed loads: fence before the
+                // runs / links they publish are read
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                if (act) {
+                    runs_l += __ldcg(&recs[j].runs);
+                    links_l += __ldcg(&recs[j].links);
+                }
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            off += __shfl_xor_sync(0xFFFFFFFFu, off, o);
+            runs_l += __shfl_xor_sync(0xFFFFFFFFu, runs_l, o);
+            links_l += __shfl_xor_sync(0xFFFFFFFFu, links_l, o);
+        }
         if (lane == 0) {
             stamp(prm, scan_no, 19, globaltimer());
             fs.edge = (first != carry_last) ? 1u : 0u;
             fs.base = off;
             fs.n_total = off + static_cast<long long>(first != carry_last) + inside;
+            if (last_strip) {  // this strip's own record + every record to the left
+                long long runs = 0;
+                for (int w = 0; w < NW; ++w) runs += fs.red[w];
+                fs.tot_runs = runs_l + runs;
+                fs.tot_links = links_l + static_cast<long long>(strip_links + (kLinks ? fs.seglinks : 0ull));
+            }
         }
     }
     // (5) the outputs are shared with the previous scan: its finishers must be done
@@ -627,36 +643,11 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
             prm.boundaries[fs.base + e + fs.wpre[wi] + __popc(m & ((1u << lane) - 1u))] = w * 32 + lane;
     }
 
-    // (6) the right-most strip also writes run/link totals once every strip released them
-    if (last_strip && warp == 0) {
-        long long runs = 0, links = 0;
-        for (int jb = 0; jb < S; jb += 32) {
-            const int j = jb + lane;
-            const bool act = j < S;
-            unsigned long long vv = 0;
-            bool ok = !act;
-            while (true) {
-                if (!ok) {
-                    vv = ld_acquire(&recs[j].tstat);
-                    ok = static_cast<uint32_t>(vv) == epoch;
-                }
-                if (__all_sync(0xFFFFFFFFu, ok)) break;
-            }
-            if (act) {
-                runs += __ldcg(&recs[j].runs);
-                links += __ldcg(&recs[j].links);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            runs += __shfl_xor_sync(0xFFFFFFFFu, runs, o);
-            links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
-        }
-        if (lane == 0) {
-            prm.totals[0] = runs;
-            prm.totals[1] = kLinks ? links : 0;
-            prm.totals[2] = kLinks ? runs - links : -1;
-        }
+    // (6) the right-most strip writes the run / link / hyperedge totals
+    if (last_strip && tid == 0) {
+        prm.totals[0] = fs.tot_runs;
+        prm.totals[1] = kLinks ? fs.tot_links : 0;
+        prm.totals[2] = kLinks ? fs.tot_runs - fs.tot_links : -1;
     }
     if (tid == 0) stamp(prm, scan_no, 21, globaltimer());
     __syncthreads();
@@ -800,12 +791,28 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             s.pab = s.pa & s.pb;
 
             int since_flush = 0;
+            int fails = 0, untested = 0;  // unchanged-block test back-off (warp-uniform)
             for (int bi = 0; bi < nb; ++bi) {
                 const int st = it % kS;
                 mbar_wait(&my_bars[st], (it / kS) & 1u);
                 if (bi == 0 && tid == 0 && seg_i == 0) stamp(prm, scan_idx, 6, globaltimer());
                 const uint8_t* sp = my_stages + st * kStageBytes;
-                const bool skip = kLinks && prm.skip_same && block_unchanged(sp, lane, s.praw, phalo);
+                // The unchanged-block test backs off on dense content: after f
+                // consecutive changed blocks the next 2^(f-1) - 1 blocks are not tested
+                // (a random mask pays ~5 tests per band; a banded one, whose changed
+                // blocks are isolated, still tests every block).
+                bool skip = false;
+                if (kLinks && prm.skip_same) {
+                    if (untested > 0) {
+                        --untested;
+                    } else if (block_unchanged(sp, lane, s.praw, phalo)) {
+                        skip = true;
+                        fails = 0;
+                    } else {
+                        fails = fails < 5 ? fails + 1 : 5;
+                        untested = (1 << (fails - 1)) - 1;
+                    }
+                }
                 if (!skip) {
 #ifdef YCHG_NO_HEAD  // diagnostics build: never take the head-mode block (wrong results, timing only)
                     if (false)
