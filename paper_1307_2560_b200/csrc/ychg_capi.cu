@@ -1633,10 +1633,26 @@ extern "C" int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold,
 // round-robin over the given devices, one host thread per device; the strip
 // counts are gathered, K2 runs once over them (ychg_detect_boundary_columns), and
 // runs / links add up (a strip counts its own pairs, the halo one included).
+namespace {
+// Restores the calling thread's current device on scope exit: the sharded entry
+// point switches devices (peer access, the gathering device) and must not leave
+// a caller such as torch on another one.
+struct DeviceRestore {
+    int prev = -1;
+    DeviceRestore() {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    }
+    ~DeviceRestore() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
 extern "C" int ychg_scan_host_sharded(const uint8_t* bits, int32_t width, int32_t height, int64_t row_stride,
                                       int32_t n_parts, const int32_t* devices, int32_t n_devices,
                                       int32_t with_hyperedges, int32_t* counts_out, int32_t* boundaries_out,
                                       ychg_totals* totals_out) {
+    const DeviceRestore restore_device;
     if (width < 0 || height < 0) return fail(YCHG_ERR_INVALID, "scan_sharded: negative geometry %dx%d", width, height);
     if (n_parts < 1) return fail(YCHG_ERR_INVALID, "scan_sharded: n_parts must be >= 1, got %d", n_parts);
     const int64_t row_bytes = (int64_t(width) + 7) / 8;

@@ -723,3 +723,36 @@ def test_column_runs_byte_column_path(gpu, orc, ref):
     for col in (0, 4, 8):
         got = y.column_runs(img, col)
         assert got.shape[0] > 65536 and np.array_equal(got, rimg.column_runs(col)), col
+
+
+def test_scan_sharded_restores_caller_device(gpu, orc):
+    """ychg_scan_host_sharded switches devices internally (peer access, the gathering
+    device); the caller's current device must be the same afterwards."""
+    import ctypes
+    y = gpu
+    sp = Spec.random(3000, 200, 0.5, 8)
+    img = y.BinaryImage(sp.width, sp.height, orc.synth(sp))
+    rt = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    n = y.device_count()
+    for dev in range(min(n, 2)):
+        y._check(y._lib.ychg_set_device(dev), "set_device")
+        y.scan_sharded(img, 3, devices=list(range(n))[:2])
+        if rt is not None:
+            cur = ctypes.c_int(-1)
+            rt.cudaGetDevice(ctypes.byref(cur))
+            assert cur.value == dev
+    y._check(y._lib.ychg_set_device(0), "set_device")
+
+
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2", reason="needs two GPUs (peer stores over NVLink)")
+def test_scan_sharded_peer_gather_two_devices(gpu, orc):
+    """Strips on two devices: the finishers on device 1 store their counts straight
+    into the gathering array on device 0 (peer pointers), bit-exact with one device."""
+    y = gpu
+    for sp in (Spec.random(9000, 700, 0.5, 12), Spec.hbands(5000, 600, 37)):
+        img = y.BinaryImage(sp.width, sp.height, orc.synth(sp))
+        want = y.scan(img)
+        for n in (2, 3, 4):
+            got = y.scan_sharded(img, n, devices=[0, 1])
+            assert np.array_equal(got.counts, want.counts) and np.array_equal(got.boundaries, want.boundaries)
+            assert (got.total_runs, got.links, got.hyperedges) == (want.total_runs, want.links, want.hyperedges)
