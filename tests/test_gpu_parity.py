@@ -732,15 +732,14 @@ def test_scan_sharded_restores_caller_device(gpu, orc):
     y = gpu
     sp = Spec.random(3000, 200, 0.5, 8)
     img = y.BinaryImage(sp.width, sp.height, orc.synth(sp))
-    rt = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    drv = ctypes.CDLL("libcuda.so.1")  # the driver's current context is the thread's current device
     n = y.device_count()
     for dev in range(min(n, 2)):
         y._check(y._lib.ychg_set_device(dev), "set_device")
         y.scan_sharded(img, 3, devices=list(range(n))[:2])
-        if rt is not None:
-            cur = ctypes.c_int(-1)
-            rt.cudaGetDevice(ctypes.byref(cur))
-            assert cur.value == dev
+        cur = ctypes.c_int(-1)
+        assert drv.cuCtxGetDevice(ctypes.byref(cur)) == 0
+        assert cur.value == dev
     y._check(y._lib.ychg_set_device(0), "set_device")
 
 
