@@ -22,8 +22,9 @@ __device__ __forceinline__ void process_block_ilp(const uint8_t* const* stage, i
             const uint32_t P = lop3<0x3A>(a0, s[j].pa, a1);
             const uint32_t b0 = right_neighbour_msb(a0, r0[4], mul2, mulnb);
             const uint32_t b1 = right_neighbour_msb(a1, r1[4], mul2, mulnb);
-            const uint32_t l0 = k3_step<false>(a0, b0, s[j]);
-            const uint32_t l1 = k3_step<false>(a1, b1, s[j]);
+            uint32_t apa0, apa1;
+            const uint32_t l0 = k3_step<false>(a0, b0, s[j], apa0);
+            const uint32_t l1 = k3_step<false>(a1, b1, s[j], apa1);
             s[j].links = __popc(l0 * mul1 + l1) * mul1 + s[j].links;
             if ((q & 1) == 0) { Pprev[j] = P; continue; }
             const int m = q >> 1;
