@@ -111,14 +111,20 @@ namespace {
 // scans are in flight (measured at 21000^2, K=100 graph, us/scan hbands(147) /
 // random(0.5): 0.57 CTA/SM (k=4) 9.05 / 11.9; 1 CTA/SM (k=7) 9.2 / 12.5; 3 CTA/SM
 // (k=21) 14.8 / 18).  An isolated scan (YCHG_PLAN_LATENCY, the host entry points)
-// instead wants one CTA per SM, all SMs streaming at once (25 vs 33 us at 21000^2).
+// instead wants every SM streaming at once with more bytes in flight: two CTAs
+// per SM (21000^2 hbands / random, one launch, CUDA events: 1/SM 33.4 / 39.0 us,
+// 2/SM 28.8 / 34.7, 3/SM 29.5 / 35.5).
 // Bounds: a segment holds <= kMaxSegmentRows rows (u16 partials), every warp band
 // gets >= 2 blocks (tiny masks: fewer, fuller segments), k <= kMaxSegPerStrip.
 int choose_segments(int n_strips, int n_blocks, int sms, int warps, bool latency) {
     const int max_seg_blocks = ychg_dev::kMaxSegmentRows / ychg_dev::kBlockRows;
     const int kmin = std::max(1, (n_blocks + max_seg_blocks - 1) / max_seg_blocks);
     const int ns = std::max(1, n_strips);
-    int k = latency ? sms / ns : (sms + ns) / (2 * ns);  // floor(sms / S) | round(sms / 2S)
+    static const int lat_per_sm = [] {
+        const char* v = getenv("YCHG_LAT_CTAS_PER_SM");  // A/B timing hook (default 2)
+        return v && *v ? std::max(1, atoi(v)) : 2;
+    }();
+    int k = latency ? lat_per_sm * sms / ns : (sms + ns) / (2 * ns);  // floor(sms / S) | round(sms / 2S)
     k = std::max(1, k);
     k = std::min(k, std::max(1, n_blocks / (2 * warps)));
     k = std::min(k, ychg_dev::kMaxSegPerStrip);
@@ -176,6 +182,11 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         p.wait_inputs = (flags & YCHG_PLAN_SYNC_INPUTS) ? 1 : 0;
         p.skip_same = (flags & YCHG_PLAN_NO_SKIP) ? 0 : 1;
         if (const char* v = getenv("YCHG_NO_SKIP"); v && v[0] == '1') p.skip_same = 0;  // A/B timing hook
+        // An isolated scan starts every CTA at once: one box per warp first gets each
+        // warp's data back sooner, the rest of the ring follows (pipelined plans
+        // start CTAs one by one as slots free, the whole ring at once)
+        p.ramp_boxes = (flags & YCHG_PLAN_LATENCY) ? 1 : 0;
+        if (const char* v = getenv("YCHG_RAMP_BOXES"); v && *v) p.ramp_boxes = atoi(v);  // A/B timing hook
         // Resident CTAs per SM of each path's kernel (its grid is capped to what is
         // resident: a strip finisher may wait on other CTAs of the same scan).
         if (const int rc2 = ychg_scan_kernel_prepare())

@@ -68,13 +68,14 @@ __host__ __device__ constexpr int scan_smem() { return ScanSmem<scan_warps<kLink
 
 // What a strip's finisher publishes for the strips to its right: `status`
 // packs the epoch, the number of change flags strictly inside the strip and the
-// counts of its first and last column (counts < 2^21, i.e. height < 2^22); it is
-// release-stored after the strip's run and link totals.
+// counts of its first and last column (counts < 2^21, i.e. height < 2^22).  The
+// run and link totals carry the epoch too, so the three words need no ordering
+// fence: a reader polls each word until its epoch matches.
 struct StripRecord {
-    unsigned long long status;  // epoch:12 | inside:10 | first:21 | last:21 (release-published)
+    unsigned long long status;  // epoch:12 | inside:10 | first:21 | last:21
     unsigned long long pad;
-    long long runs;             // sum of the strip's counts
-    long long links;            // K3 links of the strip's column pairs
+    unsigned long long runs;    // epoch:12 | sum of the strip's counts:52
+    unsigned long long links;   // epoch:12 | K3 links of the strip's column pairs:52
 };
 
 // ----------------------------------------------------------------------------
@@ -96,6 +97,7 @@ struct ScanParams {
     uint32_t mul2, mulnb;     // 2 and 1 << 25 as runtime values: keeps the b-word shifts on IMAD
     uint32_t mul1, mulm1;     // 1 and -1 as runtime values: keeps disjoint adds / subset subtracts on IMAD
     int32_t skip_same;        // 1: skip 32-row blocks identical to the row above (state is unchanged)
+    int32_t ramp_boxes;       // TMA boxes a warp issues at its band's start (the rest after the first lands)
     // per scan parity (two halves: scan t+1 fills one while scan t's finishers read the other)
     uint32_t* part;           // [2][n_segments][512] per-segment u16x2 column counts
     uint32_t* sums;           // [2][n_segments][7][32] K3 band summaries (one per segment)

@@ -277,9 +277,10 @@ __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long lon
     return v;
 }
 
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+
 
 __device__ __forceinline__ BandSummary load_summary(const uint32_t* a, int lane) {
     return BandSummary{a[lane], a[32 + lane], a[64 + lane], a[96 + lane], a[128 + lane], a[160 + lane], a[192 + lane]};
@@ -472,10 +473,6 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
         fs.sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(hi[q]);
     }
     __syncthreads();
-    if (tid == 0 && k <= kFinishChunk) {
-        // every input of this half is read: scan t+2 may overwrite it
-        st_release(prm.fin_loaded + par * S + s, scan_no + 1);
-    }
     if (tid == 0) stamp(prm, scan_no, 16, globaltimer());
 
     // (2) flags strictly inside the strip (columns 1..1023), run total
@@ -557,7 +554,6 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
             strip_links += m;
         }
     }
-    if (tid == 0 && k > kFinishChunk) st_release(prm.fin_loaded + par * S + s, scan_no + 1);
     if (tid == 0) stamp(prm, scan_no, 18, globaltimer());
 
     if (warp == 0) {
@@ -568,9 +564,12 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
         if (lane == 0) {
             long long runs = 0;
             for (int w = 0; w < NW; ++w) runs += fs.red[w];
-            rec->runs = runs;
-            rec->links = static_cast<long long>(strip_links + (kLinks ? fs.seglinks : 0ull));
-            st_release(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
+            // three self-validating words (each carries the scan epoch): no fence
+            // orders them, a reader polls each until its epoch matches
+            const unsigned long long tag = static_cast<unsigned long long>(epoch & 0xFFFu) << 52;
+            st_relaxed(&rec->runs, tag | static_cast<unsigned long long>(runs));
+            st_relaxed(&rec->links, tag | (strip_links + (kLinks ? fs.seglinks : 0ull)));
+            st_relaxed(&rec->status, pack_strip_status(epoch, inside, first, fs.sc[kStripCols - 1]));
         }
         long long off = 0, runs_l = 0, links_l = 0;
         int32_t carry_last = 0;  // last(j-1) entering each chunk; last(-1) := 0
@@ -591,13 +590,22 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
             if (lane == 0) prev_last = carry_last;
             if (act) off += static_cast<long long>((st >> 42) & 0x3FFu) + (fj != prev_last ? 1 : 0);
             carry_last = __shfl_sync(0xFFFFFFFFu, lj, (s - 1 - jb) < 31 ? (s - 1 - jb) : 31);
-            if (last_strip) {
-                // the statuses were observed with relaxed loads: fence before the
-                // runs / links they publish are read
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            if (last_strip) {  // every record's epoch-tagged run and link words
+                unsigned long long rw = 0, lw = 0;
+                bool rok = !act, lok = !act;
+                while (!__all_sync(0xFFFFFFFFu, rok && lok)) {
+                    if (!rok) {
+                        rw = ld_relaxed(&recs[j].runs);
+                        rok = static_cast<uint32_t>(rw >> 52) == (epoch & 0xFFFu);
+                    }
+                    if (!lok) {
+                        lw = ld_relaxed(&recs[j].links);
+                        lok = static_cast<uint32_t>(lw >> 52) == (epoch & 0xFFFu);
+                    }
+                }
                 if (act) {
-                    runs_l += __ldcg(&recs[j].runs);
-                    links_l += __ldcg(&recs[j].links);
+                    runs_l += static_cast<long long>(rw & 0xFFFFFFFFFFFFFull);
+                    links_l += static_cast<long long>(lw & 0xFFFFFFFFFFFFFull);
                 }
             }
         }
@@ -654,7 +662,10 @@ __device__ void finish_strip(const ScanParams& prm, int s, unsigned long long sc
     if (tid == 0) {
         stamp(prm, scan_no, 4, globaltimer());
         stamp(prm, scan_no, 10, scan_no + 1);
+        // one fence for both: this half's partials are consumed (scan t+2 may refill
+        // them), and every record / output write of this finish precedes fin_all
         __threadfence();
+        st_relaxed(prm.fin_loaded + par * S + s, scan_no + 1);
         atomicAdd(prm.fin_all, 1ull);
     }
 }
@@ -673,12 +684,13 @@ __device__ __forceinline__ void band_of(const ScanParams& prm, int seg, int warp
     nb = sb0 + ((warp + 1) * nseg) / NW - wb0;
 }
 
-// Lane 0: fill the first stages of the warp's TMA ring for a band.
+// Lane 0: fill the first `n` stages of the warp's TMA ring for a band (blocks
+// i0 .. i0+n-1 of the band into stages it+i0 ...).
 template <int kS>
 __device__ __forceinline__ void kick_ring(const CUtensorMap* tmap, uint8_t* my_stages, uint64_t* my_bars,
-                                          uint32_t it, int x0, int wb0, int nb) {
-    const int npre = nb < kS ? nb : kS;
-    for (int i = 0; i < npre; ++i) {
+                                          uint32_t it, int x0, int wb0, int nb, int i0 = 0, int n = kS) {
+    const int npre = nb < i0 + n ? nb : i0 + n;
+    for (int i = i0; i < npre; ++i) {
         const int st = (it + i) % kS;
         mbar_arrive_expect_tx(&my_bars[st], kStageBytes);
         tma_load_2d(my_stages + st * kStageBytes, tmap, &my_bars[st], x0, (wb0 + i) * kBlockRows);
@@ -707,6 +719,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     uint8_t* my_stages = stages + warp * kS * kStageBytes;
     uint64_t* my_bars = bars + warp * kS;
     const bool have_seg = static_cast<int>(blockIdx.x) < prm.n_segments;
+    const int ramp = (prm.ramp_boxes >= 1 && prm.ramp_boxes < kS) ? prm.ramp_boxes : kS;  // boxes issued at a band's start
 
     // Each warp owns its ring: lane 0 initialises the warp's barriers and -- unless
     // the image is still being written by the preceding kernel -- starts the first
@@ -717,7 +730,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         if (have_seg && !prm.wait_inputs) {
             int strip, nseg, wb0, nb;
             band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
-            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb);
+            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb, 0, ramp);
         }
     }
     // This CTA's scan number for each of its segments, drawn BEFORE triggering the
@@ -740,7 +753,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         if (lane == 0 && have_seg) {
             int strip, nseg, wb0, nb;
             band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
-            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb);
+            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb, 0, ramp);
         }
     }
     if (tid == 0 && have_seg) stamp(prm, seg_tick[0], 0, t_entry);
@@ -769,7 +782,7 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
         uint32_t O = 0;
 
         if (nb > 0) {
-            if (seg_i > 0 && lane == 0) kick_ring<kS>(&tmap, my_stages, my_bars, it, x0, wb0, nb);
+            if (seg_i > 0 && lane == 0) kick_ring<kS>(&tmap, my_stages, my_bars, it, x0, wb0, nb, 0, ramp);
             // Halo row y0-1 (the reference's prev row, runscan.cpp:45; zero above row 0).
             const int y0 = wb0 * kBlockRows;
             uint32_t raw = 0, nbyte = 0;
@@ -795,7 +808,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
             for (int bi = 0; bi < nb; ++bi) {
                 const int st = it % kS;
                 mbar_wait(&my_bars[st], (it / kS) & 1u);
-                if (bi == 0 && tid == 0 && seg_i == 0) stamp(prm, scan_idx, 6, globaltimer());
+                if (bi == 0) {
+                    // a short ramp (ramp_boxes < kS) gets each warp's first box back sooner
+                    // when every CTA starts at once; the rest of the ring follows it
+                    if (lane == 0 && ramp < kS) kick_ring<kS>(&tmap, my_stages, my_bars, it, x0, wb0, nb, ramp, kS - ramp);
+                    if (tid == 0 && seg_i == 0) stamp(prm, scan_idx, 6, globaltimer());
+                }
                 const uint8_t* sp = my_stages + st * kStageBytes;
                 // The unchanged-block test backs off on dense content: after f
                 // consecutive changed blocks the next 2^(f-1) - 1 blocks are not tested

@@ -27,7 +27,7 @@ for k in ks:
     else:
         os.environ.pop("YCHG_SEGMENTS", None)
     for skip in (True, False):
-        plan = y.Plan(W, H, skip=skip)
+        plan = y.Plan(W, H, skip=skip, latency=True)
         info = plan.info()
         plan.set_timing(True)
         for links in (True, False):
