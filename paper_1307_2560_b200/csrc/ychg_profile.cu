@@ -39,6 +39,7 @@ struct ProfileArgs {
     int32_t width, height, row_bytes;
     int32_t n_words;   // ceil(width / 32)
     int32_t n_bands;   // ceil(height / kBandRows)
+    int32_t band_major;  // fill grid order: 1 = consecutive warps take consecutive words of one band
 };
 
 // Word `w` of row y in MSB-first column order (bit 31 - j = column 32w + j),
@@ -258,7 +259,12 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
     const int gw = blockIdx.x * kFillWarps + wib;
     const int lane = threadIdx.x & 31;
     if (gw >= a.n_words * a.n_bands) return;
-    const int w = gw / a.n_bands, band = gw - w * a.n_bands;  // consecutive warps: bands of one word
+    // Grid order.  Word-major (consecutive warps: bands of one word) keeps each
+    // lane's output stream local; band-major (consecutive warps and CTAs: words of
+    // one band) reads each 32 B row sector of the mask in 8 nearby warps at once
+    // (L1/L2 hits instead of one DRAM re-read per word).
+    const int w = a.band_major ? gw % a.n_words : gw / a.n_bands;
+    const int band = a.band_major ? gw / a.n_words : gw - w * a.n_bands;
     const int c = 32 * w + 8 * (lane >> 3) + 7 - (lane & 7);
     const bool live = c < a.width;
     const int y0 = band * kBandRows;
@@ -386,6 +392,8 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
     a.row_bytes = (width + 7) / 8;
     a.n_words = (width + 31) / 32;
     a.n_bands = (height + kBandRows - 1) / kBandRows;
+    a.band_major = -1;
+    if (const char* v = std::getenv("YCHG_FILL_BAND_MAJOR"); v && *v) a.band_major = std::atoi(v);  // A/B hook
     const int strips = (a.n_words + 31) / 32;
     const int warps = strips * a.n_bands;
     const int blocks = (warps + 7) / 8;
@@ -408,6 +416,11 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
             else if (!std::strcmp(f, "rowwise")) kind = 1;
             else if (!std::strcmp(f, "staged")) kind = 2;
         }
+        // Grid order (profiles/r02_fill_ncu.md, 21000^2): band-major for the staged
+        // kernel (checker(7) 552 -> 498 us, random 1154 -> 1053, checker(21) 334 -> 239)
+        // and for the direct walk on very sparse masks (hbands 100 -> 77 us);
+        // word-major for the direct walk otherwise (checker(21) 197 vs 216 us).
+        if (a.band_major < 0) a.band_major = (kind == 2 || rho < 0.01) ? 1 : 0;
         if (kind == 0) {
             constexpr int wpc = fill_warps_per_cta<false>();
             profile_fill_kernel<false><<<static_cast<unsigned>((fill_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
