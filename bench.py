@@ -472,8 +472,18 @@ def run_ours(a):
             lp.scan_device(b.data_ptr(), pitch, osl["counts"].data_ptr(), osl["flags"].data_ptr(),
                            osl["bounds"].data_ptr(), osl["totals"].data_ptr(), stream.cuda_stream, with_links)
             isl.append(lp.last_ms()[0] * 1e3)
+        # the same measurement of a near-empty kernel: the event/launch floor of any single launch
+        fl = []
+        for i in range(25):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            torch.cuda._sleep(1)
+            e1.record(stream)
+            e1.synchronize()
+            fl.append(e0.elapsed_time(e1) * 1e3)
         iso = {"us": round(sorted(isl[5:])[len(isl[5:]) // 2], 2), "plan": "YCHG_PLAN_LATENCY",
-               "grid": lp.info().grid, "timing": "CUDA events around one launch on an idle stream, median of 20"}
+               "grid": lp.info().grid, "timing": "CUDA events around one launch on an idle stream, median of 20",
+               "empty_kernel_us": round(sorted(fl[5:])[len(fl[5:]) // 2], 2)}
         lp.close()
     clk = clocks.stop()
 

@@ -684,6 +684,22 @@ __device__ __forceinline__ void band_of(const ScanParams& prm, int seg, int warp
     nb = sb0 + ((warp + 1) * nseg) / NW - wb0;
 }
 
+// Halo row wb0*32 - 1 of a band (the reference's previous row, runscan.cpp:45;
+// zero above row 0): this lane's 4 bytes and the next byte.
+__device__ __forceinline__ void load_halo_row(const ScanParams& prm, int wb0, int x0, int lane, uint32_t& raw,
+                                              uint32_t& nbyte) {
+    const int y0 = wb0 * kBlockRows;
+    raw = nbyte = 0;
+    if (y0 > 0) {
+        const uint8_t* row = prm.bits + static_cast<int64_t>(y0 - 1) * prm.pitch;
+        const int c = x0 + 4 * lane;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (c + q < prm.row_bytes) raw |= static_cast<uint32_t>(__ldg(row + c + q)) << (8 * q);
+        if (c + 4 < prm.row_bytes) nbyte = __ldg(row + c + 4);
+    }
+}
+
 // Lane 0: fill the first `n` stages of the warp's TMA ring for a band (blocks
 // i0 .. i0+n-1 of the band into stages it+i0 ...).
 template <int kS>
@@ -724,14 +740,18 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     // Each warp owns its ring: lane 0 initialises the warp's barriers and -- unless
     // the image is still being written by the preceding kernel -- starts the first
     // band's loads right away, so the TMA round trip overlaps the ticket draw.
-    if (lane == 0) {
-        for (int i = 0; i < kS; ++i) mbar_init(&my_bars[i], 1);
-        fence_proxy_async();
-        if (have_seg && !prm.wait_inputs) {
-            int strip, nseg, wb0, nb;
-            band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
-            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb, 0, ramp);
+    uint32_t halo_raw = 0, halo_nb = 0;  // the first band's halo row (loaded with the first boxes)
+    {
+        int strip = 0, nseg = 0, wb0 = 0, nb = 0;
+        if (have_seg) band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
+        if (lane == 0) {
+            for (int i = 0; i < kS; ++i) mbar_init(&my_bars[i], 1);
+            fence_proxy_async();
+            if (have_seg && !prm.wait_inputs)
+                kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb, 0, ramp);
         }
+        // the halo row's loads overlap the TMA round trip and the ticket atomic below
+        if (have_seg && nb > 0 && !prm.wait_inputs) load_halo_row(prm, wb0, strip * kStripBytes, lane, halo_raw, halo_nb);
     }
     // This CTA's scan number for each of its segments, drawn BEFORE triggering the
     // next scan's launch: tickets then follow launch order even when consecutive
@@ -750,10 +770,11 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     // flush before its first load; back-to-back scans read images written long before.
     if (prm.wait_inputs) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (lane == 0 && have_seg) {
+        if (have_seg) {
             int strip, nseg, wb0, nb;
             band_of<NW>(prm, blockIdx.x, warp, strip, nseg, wb0, nb);
-            kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb, 0, ramp);
+            if (lane == 0) kick_ring<kS>(&tmap, my_stages, my_bars, 0u, strip * kStripBytes, wb0, nb, 0, ramp);
+            if (nb > 0) load_halo_row(prm, wb0, strip * kStripBytes, lane, halo_raw, halo_nb);
         }
     }
     if (tid == 0 && have_seg) stamp(prm, seg_tick[0], 0, t_entry);
@@ -783,17 +804,10 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 
         if (nb > 0) {
             if (seg_i > 0 && lane == 0) kick_ring<kS>(&tmap, my_stages, my_bars, it, x0, wb0, nb, 0, ramp);
-            // Halo row y0-1 (the reference's prev row, runscan.cpp:45; zero above row 0).
-            const int y0 = wb0 * kBlockRows;
-            uint32_t raw = 0, nbyte = 0;
-            if (y0 > 0) {
-                const uint8_t* row = prm.bits + static_cast<int64_t>(y0 - 1) * prm.pitch;
-                const int c = x0 + 4 * lane;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (c + q < prm.row_bytes) raw |= static_cast<uint32_t>(__ldg(row + c + q)) << (8 * q);
-                if (c + 4 < prm.row_bytes) nbyte = __ldg(row + c + 4);
-            }
+            // Halo row y0-1 (the reference's prev row, runscan.cpp:45; zero above row 0),
+            // for the first segment already loaded at CTA entry
+            uint32_t raw = halo_raw, nbyte = halo_nb;
+            if (seg_i > 0) load_halo_row(prm, wb0, x0, lane, raw, nbyte);
             s.praw = raw;
             uint32_t phalo = __shfl_sync(0xFFFFFFFFu, nbyte, 31);  // right-halo byte of the row above
             s.pa = kLinks ? __byte_perm(raw, 0u, 0x0123u) : raw;     // word order of process_block<kLinks>

@@ -58,8 +58,8 @@ for k in ks:
         os.environ["YCHG_SEGMENTS"] = k
     else:
         os.environ.pop("YCHG_SEGMENTS", None)
-    for links in (True,):
-        plan = y.Plan(W, H)
+    for links in ((True, False) if os.environ.get("YCHG_TL_COUNTS") == "1" else (True,)):
+        plan = y.Plan(W, H, latency=os.environ.get("YCHG_TL_LATENCY") == "1")
         info = plan.info()
         print(f"{S}^2 {pat} k={info.seg_per_strip} grid={info.grid} links={links}", flush=True)
         plan.debug_stamps(True)
