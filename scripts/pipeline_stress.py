@@ -1,7 +1,8 @@
 """Long randomized stress of the pipelined scan (not part of the test suite):
-random geometries, segment counts and grids; CUDA graphs of back-to-back scans of
-distinct images, full and counts-only mixed; every output checked against the
-oracle; a stall aborts after 20 s.  Usage: python scripts/pipeline_stress.py [trials] [seed]"""
+random geometries, segment counts and grids, latency / default plans, the
+unchanged-block skip on and off, random / banded / checker content; CUDA graphs
+of back-to-back scans of distinct images, full and counts-only mixed; every
+output checked against the oracle; a stall aborts after 20 s.  Usage: python scripts/pipeline_stress.py [trials] [seed]"""
 import os
 import sys
 import time
@@ -22,8 +23,14 @@ for trial in range(trials):
     H = int(rng.choice([1, 2, 31, 32, 33, 63, 64, 65, 257, 1000, 2500, 4000]))
     os.environ["YCHG_SEGMENTS"] = str(int(rng.integers(1, 12)))
     os.environ["YCHG_GRID"] = str(int(rng.choice([1, 2, 3, 5, 1000])))
-    specs = [Spec.random(W, H, float(rng.choice([0.05, 0.3, 0.5, 0.7, 0.95])), int(rng.integers(0, 1 << 40)))
-             for _ in range(3)]
+    def pick():
+        kind = int(rng.integers(0, 4))
+        if kind == 1 and H >= 2:
+            return Spec.hbands(W, H, int(rng.integers(1, max(2, H // 2 + 1))))
+        if kind == 2:
+            return Spec.checker(W, H, int(rng.choice([1, 3, 7, 33, 100])))
+        return Spec.random(W, H, float(rng.choice([0.05, 0.3, 0.5, 0.7, 0.95])), int(rng.integers(0, 1 << 40)))
+    specs = [pick() for _ in range(3)]
     pitch = y.pitch_for(W)
     imgs = []
     for sp in specs:
@@ -33,7 +40,7 @@ for trial in range(trials):
         counts = orc.counts(bits, W)
         imgs.append((torch.from_numpy(dev).cuda(), counts, orc.boundaries(counts), orc.hyperedges(bits, W)[0]))
     try:
-        plan = y.Plan(W, H)
+        plan = y.Plan(W, H, latency=bool(rng.integers(0, 2)), skip=bool(rng.integers(0, 4)))
     except y.ValidationError:
         continue  # e.g. more segments per CTA than supported with a tiny forced grid
     n = int(rng.integers(2, 13))
