@@ -73,11 +73,13 @@ HOLD_NOTE = ("spin kernel holds the stream while the host submits the timed work
              "measures device execution, not graph-submission latency (nvbench's blocking-kernel method)")
 
 
-def hold_stream(stream, steps: int) -> bool:
-    """Spin ~10 us of submission budget per step (>= 0.2 ms) before the start event;
-    YCHG_BENCH_HOLD_CYCLES overrides (0 disables)."""
+def hold_stream(stream, steps: int, per_step_cycles: int = 20_000) -> bool:
+    """Spin before the start event: ~10 us of submission budget per step for one
+    graph launch (>= 0.2 ms), ~100 us per step when the steps are submitted
+    eagerly (collectives + kernels per step); YCHG_BENCH_HOLD_CYCLES overrides (0
+    disables)."""
     v = os.environ.get("YCHG_BENCH_HOLD_CYCLES")
-    n = int(v) if v is not None else max(400_000, 20_000 * steps)
+    n = int(v) if v is not None else max(400_000, per_step_cycles * steps)
     if n <= 0:
         return False
     import torch
@@ -280,7 +282,7 @@ def graph_time(torch, body, stream, steps, dist=None):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    held = hold_stream(stream, steps)
+    held = hold_stream(stream, steps, 20_000 if g is not None else 200_000)
     e0.record(stream)
     if g is not None:
         g.replay()
