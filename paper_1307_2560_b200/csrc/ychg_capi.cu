@@ -397,7 +397,7 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
 
     if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
     const int rc = ychg_launch_scan(&plan->map, &p, with_hyperedges ? plan->grid : plan->grid_counts,
-                                    with_hyperedges ? 1 : 0, st, nullptr);
+                                    with_hyperedges ? 1 : 0, st);
     if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "scan kernel launch");
     if (plan->timing) {
         CK(cudaEventRecord(plan->ev[1], st));

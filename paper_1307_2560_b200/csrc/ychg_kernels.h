@@ -9,9 +9,10 @@ struct ScanParams;
 }
 
 extern "C" {
-// Enqueue the fused scan kernel (cooperative launch) on `stream`.  Returns cudaError_t.
+// Enqueue one scan (ONE programmatic-dependent launch of ychg_scan_kernel) on `stream`.
+// Returns cudaError_t.
 int ychg_launch_scan(const void* tmap, const ychg_dev::ScanParams* prm, int grid, int with_links,
-                     cudaStream_t stream, cudaEvent_t ev_mid);
+                     cudaStream_t stream);
 
 // Set the kernels' dynamic shared-memory opt-in on the current device.
 int ychg_scan_kernel_prepare(void);

@@ -7,12 +7,13 @@
 //
 // The mask is cut into 1024-column strips (one 32-bit word per lane) and every
 // strip into k row segments; CTA g owns segments g, g+G, ... (one each when the
-// grid covers them: the planner sizes k so one scan fills every resident CTA
-// slot of the GPU).  A segment is split into NW consecutive warp bands; each
-// warp streams its band through its own TMA ring (cp.async.bulk.tensor, 32 rows
-// x 144 B per stage: 128 B of the strip + a 16 B right halo) and runs K1 + K3
-// bit-sliced in registers.  The CTA merges its warps in shared memory, writes
-// one partial per segment (counts + K3 band summary + links) into a workspace
+// grid covers them; the planner sizes k per plan kind: about half a CTA per SM per
+// scan for back-to-back scans, two per SM for an isolated one).  A segment is split
+// into NW consecutive warp bands; each warp streams its band through its own TMA
+// ring (cp.async.bulk.tensor, 32 rows x 144 B per stage: 128 B of the strip + a
+// 16 B right halo), skips 32-row blocks equal to the row above, and runs K1 + K3
+// bit-sliced in registers.  The CTA merges its warps in shared memory, writes one
+// partial per segment (counts + K3 band summary + links) into a workspace
 // double-buffered by scan parity, and counts itself in on the strip's arrival
 // counter.  The LAST segment of a strip to arrive finishes the strip in the same
 // CTA (no second kernel, no CTA waiting on a segment): it sums the k partials,
@@ -20,15 +21,16 @@
 // offset and first-column flag from every record to its left (warp-parallel
 // look-back), compacts the boundary list; the right-most strip writes totals.
 //
-// Consecutive scans overlap: every CTA triggers the next scan's launch at entry,
-// so the next scan's CTAs take SM slots as this scan's CTAs retire.  Invariants
-// (DESIGN.md §3): tickets drawn before the trigger (they then follow launch
-// order); a segment's partial half is reused only after the finisher of the
-// scan two back loaded it (fin_loaded); a strip finisher publishes nothing
-// before every finisher of the previous scan is done (fin_all).  Waits are
-// deadlock-free: all CTAs of a scan are resident before the next scan launches
-// (PDL trigger semantics), a CTA processes its segments in increasing order,
-// and a finisher only waits on strips to its left or on the previous scan.
+// Consecutive scans overlap: every CTA triggers the next scan's launch right after
+// drawing its tickets, so the next scan's CTAs take SM slots as this scan's
+// retire.  Invariants: tickets drawn before the trigger (they then
+// follow launch order); a segment's partial half is reused only after the
+// finisher of the scan two back loaded it (fin_loaded); a strip record is
+// rewritten only after every finisher of the scan two back is done, and the
+// outputs only after every finisher of the previous scan is done (fin_all).
+// Waits are deadlock-free: all CTAs of a scan are resident before the next scan
+// launches (PDL trigger semantics), a CTA processes its segments in increasing
+// order, and a finisher only waits on strips to its left or on older scans.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -995,8 +997,7 @@ extern "C" int ychg_scan_kernel_prepare(void) {
 // next launch at CTA entry, so back-to-back scans (e.g. one CUDA graph) overlap
 // the tail of one scan with the start of the next.
 extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int grid, int with_links,
-                                cudaStream_t stream, cudaEvent_t ev_mid) {
-    (void)ev_mid;
+                                cudaStream_t stream) {
     if (const int rc = ychg_scan_kernel_prepare()) return rc;
     const void* fa = with_links ? reinterpret_cast<const void*>(&ychg_scan_kernel<true>)
                                 : reinterpret_cast<const void*>(&ychg_scan_kernel<false>);
