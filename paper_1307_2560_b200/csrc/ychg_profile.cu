@@ -21,6 +21,7 @@
 // ColumnProfile::runs flattened (runscan.hpp:40-50).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -39,7 +40,8 @@ struct ProfileArgs {
     int32_t width, height, row_bytes;
     int32_t n_words;   // ceil(width / 32)
     int32_t n_bands;   // ceil(height / kBandRows)
-    int32_t band_major;  // fill grid order: 1 = consecutive warps take consecutive words of one band
+    int32_t band_major;  // fill grid order: 1 = consecutive warps take consecutive words of one band group
+    int32_t group;       // fill work unit: bands per warp (walked top to bottom)
 };
 
 // Word `w` of row y in MSB-first column order (bit 31 - j = column 32w + j),
@@ -258,113 +260,122 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
     const int wib = threadIdx.x >> 5;
     const int gw = blockIdx.x * kFillWarps + wib;
     const int lane = threadIdx.x & 31;
-    if (gw >= a.n_words * a.n_bands) return;
-    // Grid order.  Word-major (consecutive warps: bands of one word) keeps each
-    // lane's output stream local; band-major (consecutive warps and CTAs: words of
-    // one band) reads each 32 B row sector of the mask in 8 nearby warps at once
-    // (L1/L2 hits instead of one DRAM re-read per word).
-    const int w = a.band_major ? gw % a.n_words : gw / a.n_bands;
-    const int band = a.band_major ? gw / a.n_words : gw - w * a.n_bands;
+    const int n_groups = (a.n_bands + a.group - 1) / a.group;
+    if (gw >= a.n_words * n_groups) return;
+    // Work unit: one word (32 columns) x a group of `group` consecutive 256-row
+    // bands, walked top to bottom, so each lane writes ONE contiguous piece of its
+    // column's list per group (fewer pieces = fewer partially written output
+    // sectors, whose L2 evictions cost DRAM fill reads; profiles/r02_fill_ncu.md).
+    // Grid order: word-major (consecutive warps: groups of one word) or band-major
+    // (consecutive warps and CTAs: words of one group).
+    const int w = a.band_major ? gw % a.n_words : gw / n_groups;
+    const int grp = a.band_major ? gw / a.n_words : gw - w * n_groups;
     const int c = 32 * w + 8 * (lane >> 3) + 7 - (lane & 7);
     const bool live = c < a.width;
-    const int y0 = band * kBandRows;
-    const int y1 = min(a.height, y0 + kBandRows);
+    const int b0 = grp * a.group;
+    const int b1 = min(a.n_bands, b0 + a.group);
     const uint8_t* col = a.bits + 4 * static_cast<int64_t>(w);
-    // The whole band's rows are loaded up front: 8 independent loads per lane.
-    constexpr int kChunks = kBandRows / 32;
-    uint32_t raw[kChunks];
-#pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-        const int y = y0 + 32 * q + lane;
-        raw[q] = y < y1 ? __ldg(reinterpret_cast<const uint32_t*>(col + static_cast<int64_t>(y) * a.pitch)) : 0u;
-    }
-    uint32_t prev = y0 > 0 ? (__ldg(reinterpret_cast<const uint32_t*>(col + static_cast<int64_t>(y0 - 1) * a.pitch)) >> lane) & 1u
-                           : 0u;
-    int64_t idx = live ? col_off[c] + band_base[static_cast<int64_t>(band) * a.n_words * 32 + c] : 0;
-    int top = -1;  // y_top of a run opened in this band and still open
+    const int gy0 = b0 * kBandRows;
+    uint32_t prev = gy0 > 0 ? (__ldg(reinterpret_cast<const uint32_t*>(col + static_cast<int64_t>(gy0 - 1) * a.pitch)) >> lane) & 1u
+                            : 0u;
+    int64_t idx = live ? col_off[c] + band_base[static_cast<int64_t>(b0) * a.n_words * 32 + c] : 0;
+    int top = -1;  // y_top of a run opened in this group and still open
     int32_t* mine = kStaged ? &stage[wib][lane * kLaneSlot] : nullptr;
+    for (int band = b0; band < b1; ++band) {
+        const int y0 = band * kBandRows;
+        const int y1 = min(a.height, y0 + kBandRows);
+        // The whole band's rows are loaded up front: 8 independent loads per lane.
+        constexpr int kChunks = kBandRows / 32;
+        uint32_t raw[kChunks];
 #pragma unroll
-    for (int q = 0; q < kChunks; ++q) {
-        const int yb = y0 + 32 * q;
-        if (yb >= y1) break;  // warp-uniform
-        const uint32_t s = warp_transpose32(raw[q], lane);  // bit k = row yb + k
-        const int nk = min(32, y1 - yb);
-        const uint32_t valid = nk == 32 ? 0xFFFFFFFFu : (1u << nk) - 1u;
-        const uint32_t above = (s << 1) | prev;  // bit k = row yb + k - 1
-        const uint32_t rises = s & ~above;
-        prev = (s >> (nk - 1)) & 1u;
-        // One iteration per run that closes in this chunk (a fall at row k): its
-        // y_top is the last rise below k, or the carried `top`.  Uniform body,
-        // half the iterations of an event walk.
-        uint32_t falls = live ? (above & ~s) & valid : 0u;
-        uint32_t rs = live ? rises & valid : 0u;
-        int n = 0;  // records of this lane in this chunk
-        while (falls) {
-            const int k = __ffs(falls) - 1;
-            falls &= falls - 1;
-            const uint32_t below = (1u << k) - 1u;
-            const uint32_t r = rs & below;
-            rs &= ~below;
-            const int t = r ? yb + 31 - __clz(r) : top;
-            top = -1;
-            if (t >= 0) {
-                int32_t* rec = kStaged ? mine + 3 * n : runs + 3 * (idx + n);
-                rec[0] = c;
-                rec[1] = t;
-                rec[2] = yb + k - 1;
-                ++n;
-            } else {
-                runs[3 * (idx - 1) + 2] = yb + k - 1;  // opened in an earlier band
-            }
+        for (int q = 0; q < kChunks; ++q) {
+            const int y = y0 + 32 * q + lane;
+            raw[q] = y < y1 ? __ldg(reinterpret_cast<const uint32_t*>(col + static_cast<int64_t>(y) * a.pitch)) : 0u;
         }
-        if (rs) top = yb + 31 - __clz(rs);  // a run left open (at most one rise after the last fall)
-        if (kStaged) {
-        __syncwarp();
-        // Coalesced write-out of the chunk's records (T ints in total, warp-
-        // uniform).  T <= 512: one warp-wide segmented copy -- item t belongs to
-        // the last lane l whose exclusive offset is <= t (5 shuffles) and goes to
-        // runs[3*idx_l + t - off_l]; fewer, independent iterations win at mid
-        // densities.  Larger T: lane by lane, each segment one coalesced store
-        // per 32 ints (measured, profiles/r01_fill_variants.md).
-        const int m3 = 3 * n;
-        int inc = m3;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-            if (lane >= o) inc += t;
-        }
-        const int total = __shfl_sync(0xFFFFFFFFu, inc, 31);
-        const int off = inc - m3;
-        if (total > 512) {
-            uint32_t pending = __ballot_sync(0xFFFFFFFFu, n > 0);
-            while (pending) {
-                const int l = __ffs(pending) - 1;
-                pending &= pending - 1;
-                const int ml = __shfl_sync(0xFFFFFFFFu, m3, l);
-                const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
-                const int32_t* src = &stage[wib][l * kLaneSlot];
-                int32_t* dst = runs + 3 * base;
-                for (int t = lane; t < ml; t += 32) dst[t] = src[t];
+        for (int q = 0; q < kChunks; ++q) {
+            const int yb = y0 + 32 * q;
+            if (yb >= y1) break;  // warp-uniform
+            const uint32_t s = warp_transpose32(raw[q], lane);  // bit k = row yb + k
+            const int nk = min(32, y1 - yb);
+            const uint32_t valid = nk == 32 ? 0xFFFFFFFFu : (1u << nk) - 1u;
+            const uint32_t above = (s << 1) | prev;  // bit k = row yb + k - 1
+            const uint32_t rises = s & ~above;
+            prev = (s >> (nk - 1)) & 1u;
+            // One iteration per run that closes in this chunk (a fall at row k): its
+            // y_top is the last rise below k, or the carried `top`.  Uniform body,
+            // half the iterations of an event walk.
+            uint32_t falls = live ? (above & ~s) & valid : 0u;
+            uint32_t rs = live ? rises & valid : 0u;
+            int n = 0;  // records of this lane in this chunk
+            while (falls) {
+                const int k = __ffs(falls) - 1;
+                falls &= falls - 1;
+                const uint32_t below = (1u << k) - 1u;
+                const uint32_t r = rs & below;
+                rs &= ~below;
+                const int t = r ? yb + 31 - __clz(r) : top;
+                top = -1;
+                if (t >= 0) {
+                    int32_t* rec = kStaged ? mine + 3 * n : runs + 3 * (idx + n);
+                    rec[0] = c;
+                    rec[1] = t;
+                    rec[2] = yb + k - 1;
+                    ++n;
+                } else {
+                    runs[3 * (idx - 1) + 2] = yb + k - 1;  // opened before this group
+                }
             }
-        } else
-        for (int b0 = 0; b0 < total; b0 += 32) {
-            const int t = b0 + lane;
-            int l = 0;
+            if (rs) top = yb + 31 - __clz(rs);  // a run left open (at most one rise after the last fall)
+            if (kStaged) {
+                __syncwarp();
+                // Coalesced write-out of the chunk's records (T ints in total, warp-
+                // uniform).  T <= 512: one warp-wide segmented copy -- item t belongs to
+                // the last lane l whose exclusive offset is <= t (5 shuffles) and goes to
+                // runs[3*idx_l + t - off_l]; fewer, independent iterations win at mid
+                // densities.  Larger T: lane by lane, each segment one coalesced store
+                // per 32 ints (measured, profiles/r01_fill_variants.md).
+                const int m3 = 3 * n;
+                int inc = m3;
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int e = __shfl_sync(0xFFFFFFFFu, off, l + step);
-                if (e <= t) l += step;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                const int total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+                const int off = inc - m3;
+                if (total > 512) {
+                    uint32_t pending = __ballot_sync(0xFFFFFFFFu, n > 0);
+                    while (pending) {
+                        const int l = __ffs(pending) - 1;
+                        pending &= pending - 1;
+                        const int ml = __shfl_sync(0xFFFFFFFFu, m3, l);
+                        const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
+                        const int32_t* src = &stage[wib][l * kLaneSlot];
+                        int32_t* dst = runs + 3 * base;
+                        for (int t = lane; t < ml; t += 32) dst[t] = src[t];
+                    }
+                } else {
+                    for (int q0 = 0; q0 < total; q0 += 32) {
+                        const int t = q0 + lane;
+                        int l = 0;
+#pragma unroll
+                        for (int step = 16; step > 0; step >>= 1) {
+                            const int e = __shfl_sync(0xFFFFFFFFu, off, l + step);
+                            if (e <= t) l += step;
+                        }
+                        const int ol = __shfl_sync(0xFFFFFFFFu, off, l);
+                        const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
+                        if (t < total) runs[3 * base + (t - ol)] = stage[wib][l * kLaneSlot + (t - ol)];
+                    }
+                }
+                __syncwarp();
             }
-            const int ol = __shfl_sync(0xFFFFFFFFu, off, l);
-            const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
-            if (t < total) runs[3 * base + (t - ol)] = stage[wib][l * kLaneSlot + (t - ol)];
+            idx += n;
         }
-        __syncwarp();
-        }
-        idx += n;
     }
     if (!live) return;
-    if (band == a.n_bands - 1 && prev) {  // the virtual background row H closes what is open
+    if (b1 == a.n_bands && prev) {  // the virtual background row H closes what is open
         if (top >= 0) {
             runs[3 * idx + 0] = c;
             runs[3 * idx + 1] = top;
@@ -372,7 +383,7 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
         } else {
             runs[3 * (idx - 1) + 2] = a.height - 1;
         }
-    } else if (top >= 0) {  // still open: a later band writes y_bot
+    } else if (top >= 0) {  // still open: a later group writes y_bot
         runs[3 * idx + 0] = c;
         runs[3 * idx + 1] = top;
     }
@@ -421,16 +432,19 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
         // and for the direct walk on very sparse masks (hbands 100 -> 77 us);
         // word-major for the direct walk otherwise (checker(21) 197 vs 216 us).
         if (a.band_major < 0) a.band_major = (kind == 2 || rho < 0.01) ? 1 : 0;
+        a.group = 1;
+        if (const char* v = std::getenv("YCHG_FILL_GROUP"); v && *v) a.group = std::max(1, std::atoi(v));  // A/B hook
+        const int64_t unit_warps = static_cast<int64_t>(a.n_words) * ((a.n_bands + a.group - 1) / a.group);
         if (kind == 0) {
             constexpr int wpc = fill_warps_per_cta<false>();
-            profile_fill_kernel<false><<<static_cast<unsigned>((fill_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
+            profile_fill_kernel<false><<<static_cast<unsigned>((unit_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
                 a, d_band_counts, d_col_off, d_runs);
         } else if (kind == 1) {
             profile_fill_rowwise_kernel<<<static_cast<unsigned>((fill_warps + 7) / 8), 256, 0, stream>>>(
                 a, d_band_counts, d_col_off, d_runs);
         } else {
             constexpr int wpc = fill_warps_per_cta<true>();
-            profile_fill_kernel<true><<<static_cast<unsigned>((fill_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
+            profile_fill_kernel<true><<<static_cast<unsigned>((unit_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
                 a, d_band_counts, d_col_off, d_runs);
         }
     }
