@@ -125,6 +125,10 @@ int choose_segments(int n_strips, int n_blocks, int sms, int warps, bool latency
         return v && *v ? std::max(1, atoi(v)) : 2;
     }();
     int k = latency ? lat_per_sm * sms / ns : (sms + ns) / (2 * ns);  // floor(sms / S) | round(sms / 2S)
+    // ... and segments of at most 8192 rows (2048 rows per warp band) for tall masks:
+    // 65536^2 (64 strips), K=100 graph, hbands / random: k=2 136 / 106 us, k=4 120 /
+    // 103, k=8 90 / 110, k=16 102 / -- (round(sms / 2S) alone would give k=1 -> 2)
+    if (!latency) k = std::max(k, (n_blocks + 255) / 256);
     k = std::max(1, k);
     k = std::min(k, std::max(1, n_blocks / (2 * warps)));
     k = std::min(k, ychg_dev::kMaxSegPerStrip);

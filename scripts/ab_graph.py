@@ -12,7 +12,7 @@ S = int(sys.argv[1]) if len(sys.argv) > 1 else 21000
 pat = sys.argv[2] if len(sys.argv) > 2 else "random"
 W = H = S
 pitch = y.pitch_for(W)
-NB = 11
+NB = 11 if S <= 32768 else 3
 st = torch.cuda.current_stream()
 bufs = [torch.empty((H, pitch), dtype=torch.uint8, device="cuda") for _ in range(NB)]
 for b in bufs:
