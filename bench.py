@@ -14,9 +14,10 @@ cut-vertex counts + change flags + ascending boundary list + hyperedge total
 * N>1 = BASELINE config[4]: ONE 65536x65536 mask cut into N column strips (strong
   scaling, multigpu.py), one rank per GPU over NCCL.  Each rank generates its
   strip (+ an 8-column right halo) in place with K0's global column offset; a
-  step = the strip scan + NCCL all-gather of the strip counts + all-reduce of
-  (runs, links) + K2 over the gathered counts (the global boundary list, with
-  every strip's first-column fix-up).  comm_ms / compute_ms are timed apart.
+  step = the strip scan (counts and totals written straight into the all-gather
+  segment) + ONE NCCL all-gather + two small kernels over the gathered buffer
+  (global counts, the global boundary list with every strip's first-column
+  fix-up, summed runs / links).  comm_ms / compute_ms are timed apart.
   Without WORLD_SIZE in the environment, `--gpus N` re-launches itself under
   torch.distributed.run with N ranks.
 
@@ -357,8 +358,13 @@ def run_ours(a):
               "bounds": torch.empty(Ws, dtype=torch.int32, device="cuda"),
               "totals": torch.zeros(4, dtype=torch.int64, device="cuda")}
         if dist is not None:
-            sl["x"] = StripExchange(dist, strips, rank, device="cpu" if share else "cuda")
-            sl["sums"] = torch.zeros(2, dtype=torch.int64, device="cpu" if share else "cuda")
+            x = StripExchange(dist, strips, rank, device="cpu" if share else "cuda")
+            sl["x"] = x
+            if not share:  # the scan writes its counts and totals straight into the all-gather segment
+                sl["counts"] = x.send[:Ws]
+                sl["totals"] = x.totals_view
+            sl["gcounts"] = torch.empty(W, dtype=torch.int32, device="cuda")
+            sl["sums"] = torch.zeros(2, dtype=torch.int64, device="cuda")
             sl["gflags"] = torch.empty(fw, dtype=torch.int32, device="cuda")
             sl["gbounds"] = torch.empty(W, dtype=torch.int32, device="cuda")
             sl["gn"] = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -373,19 +379,20 @@ def run_ours(a):
                          sl["bounds"].data_ptr(), sl["totals"].data_ptr(), s_main.cuda_stream, links)
 
     def exchange(sl, s):
-        """NCCL all-gather of the strip counts, all-reduce (runs, links), K2 over the
-        gathered counts -> global flags / boundary list / count (on stream s)."""
+        """ONE NCCL all-gather of every strip's counts + totals, then two small kernels
+        over the gathered buffer: the contiguous global counts, their change flags and
+        boundary list (the strip-edge fix-up included), and the summed (runs, links)."""
+        x = sl["x"]
         with torch.cuda.stream(s):
             if share:  # gloo: host tensors
-                sl["sums"].copy_(sl["totals"][:2].cpu())
-                g = sl["x"].run(sl["counts"].cpu(), sl["sums"])
-                gc = g.cuda()
+                x.send[:Ws].copy_(sl["counts"].cpu())
+                x.totals_view.copy_(sl["totals"].cpu())
+                g = x.run().cuda()
             else:
-                sl["sums"].copy_(sl["totals"][:2])
-                gc = sl["x"].run(sl["counts"], sl["sums"])
-            y.detect_boundaries_device(gc.data_ptr(), W, sl["gflags"].data_ptr(), sl["gbounds"].data_ptr(),
-                                       sl["gn"].data_ptr(), s.cuda_stream)
-            sl["gcounts"] = gc
+                g = x.run()
+            y.assemble_strips_device(g.data_ptr(), x.c0, x.seg, x.tot_off, sl["gcounts"].data_ptr(),
+                                     sl["gflags"].data_ptr(), sl["gbounds"].data_ptr(), sl["gn"].data_ptr(),
+                                     sl["sums"].data_ptr(), s.cuda_stream)
 
     def step(i, s_main):
         h = i % R
@@ -629,7 +636,7 @@ def run_ours(a):
                        "strip_width_per_gpu": Ws, "halo_cols": s.halo_cols,
                        "path": "counts+flags+boundaries" + ("" if a.counts_only else "+hyperedges"),
                        "l2": f"rotating {nbuf} device copies per GPU ({nbuf * pitch * H / 1e6:.0f} MB > L2 {L2 / 1e6:.0f} MB)",
-                       "parallelism": f"{world} column strips, NCCL all-gather + all-reduce" if world > 1 else "1 GPU",
+                       "parallelism": f"{world} column strips, one NCCL all-gather per step" if world > 1 else "1 GPU",
                        "plan": {"grid": info.grid, "n_strips": info.n_strips, "seg_per_strip": info.seg_per_strip,
                                 "skip_unchanged_blocks": not a.no_skip}},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -643,7 +650,7 @@ def run_ours(a):
                                     else "CUDA events around K eager steps") + (f"; a {HOLD_NOTE}" if held else "")},
             "isolated_us": iso["us"] if iso else None, "isolated": iso, "north_star_subset": alt, "skip_ab": noskip, "multi_gpu": comm,
             "e2e": e2e, "e2e_dropin": e2e_dropin, "cpu_baseline": cpu, "parity": parity, "clocks": clk,
-            "gpu_launches": info.kernels_per_scan * a.steps + (4 * a.steps if world > 1 else 0),  # + NCCL x2, K2 x2
+            "gpu_launches": info.kernels_per_scan * a.steps + (3 * a.steps if world > 1 else 0),  # + NCCL, assemble x2
             "totals": totals_json,
         }
         print(json.dumps(line), flush=True)

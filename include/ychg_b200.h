@@ -122,6 +122,15 @@ YCHG_API int ychg_detect_boundary_columns(const int32_t* counts, int64_t n, int3
 YCHG_API int64_t ychg_boundary_flag_words(int64_t n);
 YCHG_API int ychg_detect_boundaries_device(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
                                            int32_t* d_boundaries, int64_t* d_n, void* stream);
+/* Column strips all-gathered from n_seg GPUs in ONE collective:
+ * segment r of d_gathered (seg_stride int32) holds strip r's counts at [0, c0[r+1]-c0[r])
+ * and its ychg_totals at int offset totals_off (even).  Writes the contiguous global
+ * counts, flags (ychg_boundary_flag_words(width) words), the boundary list, *d_n,
+ * and d_sums[2] = summed (runs, links).  c0: host array of n_seg+1 column starts. */
+YCHG_API int ychg_assemble_strips_device(const int32_t* d_gathered, int32_t n_seg, int32_t seg_stride,
+                                         int32_t totals_off, const int32_t* c0, int64_t width, int32_t* d_counts,
+                                         uint32_t* d_flags, int32_t* d_boundaries, int64_t* d_n, int64_t* d_sums,
+                                         void* stream);
 
 /* Fused pass.  counts_out[width] (may be NULL), boundaries_out[width] (may be NULL),
  * totals_out (may be NULL).  with_hyperedges = 0 skips K3 (hyperedges = -1). */

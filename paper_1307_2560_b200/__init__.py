@@ -87,6 +87,8 @@ _SIGS = {
     "ychg_synth_device": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64, _vp, _i64, _vp]),
     "ychg_boundary_flag_words": (_i64, [_i64]),
     "ychg_detect_boundaries_device": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp]),
+    "ychg_assemble_strips_device": (ctypes.c_int, [_vp, _i32, _i32, _i32, ctypes.POINTER(_i32), _i64, _vp, _vp,
+                                                   _vp, _vp, _vp, _vp]),
     "ychg_synth_device_window": (ctypes.c_int, [_i32, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.c_double, _u64,
                                                 _vp, _i64, _vp]),
     "ychg_device_alloc": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.POINTER(_vp)]),
@@ -552,6 +554,16 @@ def detect_boundaries_device(d_counts: int, n: int, d_flags: int, d_boundaries: 
     from column strips), asynchronous on `stream`; *d_n (int64, device) = boundary count."""
     _check(_lib.ychg_detect_boundaries_device(d_counts, int(n), d_flags, d_boundaries, d_n, stream or None),
            "detect_boundaries_device")
+
+
+def assemble_strips_device(d_gathered: int, c0: list[int], seg_stride: int, totals_off: int, d_counts: int,
+                           d_flags: int, d_boundaries: int, d_n: int, d_sums: int, stream: int = 0) -> None:
+    """All-gathered column strips (segment r: counts, then ychg_totals at int offset
+    totals_off) -> global counts, flags, boundary list, *d_n and d_sums = (runs, links)."""
+    arr = (_i32 * len(c0))(*c0)
+    _check(_lib.ychg_assemble_strips_device(d_gathered, len(c0) - 1, int(seg_stride), int(totals_off), arr,
+                                            int(c0[-1]), d_counts, d_flags, d_boundaries, d_n, d_sums,
+                                            stream or None), "assemble_strips_device")
 
 
 def pitch_for(width: int) -> int:

@@ -136,6 +136,70 @@ __global__ void bcompact_kernel(const uint32_t* __restrict__ flags, int64_t n,
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *n_out = base + block_nb[blockIdx.x];
 }
 
+// ---- column strips all-gathered from several GPUs (bench / multigpu.py): rank r's
+// segment of the gathered buffer holds its strip's counts at [0, width_r) and its
+// ychg_totals (4 int64) at int offset tot_off.  One pass writes the contiguous
+// global counts and their change flags (bflags over the strided layout), and
+// block 0 sums every segment's (runs, links).
+struct GatherLayout {
+    int32_t n_seg, seg_stride, tot_off;
+    int32_t c0[65];  // first global column of each segment, c0[n_seg] = width
+};
+
+__device__ __forceinline__ int32_t gathered_count(const int32_t* __restrict__ g, const GatherLayout& L, int64_t c) {
+    int r = 0;
+    while (r + 1 < L.n_seg && c >= L.c0[r + 1]) ++r;
+    return g[static_cast<int64_t>(r) * L.seg_stride + (c - L.c0[r])];
+}
+
+__global__ void bflags_gather_kernel(const int32_t* __restrict__ g, const GatherLayout L, int64_t n,
+                                     int32_t* __restrict__ counts, uint32_t* __restrict__ flags,
+                                     int32_t* __restrict__ block_nb, long long* __restrict__ sums) {
+    __shared__ int red[8];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kColsPerBlock;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int nb = 0;
+    for (int wi = warp; wi < kColsPerBlock / 32; wi += 8) {
+        const int64_t c = base + wi * 32 + lane;
+        bool f = false;
+        if (c < n) {
+            const int32_t v = gathered_count(g, L, c);
+            const int32_t prev = c == 0 ? 0 : gathered_count(g, L, c - 1);  // counts[-1] := 0
+            counts[c] = v;
+            f = v != prev;
+        }
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+        const int64_t w = (base >> 5) + wi;
+        if (lane == 0 && w * 32 < n) flags[w] = m;
+        nb += __popc(m);
+    }
+    if (lane == 0) red[warp] = nb;
+    if (blockIdx.x == 0 && warp == 0) {
+        long long runs = 0, links = 0;
+        for (int r = lane; r < L.n_seg; r += 32) {
+            const long long* t =
+                reinterpret_cast<const long long*>(g + static_cast<int64_t>(r) * L.seg_stride + L.tot_off);
+            runs += t[0];
+            links += t[1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            runs += __shfl_xor_sync(0xFFFFFFFFu, runs, o);
+            links += __shfl_xor_sync(0xFFFFFFFFu, links, o);
+        }
+        if (lane == 0) {
+            sums[0] = runs;
+            sums[1] = links;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int i = 0; i < 8; ++i) t += red[i];
+        block_nb[blockIdx.x] = t;
+    }
+}
+
 }  // namespace
 
 // Columns [x0, x0 + win) of the width x height reference image (x0 a multiple of
@@ -306,6 +370,32 @@ extern "C" int ychg_launch_mask_pad(uint8_t* d_bits, int64_t pitch, int32_t widt
     int64_t blocks = (int64_t(height) + 255) / 256;
     if (blocks > 148 * 4) blocks = 148 * 4;
     mask_pad_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_bits, pitch, height, (width + 7) / 8 - 1, mask);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// Assemble all-gathered strips (see GatherLayout): global counts, flags, the
+// ascending boundary list and its length, and the summed (runs, links).
+extern "C" int ychg_launch_assemble_strips(const int32_t* d_gathered, int32_t n_seg, int32_t seg_stride,
+                                           int32_t tot_off, const int32_t* c0, int64_t n, int32_t* d_counts,
+                                           uint32_t* d_flags, int32_t* d_boundaries, long long* d_n,
+                                           long long* d_sums, cudaStream_t stream) {
+    if (n_seg < 1 || n_seg > 64) return static_cast<int>(cudaErrorInvalidValue);
+    GatherLayout L{};
+    L.n_seg = n_seg;
+    L.seg_stride = seg_stride;
+    L.tot_off = tot_off;
+    for (int r = 0; r <= n_seg; ++r) L.c0[r] = c0[r];
+    const int64_t blocks = (n + kColsPerBlock - 1) / kColsPerBlock;
+    if (blocks == 0) {
+        cudaMemsetAsync(d_n, 0, sizeof(long long), stream);
+        cudaMemsetAsync(d_sums, 0, 2 * sizeof(long long), stream);
+        return 0;
+    }
+    int32_t* block_nb = reinterpret_cast<int32_t*>(d_flags + blocks * (kColsPerBlock / 32));
+    bflags_gather_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_gathered, L, n, d_counts, d_flags, block_nb,
+                                                                     d_sums);
+    bcompact_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(d_flags, n, block_nb, d_boundaries, d_n);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }

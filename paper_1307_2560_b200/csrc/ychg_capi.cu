@@ -992,6 +992,27 @@ extern "C" int ychg_detect_boundaries_device(const int32_t* d_counts, int64_t n,
     return YCHG_OK;
 }
 
+extern "C" int ychg_assemble_strips_device(const int32_t* d_gathered, int32_t n_seg, int32_t seg_stride,
+                                           int32_t totals_off, const int32_t* c0, int64_t width, int32_t* d_counts,
+                                           uint32_t* d_flags, int32_t* d_boundaries, int64_t* d_n, int64_t* d_sums,
+                                           void* stream) {
+    if (n_seg < 1 || n_seg > 64) return fail(YCHG_ERR_INVALID, "assemble_strips: 1..64 segments, got %d", n_seg);
+    if (!c0 || !d_gathered || !d_n || !d_sums || (width > 0 && (!d_counts || !d_flags || !d_boundaries)))
+        return fail(YCHG_ERR_INVALID, "assemble_strips: NULL argument");
+    if (c0[0] != 0 || c0[n_seg] != width || totals_off % 2 != 0)
+        return fail(YCHG_ERR_INVALID, "assemble_strips: bad layout (c0[0]=%d, c0[n]=%d, width %lld, totals_off %d)",
+                    c0[0], c0[n_seg], static_cast<long long>(width), totals_off);
+    for (int r = 0; r < n_seg; ++r)
+        if (c0[r + 1] < c0[r] || c0[r + 1] - c0[r] > totals_off || totals_off + 8 > seg_stride)
+            return fail(YCHG_ERR_INVALID, "assemble_strips: segment %d does not fit its stride", r);
+    const int rc = ychg_launch_assemble_strips(d_gathered, n_seg, seg_stride, totals_off, c0, width, d_counts,
+                                               d_flags, d_boundaries, reinterpret_cast<long long*>(d_n),
+                                               reinterpret_cast<long long*>(d_sums),
+                                               static_cast<cudaStream_t>(stream));
+    if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "assemble kernels launch");
+    return YCHG_OK;
+}
+
 // ---------------------------------------------------------------------------- run materialisation
 namespace {
 

@@ -49,6 +49,9 @@ int ychg_launch_pack_p5(const uint8_t* d_samples, int32_t width, int32_t height,
                         int64_t pitch, cudaStream_t stream);
 int ychg_launch_mask_pad(uint8_t* d_bits, int64_t pitch, int32_t width, int32_t height, cudaStream_t stream);
 
+int ychg_launch_assemble_strips(const int32_t* d_gathered, int32_t n_seg, int32_t seg_stride, int32_t tot_off,
+                                const int32_t* c0, int64_t n, int32_t* d_counts, uint32_t* d_flags,
+                                int32_t* d_boundaries, long long* d_n, long long* d_sums, cudaStream_t stream);
 int ychg_launch_boundaries(const int32_t* d_counts, int64_t n, uint32_t* d_flags,
                            int32_t* d_boundaries, long long* d_n, cudaStream_t stream);
 }

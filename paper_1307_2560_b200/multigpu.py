@@ -8,15 +8,19 @@ runscan.cpp:18-34), so the mask is cut into vertical strips, one per rank:
 * rank r counts columns [c0, c1) (multiples of 1024: whole strips of the device
   layout) and holds one extra byte column on the right (the halo) so that the K3
   pair step sees column c1 for the pair (c1-1, c1);
-* per step the strip counts are all-gathered (NCCL over NVLink on GPUs, gloo in
-  the CPU tests) into the global count array, and (runs, links) all-reduced;
+* per step ONE all-gather (NCCL over NVLink on GPUs, gloo in the CPU tests)
+  collects every strip's counts AND its (runs, links) totals (written by the
+  scan next to its counts), from which the global count array and the sums
+  follow;
 * the boundary flag of a strip's first column needs counts[c0-1] from the left
   neighbour (runscan.cpp:147-149): the global boundary list is therefore K2 over
   the gathered counts (``detect_boundaries_device`` on GPUs, ``merge_boundaries``
   here for the tests), which is the strip-edge fix-up;
 * hyperedges = sum(runs) - sum(links).
 
-``bench.py`` drives ``StripExchange`` with device tensors and NCCL for N > 1;
+``bench.py`` drives ``StripExchange`` with device tensors and NCCL for N > 1
+(then ``assemble_strips_device``: global counts + boundary list + sums in two
+small kernels);
 ``tests/test_multigpu.py`` drives the same class with CPU tensors and gloo
 (world 2 and 3), the strips computed by the oracle.
 """
@@ -73,10 +77,13 @@ def merge_boundaries(counts: np.ndarray) -> np.ndarray:
 
 
 class StripExchange:
-    """The per-step exchange of one rank over torch.distributed: all-gather of the
-    strip counts into the global count array (padded to the widest strip when the
-    strips differ), all-reduce (sum) of the int64 pair (runs, links) in place.
-    Buffers live on `device` (a CUDA device for NCCL, "cpu" for gloo)."""
+    """The per-step exchange of one rank over torch.distributed (NCCL on GPUs, gloo
+    in the CPU tests): ONE all-gather.  Every rank contributes a segment of
+    `seg` int32 -- its strip's counts at [0, width_cnt) (the scan writes them
+    there directly) and its ychg_totals {total_runs, links, hyperedges,
+    n_boundaries} (4 int64) at int offset `tot_off` -- so the global counts AND
+    the (runs, links) sums follow from the gathered buffer without a second
+    collective (`assemble_strips_device` on GPUs, `host_assemble` here)."""
 
     def __init__(self, dist, strips: list[Strip], rank: int, device="cpu"):
         import torch
@@ -84,45 +91,50 @@ class StripExchange:
         self.dist, self.strips, self.rank = dist, strips, rank
         self.world = len(strips)
         self.width = strips[-1].c1
-        self.wmax = max(s.width_cnt for s in strips)
-        self.equal = all(s.width_cnt == self.wmax for s in strips)
-        self.send = torch.zeros(self.wmax, dtype=torch.int32, device=device)
-        self.gathered = torch.zeros(self.world * self.wmax, dtype=torch.int32, device=device)
-        self.counts = (self.gathered[: self.width] if self.equal
-                       else torch.zeros(self.width, dtype=torch.int32, device=device))
+        wmax = max(s.width_cnt for s in strips)
+        self.tot_off = (wmax + 1) // 2 * 2          # 8-byte aligned ychg_totals
+        self.seg = self.tot_off + 8
+        self.c0 = [s.c0 for s in strips] + [self.width]
+        self.send = torch.zeros(self.seg, dtype=torch.int32, device=device)
+        self.gathered = torch.zeros(self.world * self.seg, dtype=torch.int32, device=device)
 
-    def run(self, counts_local, sums):
-        """counts_local: this rank's width_cnt int32 counts; sums: int64 [runs, links],
-        all-reduced in place.  Returns the global counts (a view owned by self)."""
-        s = self.strips[self.rank]
-        src = counts_local
-        if not self.equal:
-            self.send[: s.width_cnt].copy_(counts_local)
-            src = self.send
-        self.dist.all_gather_into_tensor(self.gathered, src)
-        self.dist.all_reduce(sums)
-        if not self.equal:
-            for r, t in enumerate(self.strips):
-                self.counts[t.c0:t.c1].copy_(self.gathered[r * self.wmax:r * self.wmax + t.width_cnt])
-        return self.counts
+    @property
+    def totals_view(self):
+        """This rank's ychg_totals slot in the send buffer (4 int64)."""
+        return self.send[self.tot_off:self.tot_off + 8].view(__import__("torch").int64)
+
+    def run(self):
+        self.dist.all_gather_into_tensor(self.gathered, self.send)
+        return self.gathered
+
+    def host_assemble(self):
+        """(global counts, total runs, links) from the gathered buffer (host copy)."""
+        g = self.gathered.cpu().numpy()
+        counts = np.concatenate([g[r * self.seg:r * self.seg + (self.c0[r + 1] - self.c0[r])]
+                                 for r in range(self.world)])
+        tot = np.stack([g[r * self.seg + self.tot_off:r * self.seg + self.tot_off + 8].view(np.int64)
+                        for r in range(self.world)])
+        return counts, int(tot[:, 0].sum()), int(tot[:, 1].sum())
 
 
 def run_sharded(bits: np.ndarray, width: int, height: int, compute, dist=None):
     """One sharded pass over a host image (the CPU tests' entry point).
     `compute(sub_bits, width_img, width_cnt, height) -> (counts[width_cnt], links)`.
     Returns (counts, boundaries, total_runs, links, hyperedges) on every rank."""
-    import torch
-
     world = dist.get_world_size() if dist else 1
     rank = dist.get_rank() if dist else 0
     strips = plan_strips(width, world)
     s = strips[rank]
     counts, links = compute(strip_bits(bits, width, s), s.width_img, s.width_cnt, height)
-    local = torch.from_numpy(np.ascontiguousarray(counts, dtype=np.int32))
-    sums = torch.tensor([int(np.asarray(counts, dtype=np.int64).sum()), int(links)], dtype=torch.int64)
-    if dist:
-        full = StripExchange(dist, strips, rank).run(local, sums).numpy().copy()
-    else:
-        full = local.numpy().copy()
-    runs, lk = (int(v) for v in sums.tolist())
-    return full, merge_boundaries(full), runs, lk, runs - lk
+    counts = np.ascontiguousarray(counts, dtype=np.int32)
+    runs = int(counts.astype(np.int64).sum())
+    if not dist:
+        return counts.copy(), merge_boundaries(counts), runs, int(links), runs - int(links)
+    import torch
+
+    x = StripExchange(dist, strips, rank)
+    x.send[: s.width_cnt] = torch.from_numpy(counts)
+    x.totals_view[:] = torch.tensor([runs, int(links), runs - int(links), 0], dtype=torch.int64)
+    x.run()
+    full, runs_all, links_all = x.host_assemble()
+    return full, merge_boundaries(full), runs_all, links_all, runs_all - links_all
