@@ -347,7 +347,7 @@ def run_ours(a):
     info = plan.info()
 
     # Per-step outputs (R slots): the scan of step i writes slot i % R; for N>1 the
-    # exchange of step i (all-gather, all-reduce, K2 over the gathered counts) runs
+    # exchange of step i (one all-gather, then the assemble kernels) runs
     # on a side stream into the same slot while the next steps scan.
     R = a.steps + 1 if dist is not None else 2
     fw = y.boundary_flag_words(W)
