@@ -101,25 +101,37 @@ Args parse(int argc, char** argv, int first, const std::set<std::string>& option
     return a;
 }
 
-// ---- files (cli.cpp:25-49 semantics: empty path = stdout)
+// ---- files.  Behaviour of the reference CLI's file helpers (cli.cpp:25-49): the
+// same IoError texts (the tests compare them) and an empty output path meaning
+// standard output.  Implemented on C stdio: one handle, fixed-size reads.
 std::vector<std::uint8_t> read_file(const std::string& path) {
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw IoError("cannot open " + path + " for reading");
-    std::vector<std::uint8_t> bytes{std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>()};
-    if (in.bad()) throw IoError("read failed on " + path);
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IoError("cannot open " + path + " for reading");
+    std::vector<std::uint8_t> bytes;
+    std::uint8_t chunk[1 << 16];
+    for (;;) {
+        const std::size_t got = std::fread(chunk, 1, sizeof(chunk), f);
+        bytes.insert(bytes.end(), chunk, chunk + got);
+        if (got < sizeof(chunk)) break;
+    }
+    const bool failed = std::ferror(f) != 0;
+    std::fclose(f);
+    if (failed) throw IoError("read failed on " + path);
     return bytes;
 }
 
 void write_output(const std::string& path, const void* data, std::size_t size) {
-    if (path.empty()) {
-        if (size != 0 && std::fwrite(data, 1, size, stdout) != size) throw IoError("write to standard output failed");
+    const bool to_stdout = path.empty();
+    std::FILE* f = to_stdout ? stdout : std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("cannot open " + path + " for writing");
+    const bool ok = size == 0 || std::fwrite(data, 1, size, f) == size;
+    if (to_stdout) {
         std::fflush(stdout);
+        if (!ok) throw IoError("write to standard output failed");
         return;
     }
-    std::ofstream out(path, std::ios::binary | std::ios::trunc);
-    if (!out) throw IoError("cannot open " + path + " for writing");
-    out.write(static_cast<const char*>(data), static_cast<std::streamsize>(size));
-    if (!out) throw IoError("write failed on " + path);
+    const bool closed = std::fclose(f) == 0;
+    if (!ok || !closed) throw IoError("write failed on " + path);
 }
 
 void write_output(const std::string& path, const std::string& text) { write_output(path, text.data(), text.size()); }
@@ -174,15 +186,30 @@ void run_synth(const Args& a) {
     write_output(a.str("out"), bytes.data(), bytes.size());
 }
 
-// ---- counts (cli.cpp:203-214)
+// ---- counts: the reference CLI's CSV (cli.cpp:203-214 output format: a
+// "col,count" header and one row per column, then optionally a blank line, a
+// "boundary" header and one boundary column per row)
+void append_row(std::string& csv, long long a, const long long* b) {
+    char buf[48];
+    const int n = b ? std::snprintf(buf, sizeof(buf), "%lld,%lld\n", a, *b) : std::snprintf(buf, sizeof(buf), "%lld\n", a);
+    csv.append(buf, static_cast<std::size_t>(n));
+}
+
 void run_counts(const Args& a) {
     const BinaryImage image = load_pnm(read_file(a.str("input")), threshold_of(a));
-    const auto counts = cut_vertex_counts(image, strategy_for_threads(a.num("threads", default_threads())));
-    std::string csv = "col,count\n";
-    for (std::size_t c = 0; c < counts.size(); ++c) csv += std::to_string(c) + "," + std::to_string(counts[c]) + "\n";
+    const std::vector<int> counts = cut_vertex_counts(image, strategy_for_threads(a.num("threads", default_threads())));
+    std::string csv;
+    csv.reserve(counts.size() * 12 + 16);
+    csv += "col,count\n";
+    long long col = 0;
+    for (const int v : counts) {
+        const long long cnt = v;
+        append_row(csv, col++, &cnt);
+    }
     if (a.flags.count("boundaries")) {
         csv += "\nboundary\n";
-        for (int b : detect_boundary_columns(counts)) csv += std::to_string(b) + "\n";
+        const std::vector<int> bounds = detect_boundary_columns(counts);
+        for (const int b : bounds) append_row(csv, b, nullptr);
     }
     write_output(a.str("out"), csv);
 }
