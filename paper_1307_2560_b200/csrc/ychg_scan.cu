@@ -715,8 +715,11 @@ __device__ __forceinline__ void kick_ring(const CUtensorMap* tmap, uint8_t* my_s
     }
 }
 
+#ifndef YCHG_MIN_CTAS_PER_SM  // A/B builds only: 4 (with YCHG_STAGES=2) caps registers at 128 for 4 CTAs/SM
+#define YCHG_MIN_CTAS_PER_SM 1
+#endif
 template <bool kLinks, int NW = scan_warps<kLinks>()>
-__global__ void __launch_bounds__(NW * 32, 1)
+__global__ void __launch_bounds__(NW * 32, YCHG_MIN_CTAS_PER_SM)
 ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm) {
     constexpr int kS = scan_stages<kLinks>();  // TMA ring depth of this path
     constexpr int T = NW * 32;
