@@ -13,10 +13,12 @@
 //                             at row y opens run {c, y, ?} at the column's next
 //                             index, a fall at row y closes it with y_bot = y-1 (one
 //                             12-byte record); a virtual background row H closes
-//                             what is open at the bottom.  Three kernels, chosen by
-//                             run density (ychg_launch_profile): a transposed
-//                             fall walk (sparse), row stepping (mid), the walk with
-//                             a staged coalesced write-out (dense).
+//                             what is open at the bottom.  Default: the band-staged
+//                             kernel (16-byte row loads, records staged per band in
+//                             shared memory, written out column by column with
+//                             8-byte vector stores).  Kept for unaligned buffers and
+//                             A/B: a transposed fall walk (sparse), row stepping,
+//                             the walk with a per-chunk staged write-out.
 // The flat output is column-major and sorted by y_top inside a column -- exactly
 // ColumnProfile::runs flattened (runscan.hpp:40-50).
 #include <cuda_runtime.h>
@@ -389,6 +391,313 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
     }
 }
 
+// P3: fill, band-staged.  One warp per (256-row band, group of kW words): lane k
+// loads rows y0+32q+k of the whole group with 16-byte loads up front (8 x kW/4
+// independent loads, half or whole 32 B sectors instead of 4 B of each), then walks
+// the group's words one at a time.  For each word, a warp bit transpose per 32-row
+// chunk gives lane j its column's 32-row bit sequence; the runs that open and close
+// inside the band are paired rise <-> fall in lockstep (the k-th fall of a chunk,
+// after the one closing a run carried in from above, closes the k-th rise) and
+// staged as ONE 16-bit entry {top - y0, bot - y0} in the lane's shared-memory slot
+// (<= 128 per band).  At the end of the word's band the warp writes every column's
+// staged records out column by column, lanes = consecutive records, so each store
+// instruction covers a contiguous stretch of one column's list (12 B stride) and
+// the column's band piece is written in one pass -- no per-chunk flush.  The two
+// boundary records are written directly as in the walk kernel: the y_bot of a run
+// opened in an earlier band (index base-1), and {c, y_top} of a run left open at
+// the band's bottom (its y_bot comes from a later band or the virtual row H).
+constexpr int kBandWarps = 4;
+static_assert(kBandRows == 256, "band_write_column: <= 128 records per column and band, 2 per lane and pass");
+
+// Write-out of a warp's staged records (word w, band rows from y0): lane l holds
+// n_l 16-bit entries {top - y0 | (bot - y0) << 8} for column l of the word, to be
+// stored at runs[idx_l ..].  Many records: column by column, lanes = consecutive
+// records of one column (each store instruction covers a contiguous stretch of
+// one column's list).  Few (sparse masks, 0-2 per column): one flat pass, record t
+// found in its lane's slot by a binary search over the lanes' exclusive offsets.
+// One column's m (<= 128) staged records as 12-byte {c, top, bot} at
+// runs[3*base ..], as 8-byte vector stores: the piece's ints are c, t0, b0, c, t1,
+// b1, ...; from its first 8-byte boundary (h = 0 or 1 ints in) lane p writes the
+// three int2 holding ints h+6p .. h+6p+5 (records 2p, 2p+1: one 32-bit shared
+// load) -- whole sectors per store instruction instead of 12-byte-strided
+// partial ones.  At most one int before the boundary (always c) and one after
+// the last whole vector (always the last record's bot) are written singly.
+template <int kSlot>
+__device__ __forceinline__ void band_write_column(const uint16_t* __restrict__ stage, int lane, int l, int m,
+                                                  int64_t base, int w, int y0, int32_t* __restrict__ runs) {
+    if (m == 0) return;
+    const int cl = 32 * w + 8 * (l >> 3) + 7 - (l & 7);
+    const uint16_t* src = stage + l * kSlot;
+    const int64_t g = 3 * base;  // the piece's first int
+    const int h = static_cast<int>(g & 1);
+    const int body = 3 * m - h;  // ints from the boundary on
+    if (lane == 0 && h) runs[g] = cl;
+    if (lane == 1 && (body & 1)) runs[g + 3 * m - 1] = y0 + static_cast<int>(src[m - 1] >> 8);
+    int2* vd = reinterpret_cast<int2*>(runs + g + h);
+    const int nv = body >> 1;  // whole int2
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int pr = lane + 32 * k;  // record pair
+        if (3 * pr >= nv) break;       // this lane is past the piece
+        const uint32_t e = reinterpret_cast<const uint32_t*>(src)[pr];  // entries 2pr, 2pr+1 (reads past m are never stored)
+        const int t0 = y0 + static_cast<int>(e & 0xFFu), b0 = y0 + static_cast<int>((e >> 8) & 0xFFu);
+        const int t1 = y0 + static_cast<int>((e >> 16) & 0xFFu), b1 = y0 + static_cast<int>(e >> 24);
+        // h = 0: (c,t0) (b0,c) (t1,b1);  h = 1: (t0,b0) (c,t1) (b1,c)
+        const int2 v0 = h ? make_int2(t0, b0) : make_int2(cl, t0);
+        const int2 v1 = h ? make_int2(cl, t1) : make_int2(b0, cl);
+        const int2 v2 = h ? make_int2(b1, cl) : make_int2(t1, b1);
+        vd[3 * pr] = v0;
+        if (3 * pr + 1 < nv) vd[3 * pr + 1] = v1;
+        if (3 * pr + 2 < nv) vd[3 * pr + 2] = v2;
+    }
+}
+
+template <int kSlot>
+__device__ __forceinline__ void band_write_flat(const uint16_t* __restrict__ stage, int lane, int off, int64_t idx,
+                                                int t, int total, int w, int y0, int32_t* __restrict__ runs) {
+    int l = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const int e = __shfl_sync(0xFFFFFFFFu, off, l + step);
+        if (e <= t) l += step;
+    }
+    const int j = t - __shfl_sync(0xFFFFFFFFu, off, l);
+    const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
+    if (t < total) {
+        const uint32_t e = stage[l * kSlot + j];
+        int32_t* dst = runs + 3 * (base + j);
+        dst[0] = 32 * w + 8 * (l >> 3) + 7 - (l & 7);
+        dst[1] = y0 + static_cast<int>(e & 0xFFu);
+        dst[2] = y0 + static_cast<int>(e >> 8);
+    }
+}
+
+// Write-out of a warp's staged records (word w, band rows from y0): lane l holds
+// n_l 16-bit entries {top - y0 | (bot - y0) << 8} for column l of the word, to be
+// stored at runs[idx_l ..].  Many records: column by column, lanes = consecutive
+// records of one column (each store instruction covers a contiguous stretch of
+// one column's list).  Few (sparse masks, 0-2 per column): one flat pass, record t
+// found in its lane's slot by a binary search over the lanes' exclusive offsets.
+// Both loops handle two independent columns / 32-record groups per iteration.
+template <int kSlot>
+__device__ __forceinline__ void band_write_out(const uint16_t* __restrict__ stage, int lane, int n, int64_t idx, int w,
+                                               int y0, int mode, int32_t* __restrict__ runs) {
+    const int total = static_cast<int>(__reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned>(n)));
+#ifdef YCHG_DIAG_FILL_NOSTORE  // diagnostics build: staged records are never written (wrong output, timing only)
+    if (total >= 0) return;
+#endif
+    if (total == 0) return;
+    const uint32_t nonempty = __ballot_sync(0xFFFFFFFFu, n > 0);
+    const bool flat = mode == 2 || (mode == 0 && (total + 31) / 32 * 5 <= __popc(nonempty) * 4);
+    if (flat) {
+        int inc = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        const int off = inc - n;
+        for (int t0 = 0; t0 < total; t0 += 64) {
+            band_write_flat<kSlot>(stage, lane, off, idx, t0 + lane, total, w, y0, runs);
+            band_write_flat<kSlot>(stage, lane, off, idx, t0 + 32 + lane, total, w, y0, runs);
+        }
+    } else {
+        uint32_t pending = nonempty;
+        while (pending) {
+            const int l1 = __ffs(pending) - 1;
+            pending &= pending - 1u;
+            const int l2 = pending ? __ffs(pending) - 1 : l1;
+            pending &= pending - 1u;
+            const int m1 = __shfl_sync(0xFFFFFFFFu, n, l1);
+            const int m2 = l2 != l1 ? __shfl_sync(0xFFFFFFFFu, n, l2) : 0;
+            const int64_t b1 = __shfl_sync(0xFFFFFFFFu, idx, l1);
+            const int64_t b2 = __shfl_sync(0xFFFFFFFFu, idx, l2);
+            band_write_column<kSlot>(stage, lane, l1, m1, b1, w, y0, runs);
+            band_write_column<kSlot>(stage, lane, l2, m2, b2, w, y0, runs);
+        }
+    }
+}
+
+// P3: fill, band-staged.  One warp per (256-row band, group of kW words): lane k
+// loads rows y0+32q+k of the whole group with 16-byte loads up front (8 x kW/4
+// independent loads).  Phase 1, chunk by chunk over all kW words at once (kW
+// independent shuffle chains): a chunk whose 32 rows all repeat the row above is
+// marked unchanged; the others are bit-transposed in place (lane j: its column's
+// 32-row bit sequence).  Phase 2, word by word: the runs that open and close
+// inside the band are paired rise <-> fall in lockstep (the k-th fall of a chunk,
+// after the one closing a run carried in from above, closes the k-th rise) and
+// staged as ONE 16-bit entry {top - y0, bot - y0} in the lane's shared-memory slot
+// (<= 128 per band), then written out (band_write_out).  The
+// two boundary records are written directly as in the walk kernel: the y_bot of a
+// run opened in an earlier band (index base-1), and {c, y_top} of a run left open
+// at the band's bottom (its y_bot comes from a later band or the virtual row H).
+template <int kW>
+__global__ void __launch_bounds__(kBandWarps * 32) profile_fill_band_kernel(const ProfileArgs a,
+                                                                            const uint32_t* __restrict__ band_base,
+                                                                            const int64_t* __restrict__ col_off,
+                                                                            int32_t* __restrict__ runs /* [n][3] */) {
+    static_assert(kW == 4 || kW == 8, "word group = one or two 16-byte loads per row");
+    constexpr int kV = kW / 4;
+    constexpr int kSlot = 130;  // <= 128 entries per lane and band (+2: odd word stride)
+    __shared__ uint16_t stage[kBandWarps][32 * kSlot];
+    const int wib = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int n_groups = (a.n_words + kW - 1) / kW;
+    const int gw = blockIdx.x * kBandWarps + wib;
+    if (gw >= n_groups * a.n_bands) return;
+    const int band = gw / n_groups, grp = gw - band * n_groups;  // consecutive warps: groups of one band
+    const int y0 = band * kBandRows;
+    const int y1 = min(a.height, y0 + kBandRows);
+    const int w0 = grp * kW;
+    const int nv = (w0 + 4 < a.n_words) ? kV : 1;  // 16-byte halves inside the row (warp-uniform)
+    const uint8_t* gbase = a.bits + 4 * static_cast<int64_t>(w0);
+    uint32_t x[8][kW];  // raw words, transposed in place by phase 1
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int y = y0 + 32 * q + lane;
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+            const uint4 t = (y < y1 && v < nv) ? __ldg(reinterpret_cast<const uint4*>(gbase + static_cast<int64_t>(y) * a.pitch) + v)
+                                               : make_uint4(0u, 0u, 0u, 0u);
+            x[q][4 * v + 0] = t.x;
+            x[q][4 * v + 1] = t.y;
+            x[q][4 * v + 2] = t.z;
+            x[q][4 * v + 3] = t.w;
+        }
+    }
+    uint32_t aw[kW];  // row y0-1 (all lanes read the same 16 B: one transaction)
+#pragma unroll
+    for (int v = 0; v < kV; ++v) {
+        const uint4 t = (y0 > 0 && v < nv) ? __ldg(reinterpret_cast<const uint4*>(gbase + static_cast<int64_t>(y0 - 1) * a.pitch) + v)
+                                           : make_uint4(0u, 0u, 0u, 0u);
+        aw[4 * v + 0] = t.x;
+        aw[4 * v + 1] = t.y;
+        aw[4 * v + 2] = t.z;
+        aw[4 * v + 3] = t.w;
+    }
+    // Each column's first index in this band, loaded with the rows.
+    int64_t idx0[kW];
+#pragma unroll
+    for (int i = 0; i < kW; ++i) {
+        const int c = 32 * (w0 + i) + 8 * (lane >> 3) + 7 - (lane & 7);
+        idx0[i] = (w0 + i < a.n_words && c < a.width)
+                      ? col_off[c] + band_base[static_cast<int64_t>(band) * a.n_words * 32 + c] : 0;
+    }
+    // Phase 1: differences against the row above (all chunks and words: independent
+    // shuffles), then the transposes of the chunks that change.
+    uint64_t changed = 0;  // bit kW*q + i: chunk q of word i has a transition
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        uint32_t d = 0;
+#pragma unroll
+        for (int i = 0; i < kW; ++i) {
+            const uint32_t xu = __shfl_up_sync(0xFFFFFFFFu, x[q][i], 1);
+            const uint32_t last = q == 0 ? aw[i] : __shfl_sync(0xFFFFFFFFu, x[q > 0 ? q - 1 : 0][i], 31);
+            d |= static_cast<uint32_t>(x[q][i] != (lane == 0 ? last : xu)) << i;
+        }
+        if (y0 + 32 * q >= y1) d = 0;
+        changed |= static_cast<uint64_t>(__reduce_or_sync(0xFFFFFFFFu, d)) << (kW * q);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if ((changed >> (kW * q)) & ((1u << kW) - 1u)) {  // warp-uniform (kW <= 8)
+#pragma unroll
+            for (int i = 0; i < kW; ++i) x[q][i] = warp_transpose32(x[q][i], lane);
+        }
+    }
+    // Phase 2.
+    uint16_t* slot = &stage[wib][lane * kSlot];
+    const bool last_band = band == a.n_bands - 1;
+    // Rolled loops from here on (the walk body exists once: a fully unrolled
+    // 4-word x 8-chunk walk overflowed the instruction cache): word i's chunks are
+    // selected out of x into cur[] and shifted through it.
+#pragma unroll 1
+    for (int i = 0; i < kW; ++i) {
+        const int w = w0 + i;
+        if (w >= a.n_words) break;  // warp-uniform
+        const int c = 32 * w + 8 * (lane >> 3) + 7 - (lane & 7);
+        const bool live = c < a.width;
+        uint32_t cur[8];
+        uint32_t awi = aw[0];
+        int64_t idx = idx0[0];
+#pragma unroll
+        for (int k = 1; k < kW; ++k)
+            if (i == k) {
+                awi = aw[k];
+                idx = idx0[k];
+            }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            cur[q] = x[q][0];
+#pragma unroll
+            for (int k = 1; k < kW; ++k) cur[q] = i == k ? x[q][k] : cur[q];
+        }
+        uint32_t prev = (awi >> lane) & 1u;
+        int top = -1;  // y_top of a run opened in this band and still open
+        int n = 0;     // staged records of this lane
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) {
+            const int yb = y0 + 32 * q;
+            const uint32_t s = cur[0];  // bit k = row yb + k
+#pragma unroll
+            for (int k = 0; k < 7; ++k) cur[k] = cur[k + 1];
+            if (!((changed >> (kW * q + i)) & 1u)) continue;  // rows repeat the row above (or past y1)
+            const int nk = min(32, y1 - yb);
+            const uint32_t valid = nk == 32 ? 0xFFFFFFFFu : (1u << nk) - 1u;
+            const uint32_t above = (s << 1) | prev;
+            uint32_t R = live ? s & ~above & valid : 0u;
+            uint32_t F = live ? above & ~s & valid : 0u;
+            const bool carried = prev != 0u;
+            prev = (s >> (nk - 1)) & 1u;
+            if (carried && F) {  // the first fall closes the run open at the chunk's top
+                const int f0 = __ffs(F) - 1;
+                F &= F - 1u;
+                if (top >= 0) {
+                    slot[n++] = static_cast<uint16_t>((top - y0) | ((yb + f0 - 1 - y0) << 8));
+                } else {
+                    runs[3 * (idx - 1) + 2] = yb + f0 - 1;  // opened in an earlier band
+                }
+                top = -1;
+            }
+            // Every remaining fall closes the rise just before it: pair them from the
+            // bottom (a rise with no fall after it opens the run left open).
+            int nf = __popc(F);
+            if (__popc(R) > nf) {
+                const int r = 31 - __clz(R);
+                top = yb + r;
+                R ^= 1u << r;
+            }
+            const int off = 32 * q;
+            int at = n + nf;
+            n = at;
+            while (nf > 0) {
+                const int r = 31 - __clz(R), f = 31 - __clz(F);
+                R ^= 1u << r;
+                F ^= 1u << f;
+                slot[--at] = static_cast<uint16_t>((off + r) | ((off + f - 1) << 8));
+                --nf;
+            }
+        }
+        __syncwarp();
+        band_write_out<kSlot>(stage[wib], lane, n, idx, w, y0, a.group, runs);
+        __syncwarp();
+        idx += n;
+        if (!live) continue;
+        if (last_band && prev) {  // the virtual background row H closes what is open
+            if (top >= 0) {
+                runs[3 * idx + 0] = c;
+                runs[3 * idx + 1] = top;
+                runs[3 * idx + 2] = a.height - 1;
+            } else {
+                runs[3 * (idx - 1) + 2] = a.height - 1;
+            }
+        } else if (top >= 0) {  // still open: a later band writes y_bot
+            runs[3 * idx + 0] = c;
+            runs[3 * idx + 1] = top;
+        }
+    }
+}
+
 }  // namespace
 
 extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t width, int32_t height,
@@ -414,19 +723,25 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
         profile_colscan_kernel<<<(width + 255) / 256, 256, 0, stream>>>(a, d_band_counts, d_counts);
         profile_offsets_kernel<<<1, 1024, 0, stream>>>(width, d_counts, d_col_off, d_n_runs);
     } else {  // fill
-        // Fill kernel by run density rho = runs per pixel, known from the count
-        // pass (measured on 21000^2, profiles/r01_fill_variants.md): the direct
-        // transposed walk wins on sparse masks (hbands rho 0.007, checker(21)
-        // 0.024), the staged coalesced write-out on denser ones (checker(7) 0.071,
-        // random 0.25).  The row-stepping kernel is kept for A/B.
-        // YCHG_FILL_KERNEL=direct|rowwise|staged forces one.
+        // Fill kernel: the band-staged kernel whenever the rows and the output are
+        // 16-byte aligned (always, for the library's own buffers): on 21000^2 it
+        // beats every walk kernel at every density (profiles/r02_fill_ncu.md:
+        // hbands 77 -> 74 us, checker(21) 197 -> 127, checker(7) 501 -> 208, random
+        // 1053 -> 402).  Otherwise by run density rho = runs per pixel, known from
+        // the count pass (profiles/r01_fill_variants.md): the direct transposed walk
+        // on sparse masks, the staged coalesced write-out on denser ones.
+        // YCHG_FILL_KERNEL=direct|rowwise|staged|band forces one.
         const double rho = static_cast<double>(n_runs_hint) / (static_cast<double>(width) * height);
-        int kind = rho < 0.04 ? 0 : 2;
+        int kind = 3;
         if (const char* f = std::getenv("YCHG_FILL_KERNEL")) {
             if (!std::strcmp(f, "direct")) kind = 0;
             else if (!std::strcmp(f, "rowwise")) kind = 1;
             else if (!std::strcmp(f, "staged")) kind = 2;
+            else if (!std::strcmp(f, "band")) kind = 3;
         }
+        const bool aligned = (reinterpret_cast<uintptr_t>(d_bits) & 15u) == 0 && (pitch & 15) == 0 &&
+                             (reinterpret_cast<uintptr_t>(d_runs) & 15u) == 0;
+        if (kind == 3 && !aligned) kind = rho < 0.04 ? 0 : 2;  // 16-byte row loads, 8-byte record stores
         // Grid order (profiles/r02_fill_ncu.md, 21000^2): band-major for the staged
         // kernel (checker(7) 552 -> 498 us, random 1154 -> 1053, checker(21) 334 -> 239)
         // and for the direct walk on very sparse masks (hbands 100 -> 77 us);
@@ -442,6 +757,13 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
         } else if (kind == 1) {
             profile_fill_rowwise_kernel<<<static_cast<unsigned>((fill_warps + 7) / 8), 256, 0, stream>>>(
                 a, d_band_counts, d_col_off, d_runs);
+        } else if (kind >= 3) {
+            constexpr int kw = 4;
+            a.group = 0;  // band kernels: write-out mode (0 auto, 1 per column, 2 flat)
+            if (const char* v = std::getenv("YCHG_FILL_WRITEOUT"); v && *v) a.group = std::atoi(v);  // A/B hook
+            const int64_t units = static_cast<int64_t>((a.n_words + kw - 1) / kw) * a.n_bands;
+            const unsigned blocks_b = static_cast<unsigned>((units + kBandWarps - 1) / kBandWarps);
+            profile_fill_band_kernel<kw><<<blocks_b, kBandWarps * 32, 0, stream>>>(a, d_band_counts, d_col_off, d_runs);
         } else {
             constexpr int wpc = fill_warps_per_cta<true>();
             profile_fill_kernel<true><<<static_cast<unsigned>((unit_warps + wpc - 1) / wpc), wpc * 32, 0, stream>>>(

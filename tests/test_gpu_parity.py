@@ -315,12 +315,13 @@ def test_build_profile_invariants_and_large(gpu, orc):
             assert np.array_equal(y.column_runs(y.BinaryImage(sp.width, sp.height, bits), c), p.runs(c)), (sp, c)
 
 
-@pytest.mark.parametrize("kind", ["direct", "rowwise", "staged"])
+@pytest.mark.parametrize("kind", ["direct", "rowwise", "staged", "band"])
 def test_build_profile_each_fill_kernel(gpu, orc, monkeypatch, kind):
-    """The three fill kernels (chosen by run density; YCHG_FILL_KERNEL forces one)
+    """The four fill kernels (band-staged by default; YCHG_FILL_KERNEL forces one)
     on the golden corpus and on band / width / height edges: 255/256/257 and
-    511/513 rows (partial bands and chunks), widths off the 32-column word and the
-    8-column byte, runs crossing bands, open at the last row, one-row masks."""
+    511/513 rows (partial bands and chunks), widths off the 32-column word, the
+    8-column byte and the band kernel's 4-word group, runs crossing bands, open at
+    the last row, one-row masks, 128 runs per column and band (checker(1))."""
     y = gpu
     monkeypatch.setenv("YCHG_FILL_KERNEL", kind)
     specs = [spec_of(row["spec"]) for row in corpus()]
