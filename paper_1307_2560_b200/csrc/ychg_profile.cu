@@ -391,30 +391,9 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
     }
 }
 
-// P3: fill, band-staged.  One warp per (256-row band, group of kW words): lane k
-// loads rows y0+32q+k of the whole group with 16-byte loads up front (8 x kW/4
-// independent loads, half or whole 32 B sectors instead of 4 B of each), then walks
-// the group's words one at a time.  For each word, a warp bit transpose per 32-row
-// chunk gives lane j its column's 32-row bit sequence; the runs that open and close
-// inside the band are paired rise <-> fall in lockstep (the k-th fall of a chunk,
-// after the one closing a run carried in from above, closes the k-th rise) and
-// staged as ONE 16-bit entry {top - y0, bot - y0} in the lane's shared-memory slot
-// (<= 128 per band).  At the end of the word's band the warp writes every column's
-// staged records out column by column, lanes = consecutive records, so each store
-// instruction covers a contiguous stretch of one column's list (12 B stride) and
-// the column's band piece is written in one pass -- no per-chunk flush.  The two
-// boundary records are written directly as in the walk kernel: the y_bot of a run
-// opened in an earlier band (index base-1), and {c, y_top} of a run left open at
-// the band's bottom (its y_bot comes from a later band or the virtual row H).
 constexpr int kBandWarps = 4;
 static_assert(kBandRows == 256, "band_write_column: <= 128 records per column and band, 2 per lane and pass");
 
-// Write-out of a warp's staged records (word w, band rows from y0): lane l holds
-// n_l 16-bit entries {top - y0 | (bot - y0) << 8} for column l of the word, to be
-// stored at runs[idx_l ..].  Many records: column by column, lanes = consecutive
-// records of one column (each store instruction covers a contiguous stretch of
-// one column's list).  Few (sparse masks, 0-2 per column): one flat pass, record t
-// found in its lane's slot by a binary search over the lanes' exclusive offsets.
 // One column's m (<= 128) staged records as 12-byte {c, top, bot} at
 // runs[3*base ..], as 8-byte vector stores: the piece's ints are c, t0, b0, c, t1,
 // b1, ...; from its first 8-byte boundary (h = 0 or 1 ints in) lane p writes the
