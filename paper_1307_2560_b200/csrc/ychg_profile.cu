@@ -392,6 +392,7 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
 }
 
 constexpr int kBandWarps = 4;
+constexpr int kFlatMax = 1024;  // records of one flat write-out pass (the auto rule stays below ~800)
 static_assert(kBandRows == 256, "band_write_column: <= 128 records per column and band, 2 per lane and pass");
 
 // One column's m (<= 128) staged records as 12-byte {c, top, bot} at
@@ -431,43 +432,31 @@ __device__ __forceinline__ void band_write_column(const uint16_t* __restrict__ s
     }
 }
 
-template <int kSlot>
-__device__ __forceinline__ void band_write_flat(const uint16_t* __restrict__ stage, int lane, int off, int64_t idx,
-                                                int t, int total, int w, int y0, int32_t* __restrict__ runs) {
-    int l = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1) {
-        const int e = __shfl_sync(0xFFFFFFFFu, off, l + step);
-        if (e <= t) l += step;
-    }
-    const int j = t - __shfl_sync(0xFFFFFFFFu, off, l);
-    const int64_t base = __shfl_sync(0xFFFFFFFFu, idx, l);
-    if (t < total) {
-        const uint32_t e = stage[l * kSlot + j];
-        int32_t* dst = runs + 3 * (base + j);
-        dst[0] = 32 * w + 8 * (l >> 3) + 7 - (l & 7);
-        dst[1] = y0 + static_cast<int>(e & 0xFFu);
-        dst[2] = y0 + static_cast<int>(e >> 8);
-    }
-}
-
 // Write-out of a warp's staged records (word w, band rows from y0): lane l holds
 // n_l 16-bit entries {top - y0 | (bot - y0) << 8} for column l of the word, to be
 // stored at runs[idx_l ..].  Many records: column by column, lanes = consecutive
-// records of one column (each store instruction covers a contiguous stretch of
-// one column's list).  Few (sparse masks, 0-2 per column): one flat pass, record t
-// found in its lane's slot by a binary search over the lanes' exclusive offsets.
-// Both loops handle two independent columns / 32-record groups per iteration.
+// records of one column (band_write_column's 8-byte vectors), two independent
+// columns per iteration.  Fewer (<= ~25 per column): one flat pass over the warp's
+// records packed 32 per iteration -- record t's lane comes from a shared-memory
+// owner table each lane fills for its own range, its destination from the lane's
+// precomputed {entry offset, int base}.
+struct FlatTables {
+    uint8_t owner[kFlatMax];
+    int32_t eoff[32];
+    int64_t gbase[32];
+};
+
 template <int kSlot>
-__device__ __forceinline__ void band_write_out(const uint16_t* __restrict__ stage, int lane, int n, int64_t idx, int w,
-                                               int y0, int mode, int32_t* __restrict__ runs) {
+__device__ __forceinline__ void band_write_out(const uint16_t* __restrict__ stage, FlatTables& ft, int lane, int n,
+                                               int64_t idx, int w, int y0, int mode, int32_t* __restrict__ runs) {
     const int total = static_cast<int>(__reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned>(n)));
 #ifdef YCHG_DIAG_FILL_NOSTORE  // diagnostics build: staged records are never written (wrong output, timing only)
     if (total >= 0) return;
 #endif
     if (total == 0) return;
     const uint32_t nonempty = __ballot_sync(0xFFFFFFFFu, n > 0);
-    const bool flat = mode == 2 || (mode == 0 && (total + 31) / 32 * 5 <= __popc(nonempty) * 4);
+    const bool flat = total <= kFlatMax &&
+                      (mode == 2 || (mode == 0 && (total + 31) / 32 * 5 <= __popc(nonempty) * 4));
     if (flat) {
         int inc = n;
 #pragma unroll
@@ -476,10 +465,19 @@ __device__ __forceinline__ void band_write_out(const uint16_t* __restrict__ stag
             if (lane >= o) inc += t;
         }
         const int off = inc - n;
-        for (int t0 = 0; t0 < total; t0 += 64) {
-            band_write_flat<kSlot>(stage, lane, off, idx, t0 + lane, total, w, y0, runs);
-            band_write_flat<kSlot>(stage, lane, off, idx, t0 + 32 + lane, total, w, y0, runs);
+        for (int j = 0; j < n; ++j) ft.owner[off + j] = static_cast<uint8_t>(lane);
+        ft.eoff[lane] = lane * kSlot - off;
+        ft.gbase[lane] = 3 * (idx - off);
+        __syncwarp();
+        for (int t = lane; t < total; t += 32) {
+            const int l = ft.owner[t];
+            const uint32_t e = stage[ft.eoff[l] + t];
+            int32_t* dst = runs + ft.gbase[l] + 3 * t;
+            dst[0] = 32 * w + 8 * (l >> 3) + 7 - (l & 7);
+            dst[1] = y0 + static_cast<int>(e & 0xFFu);
+            dst[2] = y0 + static_cast<int>(e >> 8);
         }
+        __syncwarp();
     } else {
         uint32_t pending = nonempty;
         while (pending) {
@@ -519,6 +517,7 @@ __global__ void __launch_bounds__(kBandWarps * 32) profile_fill_band_kernel(cons
     constexpr int kV = kW / 4;
     constexpr int kSlot = 130;  // <= 128 entries per lane and band (+2: odd word stride)
     __shared__ uint16_t stage[kBandWarps][32 * kSlot];
+    __shared__ FlatTables flat_tabs[kBandWarps];
     const int wib = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int n_groups = (a.n_words + kW - 1) / kW;
@@ -658,7 +657,7 @@ __global__ void __launch_bounds__(kBandWarps * 32) profile_fill_band_kernel(cons
             }
         }
         __syncwarp();
-        band_write_out<kSlot>(stage[wib], lane, n, idx, w, y0, a.group, runs);
+        band_write_out<kSlot>(stage[wib], flat_tabs[wib], lane, n, idx, w, y0, a.group, runs);
         __syncwarp();
         idx += n;
         if (!live) continue;
