@@ -393,33 +393,23 @@ __global__ void __launch_bounds__(fill_warps_per_cta<kStaged>() * 32) profile_fi
 
 constexpr int kBandWarps = 4;
 constexpr int kFlatMax = 1024;  // records of one flat write-out pass (the auto rule stays below ~800)
-static_assert(kBandRows == 256, "band_write_column: <= 128 records per column and band, 2 per lane and pass");
+static_assert(kBandRows == 256, "band_write_pairs: <= 128 records per column and band, 2 per lane and pass");
 
-// One column's m (<= 128) staged records as 12-byte {c, top, bot} at
-// runs[3*base ..], as 8-byte vector stores: the piece's ints are c, t0, b0, c, t1,
-// b1, ...; from its first 8-byte boundary (h = 0 or 1 ints in) lane p writes the
-// three int2 holding ints h+6p .. h+6p+5 (records 2p, 2p+1: one 32-bit shared
-// load) -- whole sectors per store instruction instead of 12-byte-strided
-// partial ones.  At most one int before the boundary (always c) and one after
-// the last whole vector (always the last record's bot) are written singly.
-template <int kSlot>
-__device__ __forceinline__ void band_write_column(const uint16_t* __restrict__ stage, int lane, int l, int m,
-                                                  int64_t base, int w, int y0, int32_t* __restrict__ runs) {
-    if (m == 0) return;
-    const int cl = 32 * w + 8 * (l >> 3) + 7 - (l & 7);
-    const uint16_t* src = stage + l * kSlot;
-    const int64_t g = 3 * base;  // the piece's first int
-    const int h = static_cast<int>(g & 1);
-    const int body = 3 * m - h;  // ints from the boundary on
-    if (lane == 0 && h) runs[g] = cl;
-    if (lane == 1 && (body & 1)) runs[g + 3 * m - 1] = y0 + static_cast<int>(src[m - 1] >> 8);
-    int2* vd = reinterpret_cast<int2*>(runs + g + h);
-    const int nv = body >> 1;  // whole int2
+// The vector part of one column's piece of 12-byte records {c, top, bot}: the
+// piece's ints are c, t0, b0, c, t1, b1, ...; from its first 8-byte boundary
+// (h = 0 or 1 ints in, at vd) lane p writes the three int2 holding ints
+// h+6p .. h+6p+5 (records 2p, 2p+1: one 32-bit shared load) -- whole sectors per
+// store instruction instead of 12-byte-strided partial ones.  nvh = 2 * (whole
+// int2) + h.  The <= 1 int before the boundary and after the last whole int2 are
+// written by the column's own lane (band_write_out).
+__device__ __forceinline__ void band_write_pairs(const uint16_t* __restrict__ src, int lane, int cl, int nvh,
+                                                 int2* __restrict__ vd, int y0) {
+    const int nv = nvh >> 1, h = nvh & 1;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int pr = lane + 32 * k;  // record pair
-        if (3 * pr >= nv) break;       // this lane is past the piece
-        const uint32_t e = reinterpret_cast<const uint32_t*>(src)[pr];  // entries 2pr, 2pr+1 (reads past m are never stored)
+    for (int k = 0; k < 2; ++k) {  // <= 128 records = 64 pairs
+        const int pr = lane + 32 * k;
+        if (3 * pr >= nv) break;  // this lane is past the piece
+        const uint32_t e = reinterpret_cast<const uint32_t*>(src)[pr];  // entries 2pr, 2pr+1 (reads past the piece are never stored)
         const int t0 = y0 + static_cast<int>(e & 0xFFu), b0 = y0 + static_cast<int>((e >> 8) & 0xFFu);
         const int t1 = y0 + static_cast<int>((e >> 16) & 0xFFu), b1 = y0 + static_cast<int>(e >> 24);
         // h = 0: (c,t0) (b0,c) (t1,b1);  h = 1: (t0,b0) (c,t1) (b1,c)
@@ -479,18 +469,30 @@ __device__ __forceinline__ void band_write_out(const uint16_t* __restrict__ stag
         }
         __syncwarp();
     } else {
+        // Each lane prepares its own column's piece (the single head / tail ints and
+        // the vector run's address and length); then column by column, two
+        // independent columns per iteration, the warp writes the vector runs.
+        const int64_t g = 3 * idx;
+        const int h = static_cast<int>(g & 1);
+        const int body = 3 * n - h;
+        if (n > 0) {
+            if (h) runs[g] = 32 * w + 8 * (lane >> 3) + 7 - (lane & 7);
+            if (body & 1) runs[g + 3 * n - 1] = y0 + static_cast<int>(stage[lane * kSlot + n - 1] >> 8);
+        }
+        const int nvh = ((body >> 1) << 1) | h;
+        int2* const vd = reinterpret_cast<int2*>(runs + g + h);
         uint32_t pending = nonempty;
         while (pending) {
             const int l1 = __ffs(pending) - 1;
             pending &= pending - 1u;
             const int l2 = pending ? __ffs(pending) - 1 : l1;
             pending &= pending - 1u;
-            const int m1 = __shfl_sync(0xFFFFFFFFu, n, l1);
-            const int m2 = l2 != l1 ? __shfl_sync(0xFFFFFFFFu, n, l2) : 0;
-            const int64_t b1 = __shfl_sync(0xFFFFFFFFu, idx, l1);
-            const int64_t b2 = __shfl_sync(0xFFFFFFFFu, idx, l2);
-            band_write_column<kSlot>(stage, lane, l1, m1, b1, w, y0, runs);
-            band_write_column<kSlot>(stage, lane, l2, m2, b2, w, y0, runs);
+            const int q1 = __shfl_sync(0xFFFFFFFFu, nvh, l1);
+            const int q2 = l2 != l1 ? __shfl_sync(0xFFFFFFFFu, nvh, l2) : 0;
+            int2* const d1 = reinterpret_cast<int2*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(vd), l1));
+            int2* const d2 = reinterpret_cast<int2*>(__shfl_sync(0xFFFFFFFFu, reinterpret_cast<uintptr_t>(vd), l2));
+            band_write_pairs(stage + l1 * kSlot, lane, 32 * w + 8 * (l1 >> 3) + 7 - (l1 & 7), q1, d1, y0);
+            band_write_pairs(stage + l2 * kSlot, lane, 32 * w + 8 * (l2 >> 3) + 7 - (l2 & 7), q2, d2, y0);
         }
     }
 }
