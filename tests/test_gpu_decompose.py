@@ -77,6 +77,22 @@ def test_decompose_large_vs_oracle(gpu, orc, sp):
     assert got.edge_count == orc.hyperedges(bits, sp.width)[0]
 
 
+@pytest.mark.parametrize("cell", [1, 7, 23, 24, 25, 48, 200])
+def test_decompose_chain_lengths_around_the_walk(gpu, orc, cell):
+    """Chains of `cell` runs (checker(cell): every chain exactly cell columns long)
+    around the emit kernel's walk length (24: heads walk their chains and stage a
+    warp's output stretch in shared memory; longer chains are finished run by run
+    by decomp_long_kernel), plus ragged edges (widths not a multiple of cell)."""
+    y = gpu
+    for w, h in ((cell * 11 + 5, 257), (cell * 3 + 1, 1000)):
+        sp = Spec.checker(w, h, cell)
+        bits = orc.synth(sp)
+        want = orc.decompose(bits, sp.width)
+        got = y.decompose(y.BinaryImage(sp.width, sp.height, bits))
+        for a, b in zip(as_tuple(got), want):
+            assert np.array_equal(a, b), (cell, w, h)
+
+
 def test_decompose_profile_input_and_validation(gpu, orc):
     y = gpu
     sp = Spec.random(97, 61, 0.4, 5)
