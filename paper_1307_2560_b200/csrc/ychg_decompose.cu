@@ -9,15 +9,16 @@
 //               disjoint intervals) for its first overlapping run and a
 //               saturating overlap count (0, 1, 2+)              (:108-135)
 //   D2 link     r -> s iff r's only right overlap is s and s's only left
-//               overlap is r (mutual uniqueness, :136-143); every run starts a
-//               list-ranking node {ancestor, distance} on its left link
-//   D3 jump     pointer jumping until every node names its chain head (chains
-//               are at most W long: <= ceil(log2 W) rounds)
-//   D4 tails    each chain tail stores (1 edge, chain length) at its head
-//   D5 scan     exclusive scan of those (edges, runs) pairs in profile order =
-//               the canonical edge id and first output slot of every head --
-//               chains are numbered by their head's (column, y_top), exactly the
-//               reference's discovery order (:145-167)
+//               overlap is r (mutual uniqueness, :136-143); anc[r] = left link
+//               (or r for a chain head)
+//   D3 jump     one launch of concurrent pointer jumping to the chain heads
+//               (a run's distance to its head is its column difference)
+//   D4 tails    every chain tail stores the chain length at its head
+//   D5 scan     one-pass (decoupled look-back) exclusive scan of {1 edge, chain
+//               length} at the heads in profile order = the canonical edge id and
+//               first output slot of every head -- chains are numbered by their
+//               head's (column, y_top), exactly the reference's discovery order
+//               (:145-167)
 //   D6 emit     each head of a short chain walks it and writes its runs to
 //               consecutive slots from offset(head); runs of long chains go to
 //               offset(head) + distance one by one; run_to_edge[g] = id(head)
@@ -31,8 +32,8 @@ namespace {
 
 constexpr uint32_t kNoLink = 0xFFFFFFFFu;
 constexpr int kThreadsD = 256;
-constexpr int kScanItems = 8;                       // u64 items per thread in the scan tiles
-constexpr int kScanTile = kThreadsD * kScanItems;   // 2048
+constexpr int kScanItems = 16;                      // items per thread in the scan tiles
+constexpr int kScanTile = kThreadsD * kScanItems;   // 4096
 
 __device__ __forceinline__ unsigned long long pack(uint32_t hi, uint32_t lo) {
     return (static_cast<unsigned long long>(hi) << 32) | lo;
@@ -120,52 +121,76 @@ __global__ void __launch_bounds__(kThreadsD) decomp_overlap_kernel(const int32_t
 }
 
 // D2: mutual-uniqueness links; pr[g] becomes the right link (or kNoLink) and
-// node[g] = {left neighbour, 1} or {g, 0} for a chain head.
+// anc[g] the left link, or g itself for a chain head.
 __global__ void __launch_bounds__(kThreadsD) decomp_link_kernel(int64_t n, uint32_t* __restrict__ pr,
                                                                 const uint32_t* __restrict__ pl,
                                                                 const uint8_t* __restrict__ ov,
-                                                                unsigned long long* __restrict__ node) {
+                                                                uint32_t* __restrict__ anc) {
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
         const uint32_t o = ov[g];
         const uint32_t r = pr[g], l = pl[g];
         const bool right = (o & 3u) == 1u && (ov[r] >> 2) == 1u;
         const bool left = (o >> 2) == 1u && (ov[l] & 3u) == 1u;
         pr[g] = right ? r : kNoLink;
-        node[g] = left ? pack(l, 1u) : pack(static_cast<uint32_t>(g), 0u);
+        anc[g] = left ? l : static_cast<uint32_t>(g);
     }
 }
 
-// D3: one pointer-jumping round, in place ({ancestor, distance} pairs are read
-// and written as single 64-bit words, so a concurrently advanced pair is still
-// a consistent, only further-along, answer).
-__global__ void __launch_bounds__(kThreadsD) decomp_jump_kernel(int64_t n, unsigned long long* __restrict__ node,
-                                                                int* __restrict__ changed) {
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+    return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// D3: chain heads by concurrent pointer jumping in ONE launch: every run chases
+// its ancestor pointer to the head (a fixed point), storing each step back so the
+// runs behind it skip ahead (every stored value is an ancestor in the same chain:
+// the races only ever shorten a path).  Chains run left to right one column per
+// link, so a run's distance to its head is col(run) - col(head) and needs no
+// bookkeeping.  (Replaces synchronous rounds over {ancestor, distance} pairs, one
+// host round trip each.)
+__global__ void __launch_bounds__(kThreadsD) decomp_jump_kernel(int64_t n, uint32_t* __restrict__ anc) {
+    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t a = ld_volatile(anc + g);
+        if (a == static_cast<uint32_t>(g)) continue;
+        uint32_t b = ld_volatile(anc + a);
+        if (b == a) continue;  // the left neighbour heads the chain
+        for (;;) {
+            a = b;
+            b = ld_volatile(anc + a);
+            if (b == a) break;
+            anc[g] = b;  // relaxed: a further ancestor for whoever reads it next
+        }
+        anc[g] = a;
+    }
+}
+
+constexpr int kWalkMax = 24;  // chains up to this long are walked from their head
+
+// D4: every chain tail stores the chain's length (its column difference + 1) at
+// the head; *long_flag marks that D6 has chains longer than kWalkMax.
+__global__ void __launch_bounds__(kThreadsD) decomp_tail_kernel(int64_t n, const int32_t* __restrict__ runs,
+                                                                const uint32_t* __restrict__ pr,
+                                                                const uint32_t* __restrict__ anc,
+                                                                uint32_t* __restrict__ head_len,
+                                                                int* __restrict__ long_flag) {
     bool any = false;
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
-        const unsigned long long v = node[g];
-        const uint32_t a = static_cast<uint32_t>(v >> 32);
-        if (a == static_cast<uint32_t>(g)) continue;
-        const unsigned long long w = node[a];
-        const uint32_t a2 = static_cast<uint32_t>(w >> 32);
-        if (a2 == a) continue;  // a is a head: done
-        node[g] = pack(a2, static_cast<uint32_t>(v) + static_cast<uint32_t>(w));
-        any = true;
-    }
-    if (__syncthreads_or(any) && threadIdx.x == 0) *changed = 1;
-}
-
-// D4: every chain tail (no right link) stores {1 edge, chain length} at its head.
-__global__ void __launch_bounds__(kThreadsD) decomp_tail_kernel(int64_t n, const uint32_t* __restrict__ pr,
-                                                                const unsigned long long* __restrict__ node,
-                                                                unsigned long long* __restrict__ val) {
-    for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
         if (pr[g] != kNoLink) continue;
-        const unsigned long long v = node[g];
-        val[v >> 32] = pack(1u, static_cast<uint32_t>(v) + 1u);
+        const uint32_t h = anc[g];
+        const uint32_t len = static_cast<uint32_t>(__ldg(runs + 3 * g) - __ldg(runs + 3 * int64_t(h))) + 1u;
+        head_len[h] = len;
+        any |= len > static_cast<uint32_t>(kWalkMax);
     }
+    if (__syncthreads_or(any) && threadIdx.x == 0) *long_flag = 1;
 }
 
-// D5: exclusive scan of u64 in three passes (tile sums, spine, tiles).
+// D5: exclusive scan of {1 edge, chain length} at every chain head (0 elsewhere)
+// in profile order: excl[head] = {edge id, first output slot} -- edges are
+// numbered by their head's (column, y_top), exactly the reference's discovery
+// order (hypergraph.cpp:145-167).  Reduce-then-scan over tiles of kScanTile runs
+// (tile sums, one CTA over the tile sums, tiles); the items are computed from
+// anc / head_len on the fly, and only heads are written.  (A one-pass decoupled
+// look-back was slower here: ~1000 tiles in flight made every look-back walk
+// hundreds of published aggregates.)
 __device__ __forceinline__ unsigned long long block_exclusive(unsigned long long x, unsigned long long* sh,
                                                               unsigned long long* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -178,15 +203,16 @@ __device__ __forceinline__ unsigned long long block_exclusive(unsigned long long
     if (lane == 31) sh[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        unsigned long long s = lane < kThreadsD / 32 ? sh[lane] : 0ull;
+        const int nw = blockDim.x / 32;
+        unsigned long long s = lane < nw ? sh[lane] : 0ull;
         unsigned long long si = s;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long t = __shfl_up_sync(0xFFFFFFFFu, si, o);
             if (lane >= o) si += t;
         }
-        if (lane < kThreadsD / 32) sh[lane] = si - s;
-        if (lane == kThreadsD / 32 - 1) sh[32] = si;
+        if (lane < nw) sh[lane] = si - s;
+        if (lane == nw - 1) sh[32] = si;
     }
     __syncthreads();
     const unsigned long long r = sh[warp] + inc - x;
@@ -195,79 +221,99 @@ __device__ __forceinline__ unsigned long long block_exclusive(unsigned long long
     return r;
 }
 
-__global__ void __launch_bounds__(kThreadsD) scan_tile_sums_kernel(const unsigned long long* __restrict__ v, int64_t n,
-                                                                   unsigned long long* __restrict__ sums) {
+__device__ __forceinline__ unsigned long long head_item(int64_t g, int64_t n, const uint32_t* __restrict__ anc,
+                                                        const uint32_t* __restrict__ head_len) {
+    return g < n && anc[g] == static_cast<uint32_t>(g) ? pack(1u, head_len[g]) : 0ull;
+}
+
+__global__ void __launch_bounds__(kThreadsD) decomp_scan_sums_kernel(int64_t n, const uint32_t* __restrict__ anc,
+                                                                     const uint32_t* __restrict__ head_len,
+                                                                     unsigned long long* __restrict__ sums) {
     __shared__ unsigned long long sh[33];
     const int64_t base = blockIdx.x * int64_t(kScanTile) + threadIdx.x * int64_t(kScanItems);
     unsigned long long s = 0;
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i)
-        if (base + i < n) s += v[base + i];
+    for (int i = 0; i < kScanItems; ++i) s += head_item(base + i, n, anc, head_len);
     unsigned long long tot;
     block_exclusive(s, sh, &tot);
     if (threadIdx.x == 0) sums[blockIdx.x] = tot;
 }
 
-// One CTA: exclusive scan of the tile sums in place; the grand total to *total.
-__global__ void __launch_bounds__(kThreadsD) scan_spine_kernel(unsigned long long* __restrict__ sums, int64_t tiles,
-                                                               unsigned long long* __restrict__ total) {
+// One CTA (1024 threads): exclusive scan of the tile sums in place; the grand
+// total to *total.
+__global__ void __launch_bounds__(1024) decomp_scan_spine_kernel(unsigned long long* __restrict__ sums, int64_t tiles,
+                                                                 unsigned long long* __restrict__ total) {
     __shared__ unsigned long long sh[33];
+    constexpr int kPer = 8;
     unsigned long long carry = 0;
-    for (int64_t b = 0; b < tiles; b += kThreadsD) {
-        const int64_t i = b + threadIdx.x;
-        const unsigned long long x = i < tiles ? sums[i] : 0ull;
+    for (int64_t b = 0; b < tiles; b += 1024 * kPer) {
+        const int64_t i0 = b + threadIdx.x * int64_t(kPer);
+        unsigned long long x[kPer], s = 0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            x[k] = i0 + k < tiles ? sums[i0 + k] : 0ull;
+            s += x[k];
+        }
         unsigned long long tot;
-        const unsigned long long e = block_exclusive(x, sh, &tot);
-        if (i < tiles) sums[i] = carry + e;
+        unsigned long long run = carry + block_exclusive(s, sh, &tot);
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (i0 + k < tiles) {
+                sums[i0 + k] = run;
+                run += x[k];
+            }
         carry += tot;
     }
     if (threadIdx.x == 0) *total = carry;
 }
 
-__global__ void __launch_bounds__(kThreadsD) scan_tiles_kernel(unsigned long long* __restrict__ v, int64_t n,
-                                                               const unsigned long long* __restrict__ sums) {
+__global__ void __launch_bounds__(kThreadsD) decomp_scan_kernel(int64_t n, const uint32_t* __restrict__ anc,
+                                                                const uint32_t* __restrict__ head_len,
+                                                                const unsigned long long* __restrict__ sums,
+                                                                unsigned long long* __restrict__ excl) {
     __shared__ unsigned long long sh[33];
     const int64_t base = blockIdx.x * int64_t(kScanTile) + threadIdx.x * int64_t(kScanItems);
     unsigned long long x[kScanItems];
     unsigned long long s = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        x[i] = base + i < n ? v[base + i] : 0ull;
+        x[i] = head_item(base + i, n, anc, head_len);
         s += x[i];
     }
     unsigned long long tot;
     unsigned long long run = sums[blockIdx.x] + block_exclusive(s, sh, &tot);
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i)
-        if (base + i < n) {
-            v[base + i] = run;
+    for (int q = 0; q < kScanItems; q += 4) {  // whole 32-byte sectors that hold a head
+        const bool any = (x[q] | x[q + 1] | x[q + 2] | x[q + 3]) != 0;
+#pragma unroll
+        for (int i = q; i < q + 4; ++i) {
+            if (any && base + i < n) excl[base + i] = run;
             run += x[i];
         }
+    }
 }
 
 // D6: runs into hyperedge order, the run -> edge map, the edge offsets.  Each
-// chain head walks its chain along the right links (at most kWalkMax runs) and
-// writes the records to consecutive output slots.  The heads among a warp's 32
+// head of a chain of <= kWalkMax runs walks it along the right links and writes
+// the records to consecutive output slots.  The heads among a warp's 32
 // consecutive runs are consecutive edges, so their chains fill one contiguous
 // stretch of the output: staged in shared memory in output order (its first
 // kEmitStage records; the rest go straight out) and copied out with consecutive
 // 4-byte stores.  A run-by-run scatter to offset(head) + distance wrote 12-byte
 // pieces all over the output instead (one store instruction = 32 scattered
 // pieces; 2.5x DRAM write amplification, ~70 B per run at 21000^2 checker(7)).
-// Runs kWalkMax or more from their head (a walk would be that many dependent
-// loads) are scattered by decomp_long_kernel.
-constexpr int kWalkMax = 24;
+// Longer chains are written run by run by decomp_long_kernel.
 constexpr int kEmitStage = 256;  // records per warp staged in shared memory (3 KB)
 
 __global__ void __launch_bounds__(kThreadsD) decomp_emit_kernel(int64_t n, const int32_t* __restrict__ runs,
                                                                 const uint32_t* __restrict__ pr,
-                                                                const unsigned long long* __restrict__ node,
+                                                                const uint32_t* __restrict__ anc,
+                                                                const uint32_t* __restrict__ head_len,
                                                                 const unsigned long long* __restrict__ excl,
                                                                 const unsigned long long* __restrict__ total,
                                                                 int32_t* __restrict__ edge_runs,
                                                                 uint32_t* __restrict__ edge_offsets,
-                                                                uint32_t* __restrict__ run_to_edge,
-                                                                int* __restrict__ long_flag) {
+                                                                uint32_t* __restrict__ run_to_edge) {
     __shared__ int32_t stage[kThreadsD / 32][3 * kEmitStage];
     const int lane = threadIdx.x & 31;
     int32_t* st = stage[threadIdx.x >> 5];
@@ -276,15 +322,13 @@ __global__ void __launch_bounds__(kThreadsD) decomp_emit_kernel(int64_t n, const
         const int64_t g = g0 + lane;
         bool head = false;
         uint32_t e = 0, off = 0;
-        if (g < n) {
-            head = static_cast<uint32_t>(node[g] >> 32) == static_cast<uint32_t>(g);
-            if (head) {
-                const unsigned long long s = excl[g];
-                e = static_cast<uint32_t>(s >> 32);
-                off = static_cast<uint32_t>(s);
-                edge_offsets[e] = off;
-                if (g == 0) edge_offsets[*total >> 32] = static_cast<uint32_t>(n);  // run 0 always heads a chain
-            }
+        if (g < n && anc[g] == static_cast<uint32_t>(g)) {
+            const unsigned long long s = excl[g];
+            e = static_cast<uint32_t>(s >> 32);
+            off = static_cast<uint32_t>(s);
+            edge_offsets[e] = off;
+            if (g == 0) edge_offsets[*total >> 32] = static_cast<uint32_t>(n);  // run 0 always heads a chain
+            head = head_len[g] <= static_cast<uint32_t>(kWalkMax);  // a long chain: decomp_long_kernel
         }
         if (!__any_sync(0xFFFFFFFFu, head)) continue;  // members only: their heads write them
         const uint32_t first = __reduce_min_sync(0xFFFFFFFFu, head ? off : 0xFFFFFFFFu);
@@ -292,7 +336,6 @@ __global__ void __launch_bounds__(kThreadsD) decomp_emit_kernel(int64_t n, const
         if (head) {
             int64_t cur = g;
             const int sbase = static_cast<int>(off - first);  // staged slot of record 0 (may be past the stage)
-            bool ended = false;
             for (; d < kWalkMax; ++d) {
                 const int32_t c = __ldg(runs + 3 * cur), t = __ldg(runs + 3 * cur + 1), b = __ldg(runs + 3 * cur + 2);
                 const uint32_t next = pr[cur];
@@ -303,14 +346,15 @@ __global__ void __launch_bounds__(kThreadsD) decomp_emit_kernel(int64_t n, const
                 run_to_edge[cur] = e;
                 if (next == kNoLink) {
                     ++d;
-                    ended = true;
                     break;
                 }
                 cur = next;
             }
-            if (!ended) *long_flag = 1;  // runs kWalkMax and more from the head: decomp_long_kernel
         }
-        const uint32_t end = __reduce_max_sync(0xFFFFFFFFu, head ? off + static_cast<uint32_t>(d) : 0u);
+        // (a long chain between two short ones lies inside [first, end): the copy-out
+        // writes stale staged ints over its slots, and decomp_long_kernel, launched
+        // after this kernel, rewrites all of them)
+        const uint32_t end = __reduce_max_sync(0xFFFFFFFFu, head ? off + static_cast<uint32_t>(d) : first);
         __syncwarp();
         const int tot = 3 * static_cast<int>(min(end - first, static_cast<uint32_t>(kEmitStage)));
         int32_t* out = edge_runs + 3 * int64_t(first);
@@ -319,23 +363,24 @@ __global__ void __launch_bounds__(kThreadsD) decomp_emit_kernel(int64_t n, const
     }
 }
 
-// D6, runs kWalkMax or more from their head: slot offset(head) + distance.
+// D6, chains longer than kWalkMax: run g -> slot offset(head) + (col(g) - col(head)).
 __global__ void __launch_bounds__(kThreadsD) decomp_long_kernel(int64_t n, const int32_t* __restrict__ runs,
-                                                                const unsigned long long* __restrict__ node,
+                                                                const uint32_t* __restrict__ anc,
+                                                                const uint32_t* __restrict__ head_len,
                                                                 const unsigned long long* __restrict__ excl,
                                                                 const int* __restrict__ long_flag,
                                                                 int32_t* __restrict__ edge_runs,
                                                                 uint32_t* __restrict__ run_to_edge) {
     if (*long_flag == 0) return;
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
-        const unsigned long long v = node[g];
-        const uint32_t h = static_cast<uint32_t>(v >> 32), dist = static_cast<uint32_t>(v);
-        if (h == static_cast<uint32_t>(g) || dist < static_cast<uint32_t>(kWalkMax)) continue;  // walked by its head
+        const uint32_t h = anc[g];
+        if (head_len[h] <= static_cast<uint32_t>(kWalkMax)) continue;  // a short chain: its head's walk
+        const int32_t c = runs[3 * g], t = runs[3 * g + 1], b = runs[3 * g + 2];
         const unsigned long long s = excl[h];
-        const int64_t pos = int64_t(static_cast<uint32_t>(s)) + dist;
-        edge_runs[3 * pos] = runs[3 * g];
-        edge_runs[3 * pos + 1] = runs[3 * g + 1];
-        edge_runs[3 * pos + 2] = runs[3 * g + 2];
+        const int64_t pos = int64_t(static_cast<uint32_t>(s)) + (c - __ldg(runs + 3 * int64_t(h)));
+        edge_runs[3 * pos] = c;
+        edge_runs[3 * pos + 1] = t;
+        edge_runs[3 * pos + 2] = b;
         run_to_edge[g] = static_cast<uint32_t>(s >> 32);
     }
 }
@@ -388,8 +433,9 @@ extern "C" {
 // Scratch bytes the decomposition of n runs needs (ychg_launch_decompose's ws).
 int64_t ychg_decompose_ws_bytes(int64_t n) {
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-    // pr | pl (16-B rounded) | node | val | tile sums (+2) | flag (16 B) | ov
-    return ((n * 8 + 15) / 16) * 16 + n * 16 + (tiles + 2) * 8 + 16 + n + 256;
+    // pr | pl | anc | head_len (4 B each, 16-B rounded) | excl | tile sums | long flag (16 B) | ov
+    const int64_t r4 = ((n * 4 + 15) / 16) * 16;
+    return 4 * r4 + n * 8 + tiles * 8 + 16 + n + 256;
 }
 
 // Validate a host-supplied profile on the device; *d_err = min(g*4+kind) or ~0.
@@ -402,50 +448,40 @@ int ychg_launch_decompose_validate(const int32_t* d_runs, const int64_t* d_col_o
     return static_cast<int>(cudaGetLastError());
 }
 
-// The full decomposition of a device profile (n > 0).  h_flag must be pinned host
-// memory: the pointer-jumping rounds stop when a round changes nothing (one
-// stream synchronisation per round, <= ceil(log2 width) + 1 rounds).  Returns
-// the number of jump rounds run (>= 1) or -(cudaError_t).
+// The full decomposition of a device profile (n > 0), all on `stream` with no
+// host round trip.  Returns 1 or -(cudaError_t).  (h_flag is unused: kept for the
+// interface.)
 int ychg_launch_decompose(const int32_t* d_runs, const int64_t* d_col_off, const int32_t* d_counts, int32_t width,
                           int64_t n, void* d_ws, int32_t* d_edge_runs, uint32_t* d_edge_offsets,
                           uint32_t* d_run_to_edge, unsigned long long* d_total, int* h_flag, cudaStream_t stream) {
+    (void)h_flag;
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    const int64_t r4 = ((n * 4 + 15) / 16) * 16;
     uint8_t* p = static_cast<uint8_t*>(d_ws);
     uint32_t* pr = reinterpret_cast<uint32_t*>(p);
-    uint32_t* pl = pr + n;
-    unsigned long long* node = reinterpret_cast<unsigned long long*>(p + ((n * 8 + 15) / 16) * 16);
-    unsigned long long* val = node + n;
-    unsigned long long* sums = val + n;
-    int* flag = reinterpret_cast<int*>(sums + tiles + 2);
-    uint8_t* ov = reinterpret_cast<uint8_t*>(flag + 4);
+    uint32_t* pl = reinterpret_cast<uint32_t*>(p + r4);
+    uint32_t* anc = reinterpret_cast<uint32_t*>(p + 2 * r4);
+    uint32_t* head_len = reinterpret_cast<uint32_t*>(p + 3 * r4);
+    unsigned long long* excl = reinterpret_cast<unsigned long long*>(p + 4 * r4);
+    unsigned long long* sums = excl + n;
+    int* long_flag = reinterpret_cast<int*>(sums + tiles);
+    uint8_t* ov = reinterpret_cast<uint8_t*>(long_flag + 4);
     const int grid = grid_for(n);
+    const cudaError_t e0 = cudaMemsetAsync(long_flag, 0, 4, stream);
+    if (e0 != cudaSuccess) return -static_cast<int>(e0);
     decomp_overlap_kernel<<<grid, kThreadsD, 0, stream>>>(d_runs, d_col_off, d_counts, width, n, pr, pl, ov);
-    decomp_link_kernel<<<grid, kThreadsD, 0, stream>>>(n, pr, pl, ov, node);
-    int rounds = 0;
-    for (;;) {
-        cudaError_t e = cudaMemsetAsync(flag, 0, 4, stream);
-        if (e != cudaSuccess) return -static_cast<int>(e);
-        decomp_jump_kernel<<<grid, kThreadsD, 0, stream>>>(n, node, flag);
-        ++rounds;
-        e = cudaMemcpyAsync(h_flag, flag, 4, cudaMemcpyDeviceToHost, stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-        if (e != cudaSuccess) return -static_cast<int>(e);
-        if (*h_flag == 0) break;
-        if (rounds > 40) return -static_cast<int>(cudaErrorIllegalState);  // chains are <= width long
-    }
-    cudaError_t e = cudaMemsetAsync(val, 0, n * 8, stream);
-    if (e != cudaSuccess) return -static_cast<int>(e);
-    decomp_tail_kernel<<<grid, kThreadsD, 0, stream>>>(n, pr, node, val);
-    scan_tile_sums_kernel<<<static_cast<unsigned>(tiles), kThreadsD, 0, stream>>>(val, n, sums);
-    scan_spine_kernel<<<1, kThreadsD, 0, stream>>>(sums, tiles, d_total);
-    scan_tiles_kernel<<<static_cast<unsigned>(tiles), kThreadsD, 0, stream>>>(val, n, sums);
-    e = cudaMemsetAsync(flag, 0, 4, stream);
-    if (e != cudaSuccess) return -static_cast<int>(e);
-    decomp_emit_kernel<<<grid, kThreadsD, 0, stream>>>(n, d_runs, pr, node, val, d_total, d_edge_runs, d_edge_offsets,
-                                                       d_run_to_edge, flag);
-    decomp_long_kernel<<<grid, kThreadsD, 0, stream>>>(n, d_runs, node, val, flag, d_edge_runs, d_run_to_edge);
-    e = cudaGetLastError();
-    return e == cudaSuccess ? rounds : -static_cast<int>(e);
+    decomp_link_kernel<<<grid, kThreadsD, 0, stream>>>(n, pr, pl, ov, anc);
+    decomp_jump_kernel<<<grid, kThreadsD, 0, stream>>>(n, anc);
+    decomp_tail_kernel<<<grid, kThreadsD, 0, stream>>>(n, d_runs, pr, anc, head_len, long_flag);
+    decomp_scan_sums_kernel<<<static_cast<unsigned>(tiles), kThreadsD, 0, stream>>>(n, anc, head_len, sums);
+    decomp_scan_spine_kernel<<<1, 1024, 0, stream>>>(sums, tiles, d_total);
+    decomp_scan_kernel<<<static_cast<unsigned>(tiles), kThreadsD, 0, stream>>>(n, anc, head_len, sums, excl);
+    decomp_emit_kernel<<<grid, kThreadsD, 0, stream>>>(n, d_runs, pr, anc, head_len, excl, d_total, d_edge_runs,
+                                                       d_edge_offsets, d_run_to_edge);
+    decomp_long_kernel<<<grid, kThreadsD, 0, stream>>>(n, d_runs, anc, head_len, excl, long_flag, d_edge_runs,
+                                                       d_run_to_edge);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? 1 : -static_cast<int>(e);
 }
 
 }  // extern "C"
