@@ -233,6 +233,34 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
     return x;
 }
 
+// The same transpose in three instructions per stage: the partner's word is
+// rotated by +-s (one funnel shift; the bits that wrap around land in the half
+// this lane keeps) and merged with one LOP3 under a per-lane mask.  The per-lane
+// rotate amounts and masks are computed once (TransposeLane) and reused.
+struct TransposeLane {
+    uint32_t rot[5], keep[5];
+    __device__ __forceinline__ explicit TransposeLane(int lane) {
+        const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const int sh = 16 >> i;
+            const bool hi = (lane & sh) != 0;
+            rot[i] = hi ? 32 - sh : sh;            // rotate left by s (low lane) or right by s (high lane)
+            keep[i] = hi ? ~masks[i] : masks[i];   // the bits this lane keeps from its own word
+        }
+    }
+};
+
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const TransposeLane& t) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, x, 16 >> i);
+        const uint32_t r = __funnelshift_l(o, o, t.rot[i]);
+        x = (x & t.keep[i]) | (r & ~t.keep[i]);
+    }
+    return x;
+}
+
 // P3: fill.  One warp per (band, word).  Per 32-row chunk, lane k loads row k's
 // raw little-endian word (one load per lane instead of 32 broadcast loads per
 // warp) and a warp bit transpose hands lane j the 32-row bit sequence of the
@@ -578,11 +606,12 @@ __global__ void __launch_bounds__(kBandWarps * 32) profile_fill_band_kernel(cons
         if (y0 + 32 * q >= y1) d = 0;
         changed |= static_cast<uint64_t>(__reduce_or_sync(0xFFFFFFFFu, d)) << (kW * q);
     }
+    const TransposeLane tl(lane);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         if ((changed >> (kW * q)) & ((1u << kW) - 1u)) {  // warp-uniform (kW <= 8)
 #pragma unroll
-            for (int i = 0; i < kW; ++i) x[q][i] = warp_transpose32(x[q][i], lane);
+            for (int i = 0; i < kW; ++i) x[q][i] = warp_transpose32(x[q][i], tl);
         }
     }
     // Phase 2.
