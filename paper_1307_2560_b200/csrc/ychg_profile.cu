@@ -62,16 +62,27 @@ __device__ __forceinline__ uint32_t load_word(const ProfileArgs& a, int w, int y
 }
 
 // P1: counts[band][col] = rises of column col in rows [band*256, band*256+256).
-__global__ void profile_count_kernel(const ProfileArgs a, uint32_t* __restrict__ band_counts) {
-    const int gw = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);  // one warp per (band, 32 words)
-    const int lane = threadIdx.x & 31;
+// One CTA per (band, 1024-column strip): warp q walks rows [64q, 64q+64) of the
+// band, lane = one 32-bit word, bit-sliced ripple counters (16 row loads in
+// flight); the four warps' per-column byte counters (<= 32 each) are added as
+// packed bytes in shared memory and the strip's 1024 counts go out with
+// coalesced stores.  (One warp per 256-row band left 12 warps per SM waiting on
+// loads: 68 us for the 55 MB mask at 21000^2.)
+constexpr int kCountWarps = 4;
+constexpr int kCountRows = kBandRows / kCountWarps;  // 64 rows per warp: counters <= 32
+
+__global__ void __launch_bounds__(kCountWarps * 32) profile_count_kernel(const ProfileArgs a,
+                                                                        uint32_t* __restrict__ band_counts) {
+    __shared__ uint32_t part[kCountWarps][8][32];
+    __shared__ uint32_t cols[32 * 33];  // [word][column in word], padded row: conflict-free
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int strips = (a.n_words + 31) / 32;
-    if (gw >= strips * a.n_bands) return;
-    const int band = gw / strips, strip = gw - band * strips;
+    const int band = blockIdx.x / strips, strip = blockIdx.x - band * strips;
+    if (band >= a.n_bands) return;
     const int w = strip * 32 + lane;
-    const int y0 = band * kBandRows, y1 = min(a.height, y0 + kBandRows);
+    const int y0 = band * kBandRows + kCountRows * warp, y1 = min(a.height, y0 + kCountRows);
     uint32_t pl[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (w < a.n_words) {
+    if (w < a.n_words && y0 < a.height) {
         uint32_t pa = load_word(a, w, y0 - 1);
         for (int yb = y0; yb < y1; yb += kChunk) {
             uint32_t v[kChunk];  // kChunk independent row loads in flight
@@ -82,7 +93,7 @@ __global__ void profile_count_kernel(const ProfileArgs a, uint32_t* __restrict__
                 uint32_t c = v[k] & ~pa;  // rises (runscan.cpp:57); rows past y1 load 0
                 pa = v[k];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < 6; ++q) {  // <= 32 rises per column: 6 planes
                     const uint32_t t = pl[q] & c;
                     pl[q] ^= c;
                     c = t;
@@ -91,47 +102,102 @@ __global__ void profile_count_kernel(const ProfileArgs a, uint32_t* __restrict__
         }
     }
     ychg_dev::transpose8x8_bytes(pl);  // byte L of pl[p] = counter of bit 8L+p = column 31-(8L+p)
-    if (w < a.n_words) {
-        uint32_t* out = band_counts + static_cast<int64_t>(band) * (a.n_words * 32) + 32 * w;
 #pragma unroll
-        for (int p = 0; p < 8; ++p)
+    for (int p = 0; p < 8; ++p) part[warp][p][lane] = pl[p];
+    __syncthreads();
 #pragma unroll
-            for (int L = 0; L < 4; ++L) out[31 - (8 * L + p)] = (pl[p] >> (8 * L)) & 0xFFu;
+    for (int p = 2 * warp; p < 2 * warp + 2; ++p) {  // packed bytes: 4 x <= 32 never carries
+        const uint32_t v = part[0][p][lane] + part[1][p][lane] + part[2][p][lane] + part[3][p][lane];
+#pragma unroll
+        for (int L = 0; L < 4; ++L) cols[33 * lane + 31 - (8 * L + p)] = (v >> (8 * L)) & 0xFFu;
     }
+    __syncthreads();
+    uint32_t* out = band_counts + static_cast<int64_t>(band) * (a.n_words * 32) + strip * 1024;
+    for (int i = threadIdx.x; i < 1024; i += kCountWarps * 32)
+        if (strip * 32 + (i >> 5) < a.n_words) out[i] = cols[33 * (i >> 5) + (i & 31)];
 }
 
 // P2a: per column, exclusive prefix over bands (in place) and the column total.
-__global__ void profile_colscan_kernel(const ProfileArgs a, uint32_t* __restrict__ band_counts,
-                                       int32_t* __restrict__ counts) {
+// One CTA per 32 columns (lane = column): warp q takes a contiguous range of
+// bands with all of its loads in flight at once, the warps' sums are scanned in
+// shared memory, and each warp writes its bands' exclusive prefixes.
+constexpr int kScanWarps = 8;
+constexpr int kScanBandsPerWarp = 16;  // 128 bands (32768 rows) per pass; taller images loop
+
+__global__ void __launch_bounds__(kScanWarps * 32) profile_colscan_kernel(const ProfileArgs a,
+                                                                         uint32_t* __restrict__ band_counts,
+                                                                         int32_t* __restrict__ counts,
+                                                                         int64_t* __restrict__ col_off,
+                                                                         long long* __restrict__ cta_tot) {
+    __shared__ uint32_t wsum[kScanWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * 32 + lane;
+    const bool live = c < a.width;
     const int64_t stride = static_cast<int64_t>(a.n_words) * 32;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < a.width; c += gridDim.x * blockDim.x) {
-        uint32_t run = 0;
-        for (int b0 = 0; b0 < a.n_bands; b0 += 8) {
-            uint32_t v[8];
+    uint32_t carry = 0;  // bands before this pass (same in every warp)
+    for (int p0 = 0; p0 < a.n_bands; p0 += kScanWarps * kScanBandsPerWarp) {
+        const int per = (min(a.n_bands - p0, kScanWarps * kScanBandsPerWarp) + kScanWarps - 1) / kScanWarps;
+        const int b0 = p0 + warp * per;
+        uint32_t v[kScanBandsPerWarp];
+        uint32_t sum = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = b0 + k < a.n_bands ? band_counts[(b0 + k) * stride + c] : 0u;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (b0 + k < a.n_bands) {
-                    band_counts[(b0 + k) * stride + c] = run;
-                    run += v[k];
-                }
+        for (int k = 0; k < kScanBandsPerWarp; ++k) {
+            const int band = b0 + k;
+            v[k] = live && k < per && band < a.n_bands ? band_counts[band * stride + c] : 0u;
+            sum += v[k];
         }
-        counts[c] = static_cast<int32_t>(run);
+        wsum[warp][lane] = sum;
+        __syncthreads();
+        uint32_t run = carry, tot = carry;
+#pragma unroll
+        for (int q = 0; q < kScanWarps; ++q) {
+            const uint32_t x = wsum[q][lane];
+            if (q < warp) run += x;
+            tot += x;
+        }
+#pragma unroll
+        for (int k = 0; k < kScanBandsPerWarp; ++k) {
+            const int band = b0 + k;
+            if (live && k < per && band < a.n_bands) {
+                band_counts[band * stride + c] = run;
+                run += v[k];
+            }
+        }
+        carry = tot;
+        __syncthreads();  // wsum is rewritten by the next pass
+    }
+    if (warp == 0) {
+        if (live) counts[c] = static_cast<int32_t>(carry);
+        // the column offsets' first level: exclusive prefix inside these 32 columns,
+        // and their total (profile_offsets_kernel adds the prefix over the CTAs)
+        long long incl = live ? static_cast<long long>(carry) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (live) col_off[c] = incl - static_cast<long long>(carry);
+        if (lane == 31) cta_tot[blockIdx.x] = incl;
     }
 }
 
-// P2b: exclusive prefix over columns (single CTA, chunked block scan).
-__global__ void profile_offsets_kernel(int32_t n, const int32_t* __restrict__ counts, int64_t* __restrict__ col_off,
-                                       int64_t* __restrict__ n_runs) {
-    __shared__ long long warp_tot[32];
-    __shared__ long long carry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    if (tid == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += blockDim.x) {
-        const int i = base + tid;
-        const long long v = i < n ? counts[i] : 0;
+// P2b: second level of the column offsets.  Every CTA scans the colscan CTAs'
+// totals (32 columns each; a few KB, L2-resident) up to the 1024-column slice it
+// fixes up -- col_off[c] += prefix[c / 32] -- so no single CTA walks all the
+// columns; CTA 0 scans all of them and stores the run total.
+__global__ void __launch_bounds__(1024) profile_offsets_kernel(int32_t n, const long long* __restrict__ cta_tot,
+                                                               int64_t* __restrict__ col_off,
+                                                               int64_t* __restrict__ n_runs) {
+    __shared__ long long warp_tot[33];
+    __shared__ long long pre[32];  // this slice's 32 CTA prefixes
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nb = (n + 31) / 32;
+    const int slice = blockIdx.x;
+    const int need = slice == 0 ? nb : min(nb, 32 * slice + 32);
+    long long carry = 0;
+    for (int b0 = 0; b0 < need; b0 += 1024) {
+        const int i = b0 + tid;
+        const long long v = i < need ? cta_tot[i] : 0;
         long long incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -141,22 +207,25 @@ __global__ void profile_offsets_kernel(int32_t n, const int32_t* __restrict__ co
         if (lane == 31) warp_tot[warp] = incl;
         __syncthreads();
         if (warp == 0) {
-            long long wt = lane < nw ? warp_tot[lane] : 0;
+            const long long wt = warp_tot[lane];
             long long winc = wt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const long long t = __shfl_up_sync(0xFFFFFFFFu, winc, o);
                 if (lane >= o) winc += t;
             }
-            if (lane < nw) warp_tot[lane] = winc - wt;
+            warp_tot[lane] = winc - wt;
+            if (lane == 31) warp_tot[32] = winc;
         }
         __syncthreads();
-        if (i < n) col_off[i] = carry + warp_tot[warp] + incl - v;
-        __syncthreads();
-        if (tid == blockDim.x - 1) carry += warp_tot[warp] + incl;
-        __syncthreads();
+        if (i >= 32 * slice && i < 32 * slice + 32) pre[i - 32 * slice] = carry + warp_tot[warp] + incl - v;
+        carry += warp_tot[32];
+        __syncthreads();  // warp_tot is rewritten by the next chunk
     }
-    if (tid == 0) *n_runs = carry;
+    if (slice == 0 && tid == 0) *n_runs = carry;
+    __syncthreads();
+    const int c = 1024 * slice + tid;
+    if (c < n) col_off[c] += pre[tid >> 5];
 }
 
 // P3 (mid density): one warp per (band, word), lanes step the rows together.
@@ -724,13 +793,15 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
     a.band_major = -1;
     if (const char* v = std::getenv("YCHG_FILL_BAND_MAJOR"); v && *v) a.band_major = std::atoi(v);  // A/B hook
     const int strips = (a.n_words + 31) / 32;
-    const int warps = strips * a.n_bands;
-    const int blocks = (warps + 7) / 8;
     const int64_t fill_warps = static_cast<int64_t>(a.n_words) * a.n_bands;
     if (phase == 0) {  // counts + offsets
-        profile_count_kernel<<<blocks, 256, 0, stream>>>(a, d_band_counts);
-        profile_colscan_kernel<<<(width + 255) / 256, 256, 0, stream>>>(a, d_band_counts, d_counts);
-        profile_offsets_kernel<<<1, 1024, 0, stream>>>(width, d_counts, d_col_off, d_n_runs);
+        profile_count_kernel<<<static_cast<unsigned>(strips * a.n_bands), kCountWarps * 32, 0, stream>>>(a, d_band_counts);
+        // the colscan CTAs' totals live past the band counts in the same buffer
+        long long* cta_tot = reinterpret_cast<long long*>(
+            d_band_counts + ((static_cast<int64_t>(a.n_bands) * a.n_words * 32 + 1) & ~int64_t(1)));
+        profile_colscan_kernel<<<(width + 31) / 32, kScanWarps * 32, 0, stream>>>(a, d_band_counts, d_counts, d_col_off,
+                                                                                cta_tot);
+        profile_offsets_kernel<<<(width + 1023) / 1024, 1024, 0, stream>>>(width, cta_tot, d_col_off, d_n_runs);
     } else {  // fill
         // Fill kernel: the band-staged kernel whenever the rows and the output are
         // 16-byte aligned (always, for the library's own buffers): on 21000^2 it
@@ -783,8 +854,10 @@ extern "C" int ychg_launch_profile(const uint8_t* d_bits, int64_t pitch, int32_t
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }
 
+// u32 words of the band-count buffer: the per-(band, column) counts, then (8-byte
+// aligned) one int64 total per 32 columns for the column-offset scan.
 extern "C" int64_t ychg_profile_band_words(int32_t width, int32_t height) {
     const int64_t n_words = (width + 31) / 32;
     const int64_t n_bands = (height + kBandRows - 1) / kBandRows;
-    return n_bands * n_words * 32;
+    return ((n_bands * n_words * 32 + 1) & ~int64_t(1)) + 2 * ((int64_t(width) + 31) / 32) + 2;
 }
