@@ -546,7 +546,6 @@ struct HostContext {
     int64_t dws_cap = 0;
     unsigned long long* d_dscal = nullptr;  // [0] edge/run totals, [1] validation error
     unsigned long long* h_dscal = nullptr;  // pinned
-    int* h_flag = nullptr;                  // pinned: jump-round change flag
     cudaEvent_t dec_ev[2] = {nullptr, nullptr};
     // pageable host input: pinned staging ring (see h2d_staged)
     static constexpr int kStageSlots = 3;
@@ -1221,8 +1220,7 @@ int ensure_buf(T** p, int64_t* cap, int64_t elems) {
 }
 
 int ensure_decompose(HostContext& c, int64_t n) {
-    if (!c.h_flag) {
-        CK(cudaMallocHost(&c.h_flag, 16));
+    if (!c.h_dscal) {
         CK(cudaMallocHost(&c.h_dscal, 16));
         CK(cudaMalloc(&c.d_dscal, 16));
         CK(cudaEventCreate(&c.dec_ev[0]));
@@ -1256,9 +1254,9 @@ int decompose_device_profile(HostContext& c, int32_t width, int64_t n, ychg_hype
     CK(cudaMallocAsync(reinterpret_cast<void**>(&hg->d_eoff), (n + 1) * 4, c.stream));
     CK(cudaMallocAsync(reinterpret_cast<void**>(&hg->d_r2e), n * 4, c.stream));
     CK(cudaEventRecord(c.dec_ev[0], c.stream));
-    const int rounds = ychg_launch_decompose(c.d_runs, c.d_col_off, c.d_counts, width, n, c.d_dws, hg->d_eruns,
-                                             hg->d_eoff, hg->d_r2e, c.d_dscal, c.h_flag, c.stream);
-    if (rounds < 0) return cuda_fail(static_cast<cudaError_t>(-rounds), "decompose kernels");
+    const int drc = ychg_launch_decompose(c.d_runs, c.d_col_off, c.d_counts, width, n, c.d_dws, hg->d_eruns,
+                                          hg->d_eoff, hg->d_r2e, c.d_dscal, c.stream);
+    if (drc < 0) return cuda_fail(static_cast<cudaError_t>(-drc), "decompose kernels");
     CK(cudaEventRecord(c.dec_ev[1], c.stream));
     CK(cudaMemcpyAsync(c.h_dscal, c.d_dscal, 8, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));

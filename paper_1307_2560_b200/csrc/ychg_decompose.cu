@@ -449,12 +449,10 @@ int ychg_launch_decompose_validate(const int32_t* d_runs, const int64_t* d_col_o
 }
 
 // The full decomposition of a device profile (n > 0), all on `stream` with no
-// host round trip.  Returns 1 or -(cudaError_t).  (h_flag is unused: kept for the
-// interface.)
+// host round trip.  Returns 0 or -(cudaError_t).
 int ychg_launch_decompose(const int32_t* d_runs, const int64_t* d_col_off, const int32_t* d_counts, int32_t width,
                           int64_t n, void* d_ws, int32_t* d_edge_runs, uint32_t* d_edge_offsets,
-                          uint32_t* d_run_to_edge, unsigned long long* d_total, int* h_flag, cudaStream_t stream) {
-    (void)h_flag;
+                          uint32_t* d_run_to_edge, unsigned long long* d_total, cudaStream_t stream) {
     const int64_t tiles = (n + kScanTile - 1) / kScanTile;
     const int64_t r4 = ((n * 4 + 15) / 16) * 16;
     uint8_t* p = static_cast<uint8_t*>(d_ws);
@@ -481,7 +479,7 @@ int ychg_launch_decompose(const int32_t* d_runs, const int64_t* d_col_off, const
     decomp_long_kernel<<<grid, kThreadsD, 0, stream>>>(n, d_runs, anc, head_len, excl, long_flag, d_edge_runs,
                                                        d_run_to_edge);
     const cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? 1 : -static_cast<int>(e);
+    return e == cudaSuccess ? 0 : -static_cast<int>(e);
 }
 
 }  // extern "C"

@@ -42,7 +42,7 @@ int ychg_launch_decompose_validate(const int32_t* d_runs, const int64_t* d_col_o
                                    int64_t n, unsigned long long* d_err, cudaStream_t stream);
 int ychg_launch_decompose(const int32_t* d_runs, const int64_t* d_col_off, const int32_t* d_counts, int32_t width,
                           int64_t n, void* d_ws, int32_t* d_edge_runs, uint32_t* d_edge_offsets,
-                          uint32_t* d_run_to_edge, unsigned long long* d_total, int* h_flag, cudaStream_t stream);
+                          uint32_t* d_run_to_edge, unsigned long long* d_total, cudaStream_t stream);
 
 // PNM rasters (ychg_aux.cu): P5 threshold + pack, P4 padding-bit mask.
 int ychg_launch_pack_p5(const uint8_t* d_samples, int32_t width, int32_t height, int32_t threshold, uint8_t* d_bits,
