@@ -25,6 +25,7 @@
 // Integer-exact: the outputs are bit-identical to the reference's.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 namespace ychg_dev {
@@ -53,12 +54,19 @@ __device__ __forceinline__ int64_t first_reaching(const int32_t* __restrict__ ru
 // similar numbers of runs at similar heights, so the run of column c+1 reaching
 // row `top` sits near index g = b + i * n(c+1) / n(c) for the i-th run of column
 // c -- a few probes (cached by the neighbouring threads) instead of log2(n).
+// `bot_g` is the y_bot of run g (clamped into [b, e)) when the caller has already
+// loaded it (first probes of several searches issued together), else INT_MIN.
+__device__ __forceinline__ int64_t clamp_guess(int64_t b, int64_t e, int64_t g) {
+    return g < b ? b : (g >= e ? e - 1 : g);
+}
+
 __device__ __forceinline__ int64_t first_reaching_from(const int32_t* __restrict__ runs, int64_t b, int64_t e,
-                                                       int top, int64_t g) {
+                                                       int top, int64_t g, int bot_g = INT_MIN) {
     if (b >= e) return b;
-    g = g < b ? b : (g >= e ? e - 1 : g);
+    g = clamp_guess(b, e, g);
+    if (bot_g == INT_MIN) bot_g = __ldg(runs + 3 * g + 2);
     int64_t lo, hi;  // answer in [lo, hi]
-    if (__ldg(runs + 3 * g + 2) < top) {  // answer is right of g
+    if (bot_g < top) {  // answer is right of g
         int64_t step = 1;
         lo = g + 1;
         hi = g + 1;
@@ -84,7 +92,9 @@ __device__ __forceinline__ int64_t first_reaching_from(const int32_t* __restrict
 
 
 // D1: for run g, the first overlapping run in column c+1 (resp. c-1) and the
-// overlap count saturated at 2.  ov = right | left << 2.
+// overlap count saturated at 2.  ov = right | left << 2.  The two searches are
+// started together (both first probes in flight at once), and each side's two
+// overlap tests read runs j and j+1 with independent loads.
 __global__ void __launch_bounds__(kThreadsD) decomp_overlap_kernel(const int32_t* __restrict__ runs,
                                                                    const int64_t* __restrict__ col_off,
                                                                    const int32_t* __restrict__ counts, int32_t width,
@@ -93,25 +103,35 @@ __global__ void __launch_bounds__(kThreadsD) decomp_overlap_kernel(const int32_t
     for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < n; g += int64_t(gridDim.x) * blockDim.x) {
         const int c = __ldg(runs + 3 * g), top = __ldg(runs + 3 * g + 1), bot = __ldg(runs + 3 * g + 2);
         uint32_t cnt_r = 0, cnt_l = 0, jr = kNoLink, jl = kNoLink;
-        const int64_t own0 = __ldg(col_off + c);
-        const int64_t i_own = g - own0;
+        const int64_t i_own = g - __ldg(col_off + c);
         const int32_t n_own = __ldg(counts + c);
-        if (c + 1 < width) {
-            const int32_t n = __ldg(counts + c + 1);
-            const int64_t b = __ldg(col_off + c + 1), e = b + n;
-            const int64_t j = first_reaching_from(runs, b, e, top, b + (i_own * n) / (n_own > 0 ? n_own : 1));
-            if (j < e && __ldg(runs + 3 * j + 1) <= bot) {
-                cnt_r = 1 + (j + 1 < e && __ldg(runs + 3 * (j + 1) + 1) <= bot);
-                jr = static_cast<uint32_t>(j);
+        const int32_t div = n_own > 0 ? n_own : 1;
+        const bool has_r = c + 1 < width, has_l = c > 0;
+        const int32_t nr = has_r ? __ldg(counts + c + 1) : 0, nl = has_l ? __ldg(counts + c - 1) : 0;
+        const int64_t br = has_r ? __ldg(col_off + c + 1) : 0, bl = has_l ? __ldg(col_off + c - 1) : 0;
+        const int64_t er = br + nr, el = bl + nl;
+        const int64_t gr = clamp_guess(br, er, br + (i_own * nr) / div), gl = clamp_guess(bl, el, bl + (i_own * nl) / div);
+        const int vr = nr > 0 ? __ldg(runs + 3 * gr + 2) : 0, vl = nl > 0 ? __ldg(runs + 3 * gl + 2) : 0;
+        if (nr > 0) {
+            const int64_t j = first_reaching_from(runs, br, er, top, gr, vr);
+            if (j < er) {
+                const int t0 = __ldg(runs + 3 * j + 1);
+                const int t1 = j + 1 < er ? __ldg(runs + 3 * (j + 1) + 1) : INT_MAX;
+                if (t0 <= bot) {
+                    cnt_r = 1 + (t1 <= bot);
+                    jr = static_cast<uint32_t>(j);
+                }
             }
         }
-        if (c > 0) {
-            const int32_t n = __ldg(counts + c - 1);
-            const int64_t b = __ldg(col_off + c - 1), e = b + n;
-            const int64_t j = first_reaching_from(runs, b, e, top, b + (i_own * n) / (n_own > 0 ? n_own : 1));
-            if (j < e && __ldg(runs + 3 * j + 1) <= bot) {
-                cnt_l = 1 + (j + 1 < e && __ldg(runs + 3 * (j + 1) + 1) <= bot);
-                jl = static_cast<uint32_t>(j);
+        if (nl > 0) {
+            const int64_t j = first_reaching_from(runs, bl, el, top, gl, vl);
+            if (j < el) {
+                const int t0 = __ldg(runs + 3 * j + 1);
+                const int t1 = j + 1 < el ? __ldg(runs + 3 * (j + 1) + 1) : INT_MAX;
+                if (t0 <= bot) {
+                    cnt_l = 1 + (t1 <= bot);
+                    jl = static_cast<uint32_t>(j);
+                }
             }
         }
         pr[g] = jr;
