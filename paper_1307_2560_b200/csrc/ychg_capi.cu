@@ -96,6 +96,7 @@ struct ychg_plan {
     alignas(64) CUtensorMap map{};
     // timing
     bool timing = false;
+    bool latency = false;          // YCHG_PLAN_LATENCY: one-off scans (small images take the single-CTA kernel)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     bool ev_recorded = false;
     unsigned long long* dbg = nullptr;  // per-CTA %globaltimer stamps (device view of dbg_host)
@@ -174,6 +175,7 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
 
     auto plan = std::make_unique<ychg_plan>();
+    plan->latency = (flags & YCHG_PLAN_LATENCY) != 0;
     plan->device = device;
     ScanParams& p = plan->prm;
     p.width_img = width_img;
@@ -371,6 +373,31 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     if (reinterpret_cast<uintptr_t>(d_bits) % 16 != 0)
         return fail(YCHG_ERR_INVALID, "scan_device: image base must be 16-byte aligned");
 
+    // A one-off scan of a small image (one strip, <= 1024 rows): the single-CTA
+    // kernel (no TMA ring / scan protocol; ~19 -> ~9 us isolated at 512^2).
+    const char* no_small_env = getenv("YCHG_NO_SMALL");  // A/B hook (read per call: tests switch it)
+    const bool no_small = no_small_env && no_small_env[0] == '1';
+    if (plan->latency && !no_small && p.n_strips == 1 && p.height <= 1024 && p.width_img <= 1024) {
+        ScanParams q = p;
+        q.bits = d_bits;
+        q.pitch = pitch;
+        q.counts = d_counts;
+        q.flags = d_flags;
+        q.boundaries = d_boundaries;
+        q.totals = reinterpret_cast<long long*>(d_totals);
+        q.mul2 = 2u;
+        q.mul1 = 1u;
+        q.mulm1 = 0xFFFFFFFFu;
+        q.mulnb = 1u << 25;
+        if (plan->timing) CK(cudaEventRecord(plan->ev[0], st));
+        const int rc = ychg_launch_small(&q, with_hyperedges ? 1 : 0, st);
+        if (rc != 0) return cuda_fail(static_cast<cudaError_t>(rc), "small-image scan kernel launch");
+        if (plan->timing) {
+            CK(cudaEventRecord(plan->ev[1], st));
+            plan->ev_recorded = true;
+        }
+        return YCHG_OK;
+    }
     if (plan->map_ptr != d_bits || plan->map_pitch != pitch) {
         auto encode = tensor_map_encoder();
         if (!encode) return fail(YCHG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");

@@ -11,6 +11,7 @@ struct ScanParams;
 extern "C" {
 // Enqueue one scan (ONE programmatic-dependent launch of ychg_scan_kernel) on `stream`.
 // Returns cudaError_t.
+int ychg_launch_small(const ychg_dev::ScanParams* prm, int with_links, cudaStream_t stream);
 int ychg_launch_scan(const void* tmap, const ychg_dev::ScanParams* prm, int grid, int with_links,
                      cudaStream_t stream);
 

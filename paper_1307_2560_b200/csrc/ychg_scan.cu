@@ -957,6 +957,209 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
     if (tid == 0 && have_seg) stamp(prm, seg_tick[0], 5, globaltimer());
 }
 
+// ----------------------------------------------------------------------------
+// Small images (one strip, <= kSmallRows rows): ONE CTA does the whole scan.
+// All row blocks are loaded at once into shared memory (16-byte loads, every
+// load in flight together), each of 16 warps runs the same per-row K1/K3 code
+// over its 1-2 blocks, and the CTA merges the warps (counts, K3 band summaries)
+// and writes counts, flags, boundaries and totals itself -- no TMA ring, scan
+// tickets, segment partials or strip records: for a 32 KB image the pipelined
+// kernel's protocol (ramp, arrival, finish) is most of its ~11 us device time.
+constexpr int kSmallWarps = 16;
+constexpr int kSmallRows = 1024;  // 32 blocks: <= 2 per warp
+template <bool kLinks>
+__host__ __device__ constexpr int small_smem_bytes() {
+    return (kSmallRows / kBlockRows) * kStageBytes + kSmallWarps * 16 * 32 * 4 + kSmallWarps * kSumPlanes * 32 * 4 +
+           kStripCols * 4 + 256;
+}
+
+template <bool kLinks>
+__global__ void __launch_bounds__(kSmallWarps * 32) ychg_small_kernel(const ScanParams prm) {
+    constexpr int NW = kSmallWarps;
+    constexpr int T = NW * 32;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* boxes = smem;  // block b, row r: boxes + b * kStageBytes + r * kBoxBytes (128 B row + 16 B zero halo)
+    uint32_t* accs = reinterpret_cast<uint32_t*>(smem + (kSmallRows / kBlockRows) * kStageBytes);
+    uint32_t* sums = accs + NW * 16 * 32;
+    int32_t* sc = reinterpret_cast<int32_t*>(sums + NW * kSumPlanes * 32);
+    __shared__ unsigned long long wlinks[2 * NW];
+    __shared__ uint32_t fw[kStripWords];
+    __shared__ int wpre[kStripWords];
+    __shared__ long long red[NW];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nblk = prm.n_blocks;
+
+    // (1) every row of the image: 16-byte chunks, bytes past the row zeroed; the
+    //     halo chunk of every row is zero (nothing right of the only strip)
+    {
+        constexpr int kChunks = 9;  // 8 data chunks + the halo chunk per row
+        constexpr int kPer = (kSmallRows * kChunks + T - 1) / T;  // 18: every load in flight at once
+        const int total = nblk * kBlockRows * kChunks;
+        for (int i0 = tid; i0 < total; i0 += T * kPer) {
+            uint4 v[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int i = i0 + u * T;
+                v[u] = make_uint4(0u, 0u, 0u, 0u);
+                if (i < total) {
+                    const int row = i / kChunks, ch = i - row * kChunks;
+                    if (ch < 8 && row < prm.height && 16 * ch < prm.row_bytes)
+                        v[u] = __ldg(reinterpret_cast<const uint4*>(prm.bits + static_cast<int64_t>(row) * prm.pitch) + ch);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int i = i0 + u * T;
+                if (i < total) {
+                    const int row = i / kChunks, ch = i - row * kChunks;
+                    uint4 x = v[u];
+                    const int nb = prm.row_bytes - 16 * ch;  // valid bytes of this chunk
+                    if (nb < 16) {
+                        uint32_t* w = reinterpret_cast<uint32_t*>(&x);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int nq = nb - 4 * q;
+                            w[q] = nq >= 4 ? w[q] : (nq <= 0 ? 0u : (w[q] & (0xFFFFFFFFu >> (8 * (4 - nq)))));
+                        }
+                    }
+                    *reinterpret_cast<uint4*>(boxes + (row >> 5) * kStageBytes + (row & 31) * kBoxBytes + 16 * ch) = x;
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // (2) the warp's blocks [wb0, wb0 + nb)
+    const int wb0 = (warp * nblk) / NW, nb = ((warp + 1) * nblk) / NW - wb0;
+    const Muls mu{prm.mul2, prm.mulnb, prm.mul1, prm.mulm1};
+    LaneState s;
+    s.ones = s.twos = s.fours = s.eights = s.u16 = s.u32 = s.u64 = s.u128 = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s.acc[i] = 0;
+    s.mk3 = word_mask(lane, min(prm.width_cnt, prm.width_img - 1));
+    const bool full = !kLinks || __all_sync(0xFFFFFFFFu, s.mk3 == 0xFFFFFFFFu);
+    s.h1 = s.h2 = 0;
+    s.links = 0;
+    s.pa = s.pb = s.pab = s.praw = 0;
+    uint32_t O = 0;
+    if (nb > 0) {
+        uint32_t raw = 0, nbyte = 0;  // row 32*wb0 - 1 (zero above row 0)
+        if (wb0 > 0) {
+            const uint8_t* hr = boxes + (wb0 - 1) * kStageBytes + 31 * kBoxBytes + 4 * lane;
+            raw = *reinterpret_cast<const uint32_t*>(hr);
+            nbyte = hr[4];
+        }
+        s.praw = raw;
+        s.pa = kLinks ? __byte_perm(raw, 0u, 0x0123u) : raw;
+        s.pb = right_neighbour_msb(s.pa, nbyte, prm.mul2, prm.mulnb);
+        O = kLinks ? (s.pa | s.pb) : 0u;
+        s.Hd = O;
+        s.G2 = s.G3 = O;
+        s.pab = s.pa & s.pb;
+        for (int bi = 0; bi < nb; ++bi) {
+            const uint8_t* sp = boxes + (wb0 + bi) * kStageBytes;
+            if (kLinks && __any_sync(0xFFFFFFFFu, (s.Hd & s.mk3) != 0u)) {
+                if (full) process_block<kLinks, true, false>(sp, lane, s, mu);
+                else process_block<kLinks, true, true>(sp, lane, s, mu);
+            } else {
+                if (full) process_block<kLinks, false, false>(sp, lane, s, mu);
+                else process_block<kLinks, false, true>(sp, lane, s, mu);
+            }
+        }
+        flush_counts(s);  // <= 2 blocks: no intermediate flush needed
+    }
+    int slot = 0;  // non-empty warp bands in row order
+    for (int w = 0; w < warp; ++w) slot += ((w + 1) * nblk) / NW > (w * nblk) / NW;
+    if (kLinks) {
+        if (nb > 0) {
+            const uint32_t m = s.mk3;
+            uint32_t* ws = sums + slot * kSumPlanes * 32;
+            ws[0 * 32 + lane] = O & m;
+            ws[1 * 32 + lane] = O & ~s.Hd & m;
+            ws[2 * 32 + lane] = s.h1 & m;
+            ws[3 * 32 + lane] = s.h2 & m;
+            ws[4 * 32 + lane] = (s.pa | s.pb) & m;
+            ws[5 * 32 + lane] = s.G2 & m;
+            ws[6 * 32 + lane] = s.G3 & m;
+        }
+        unsigned long long l = s.links;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xFFFFFFFFu, l, o);
+        if (lane == 0) wlinks[warp] = l;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) accs[warp * 16 * 32 + i * 32 + lane] = s.acc[i];
+    __syncthreads();
+
+    // (3) merge: per-column counts (u16x2 sums over the warps) and the K3 stitch
+    for (int idx = tid; idx < 16 * 32; idx += T) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) v += accs[w * 16 * 32 + idx];
+        const int i = idx >> 5, ln = idx & 31;
+        sc[32 * ln + acc_column<kLinks>(i, 0)] = static_cast<int32_t>(v & 0xFFFFu);
+        sc[32 * ln + acc_column<kLinks>(i, 1)] = static_cast<int32_t>(v >> 16);
+    }
+    unsigned long long links = 0;
+    if (kLinks) {
+        int nfull = 0;
+        for (int w = 0; w < NW; ++w) nfull += ((w + 1) * nblk) / NW > (w * nblk) / NW;
+        unsigned long long jl = 0;
+        const BandSummary C = chain_compose<NW>(sums, nfull, wlinks + NW, jl);  // (contains __syncthreads)
+        if (warp == 0) {
+            unsigned long long m = __popc(C.OE & C.T2 & ~C.T3);  // closed by the virtual background row H
+            m += lane < NW ? wlinks[lane] : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xFFFFFFFFu, m, o);
+            links = m + jl;
+        }
+    }
+    __syncthreads();
+
+    // (4) flags (column 0 against 0, runscan.cpp:147), run total, boundary prefix
+    long long local_sum = 0;
+    for (int wi = warp; wi < kStripWords; wi += NW) {
+        const int col = wi * 32 + lane;
+        const bool valid = col < prm.width_cnt;
+        const int32_t c = valid ? sc[col] : 0;
+        const int32_t prev = col > 0 ? sc[col - 1] : 0;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, valid && c != prev);
+        if (lane == 0) fw[wi] = m;
+        local_sum += c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local_sum += __shfl_xor_sync(0xFFFFFFFFu, local_sum, o);
+    if (lane == 0) red[warp] = local_sum;
+    __syncthreads();
+    if (warp == 0) {
+        const int c = __popc(fw[lane]);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        wpre[lane] = incl - c;
+        if (lane == 31) {
+            long long runs = 0;
+            for (int w = 0; w < NW; ++w) runs += red[w];
+            prm.totals[0] = runs;
+            prm.totals[1] = kLinks ? static_cast<long long>(links) : 0;
+            prm.totals[2] = kLinks ? runs - static_cast<long long>(links) : -1;
+            prm.totals[3] = incl;
+        }
+    }
+    __syncthreads();
+    // (5) outputs
+    const int nwords = (prm.width_cnt + 31) >> 5;
+    for (int col = tid; col < prm.width_cnt; col += T) prm.counts[col] = sc[col];
+    for (int wi = warp; wi < nwords; wi += NW) {
+        const uint32_t m = fw[wi];
+        if (lane == 0) prm.flags[wi] = m;
+        if ((m >> lane) & 1u) prm.boundaries[wpre[wi] + __popc(m & ((1u << lane) - 1u))] = wi * 32 + lane;
+    }
+}
+
 }  // namespace ychg_dev
 
 // ----------------------------------------------------------------------------
@@ -1023,5 +1226,26 @@ extern "C" int ychg_launch_scan(const void* tmap, const ScanParams* prm, int gri
     ca.attrs = attr;
     ca.numAttrs = 1;
     const cudaError_t e = cudaLaunchKernelExC(&ca, fa, args_a);
+    return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+// Small images (one strip, <= kSmallRows rows): the single-CTA kernel.  Returns
+// -1 when the geometry does not qualify (the caller uses the pipelined kernel).
+extern "C" int ychg_launch_small(const ScanParams* prm, int with_links, cudaStream_t stream) {
+    if (prm->n_strips != 1 || prm->height > kSmallRows || prm->width_img > kStripCols) return -1;
+    static bool prepared[64][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int li = with_links ? 1 : 0;
+    if (dev < 64 && !prepared[dev][li]) {
+        const cudaError_t e = with_links
+            ? cudaFuncSetAttribute(&ychg_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, small_smem_bytes<true>())
+            : cudaFuncSetAttribute(&ychg_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, small_smem_bytes<false>());
+        if (e != cudaSuccess) return static_cast<int>(e);
+        prepared[dev][li] = true;
+    }
+    if (with_links) ychg_small_kernel<true><<<1, kSmallWarps * 32, small_smem_bytes<true>(), stream>>>(*prm);
+    else ychg_small_kernel<false><<<1, kSmallWarps * 32, small_smem_bytes<false>(), stream>>>(*prm);
+    const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : static_cast<int>(e);
 }

@@ -51,6 +51,33 @@ def test_strategies_identical_and_validated(gpu, orc):
         y.cut_vertex_counts(img, y.ScanStrategy.parallel(0))
 
 
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_small_image_kernel_vs_oracle(gpu, orc, monkeypatch, small):
+    """One-off scans of images of one strip and <= 1024 rows take the single-CTA
+    kernel (YCHG_NO_SMALL=1 forces the pipelined one): both against the oracle at
+    its geometry edges -- 1 row / 1 column, widths off the byte and word, exactly
+    1024 columns / rows, one past them (pipelined), every pattern, counts-only."""
+    y = gpu
+    monkeypatch.setenv("YCHG_NO_SMALL", "0" if small == "1" else "1")
+    geoms = [(1, 1), (7, 3), (8, 1024), (9, 1), (31, 33), (32, 64), (33, 1023), (513, 257), (1000, 1000),
+             (1023, 1024), (1024, 1024), (1024, 1), (1025, 100), (600, 1025)]
+    rng = np.random.default_rng(77)
+    for w, h in geoms:
+        specs = [Spec.random(w, h, float(rng.choice([0.1, 0.5, 0.9])), int(rng.integers(0, 1 << 62))),
+                 Spec.checker(w, h, int(rng.integers(1, 9)))]
+        if h >= 2:
+            specs.append(Spec.hbands(w, h, min(147, h // 2)))
+        for sp in specs:
+            bits = orc.synth(sp)
+            img = y.BinaryImage(w, h, bits)
+            r = y.scan(img)
+            c = orc.counts(bits, w)
+            assert np.array_equal(r.counts, c), sp
+            assert np.array_equal(r.boundaries, orc.boundaries(c)), sp
+            assert r.hyperedges == orc.hyperedges(bits, w)[0], sp
+            assert np.array_equal(y.cut_vertex_counts(img), c), sp
+
+
 def test_golden_corpus(gpu, orc):
     y = gpu
     for row in corpus():
