@@ -373,11 +373,12 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
     if (reinterpret_cast<uintptr_t>(d_bits) % 16 != 0)
         return fail(YCHG_ERR_INVALID, "scan_device: image base must be 16-byte aligned");
 
-    // A one-off scan of a small image (one strip, <= 1024 rows): the single-CTA
-    // kernel (no TMA ring / scan protocol; ~19 -> ~9 us isolated at 512^2).
+    // A one-off scan of a small image (one strip, <= 512 rows): the single-CTA
+    // kernel (no TMA ring / scan protocol: 32^2 isolated 16 -> 13 us, drop-in call
+    // 39 -> 33 us; from ~1000 rows on the multi-CTA latency plan is faster).
     const char* no_small_env = getenv("YCHG_NO_SMALL");  // A/B hook (read per call: tests switch it)
     const bool no_small = no_small_env && no_small_env[0] == '1';
-    if (plan->latency && !no_small && p.n_strips == 1 && p.height <= 1024 && p.width_img <= 1024) {
+    if (plan->latency && !no_small && p.n_strips == 1 && p.height <= 512 && p.width_img <= 1024) {
         ScanParams q = p;
         q.bits = d_bits;
         q.pitch = pitch;

@@ -961,12 +961,12 @@ ychg_scan_kernel(const __grid_constant__ CUtensorMap tmap, const ScanParams prm)
 // Small images (one strip, <= kSmallRows rows): ONE CTA does the whole scan.
 // All row blocks are loaded at once into shared memory (16-byte loads, every
 // load in flight together), each of 16 warps runs the same per-row K1/K3 code
-// over its 1-2 blocks, and the CTA merges the warps (counts, K3 band summaries)
+// over its block, and the CTA merges the warps (counts, K3 band summaries)
 // and writes counts, flags, boundaries and totals itself -- no TMA ring, scan
 // tickets, segment partials or strip records: for a 32 KB image the pipelined
 // kernel's protocol (ramp, arrival, finish) is most of its ~11 us device time.
 constexpr int kSmallWarps = 16;
-constexpr int kSmallRows = 1024;  // 32 blocks: <= 2 per warp
+constexpr int kSmallRows = 512;  // 16 blocks: <= 1 per warp (at 1000^2 the pipelined latency plan is faster)
 template <bool kLinks>
 __host__ __device__ constexpr int small_smem_bytes() {
     return (kSmallRows / kBlockRows) * kStageBytes + kSmallWarps * 16 * 32 * 4 + kSmallWarps * kSumPlanes * 32 * 4 +
@@ -993,7 +993,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32) ychg_small_kernel(const Scan
     //     halo chunk of every row is zero (nothing right of the only strip)
     {
         constexpr int kChunks = 9;  // 8 data chunks + the halo chunk per row
-        constexpr int kPer = (kSmallRows * kChunks + T - 1) / T;  // 18: every load in flight at once
+        constexpr int kPer = (kSmallRows * kChunks + T - 1) / T;  // every load in flight at once
         const int total = nblk * kBlockRows * kChunks;
         for (int i0 = tid; i0 < total; i0 += T * kPer) {
             uint4 v[kPer];

@@ -53,14 +53,14 @@ def test_strategies_identical_and_validated(gpu, orc):
 
 @pytest.mark.parametrize("small", ["1", "0"])
 def test_small_image_kernel_vs_oracle(gpu, orc, monkeypatch, small):
-    """One-off scans of images of one strip and <= 1024 rows take the single-CTA
+    """One-off scans of images of one strip and <= 512 rows take the single-CTA
     kernel (YCHG_NO_SMALL=1 forces the pipelined one): both against the oracle at
     its geometry edges -- 1 row / 1 column, widths off the byte and word, exactly
-    1024 columns / rows, one past them (pipelined), every pattern, counts-only."""
+    1024 columns / 512 rows, one past them (pipelined), every pattern, counts-only."""
     y = gpu
     monkeypatch.setenv("YCHG_NO_SMALL", "0" if small == "1" else "1")
-    geoms = [(1, 1), (7, 3), (8, 1024), (9, 1), (31, 33), (32, 64), (33, 1023), (513, 257), (1000, 1000),
-             (1023, 1024), (1024, 1024), (1024, 1), (1025, 100), (600, 1025)]
+    geoms = [(1, 1), (7, 3), (8, 512), (9, 1), (31, 33), (32, 64), (33, 511), (513, 257), (1000, 500),
+             (1023, 512), (1024, 512), (1024, 1), (1025, 100), (600, 513)]
     rng = np.random.default_rng(77)
     for w, h in geoms:
         specs = [Spec.random(w, h, float(rng.choice([0.1, 0.5, 0.9])), int(rng.integers(0, 1 << 62))),
