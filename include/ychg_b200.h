@@ -213,9 +213,10 @@ YCHG_API int ychg_scan_pnm(const uint8_t* bytes, int64_t n, int32_t threshold, i
  * (multi-GPU column strips).  A plan is not safe for concurrent use. */
 YCHG_API int ychg_plan_create(int device, int32_t width_img, int32_t width_cnt, int32_t height,
                      ychg_plan** out);
-/* Plan flags.  YCHG_PLAN_LATENCY sizes the launch for one isolated scan (about
- * one CTA per SM, all SMs streaming at once: the host entry points use it); the
- * default favours back-to-back scans (about half a CTA per SM per scan, so that
+/* Plan flags.  YCHG_PLAN_LATENCY sizes the launch for one isolated scan (two
+ * CTAs per SM, all SMs streaming at once; images of one strip and <= 512 rows
+ * take a single-CTA kernel instead: the host entry points use it); the default
+ * favours back-to-back scans (about half a CTA per SM per scan, so that
  * consecutive scans interleave on the SMs). */
 #define YCHG_PLAN_LATENCY 1
 /* YCHG_PLAN_SYNC_INPUTS: the streaming kernel waits (griddepcontrol.wait) for the
