@@ -345,6 +345,20 @@ int ychg_plan_debug_peek(ychg_plan* plan, uint64_t* host_out, int32_t capacity) 
     return YCHG_OK;
 }
 
+// L2 promotion of the image's TMA boxes (YCHG_TMAP_PROMO=0..3: none / 64 / 128 /
+// 256 B; A/B hook, default 256 B).
+static CUtensorMapL2promotion tmap_promotion() {
+    static const CUtensorMapL2promotion p = [] {
+        const char* v = getenv("YCHG_TMAP_PROMO");
+        const int i = v && *v ? atoi(v) : 3;
+        return i == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+               : i == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : i == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                        : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
+    return p;
+}
+
 int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int32_t with_hyperedges,
                      int32_t* d_counts, uint32_t* d_flags, int32_t* d_boundaries, ychg_totals* d_totals,
                      void* stream) {
@@ -408,7 +422,7 @@ int ychg_scan_device(ychg_plan* plan, const uint8_t* d_bits, int64_t pitch, int3
         cuuint32_t estr[2] = {1, 1};
         const CUresult r = encode(&plan->map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_bits),
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, tmap_promotion(),
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(YCHG_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
         plan->map_ptr = d_bits;
