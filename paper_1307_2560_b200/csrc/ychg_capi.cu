@@ -192,6 +192,7 @@ int ychg_plan_create_ex(int device, int32_t width_img, int32_t width_cnt, int32_
         // warp's data back sooner, the rest of the ring follows (pipelined plans
         // start CTAs one by one as slots free, the whole ring at once)
         p.ramp_boxes = (flags & YCHG_PLAN_LATENCY) ? 1 : 0;
+        if (const char* v = getenv("YCHG_RAMP_BOXES"); v && *v) p.ramp_boxes = atoi(v);  // A/B hook
         if (const char* v = getenv("YCHG_RAMP_BOXES"); v && *v) p.ramp_boxes = atoi(v);  // A/B timing hook
         // Resident CTAs per SM of each path's kernel (its grid is capped to what is
         // resident: a strip finisher may wait on other CTAs of the same scan).
