@@ -132,6 +132,21 @@ def test_decompose_live_reference(gpu, orc, ref):
             assert np.array_equal(a, b)
 
 
+def test_decompose_max_size_65536_vs_reference(gpu, ref):
+    """BASELINE config-5 geometry (65536^2 hbands(147): 9.6M runs in 147 chains of
+    65536 runs, every one longer than the emit kernel's walk): the device
+    decomposition element-wise against the unmodified reference's decompose."""
+    y = gpu
+    n = 65536
+    sp = Spec.hbands(n, n, 147)
+    img = y.synth("hbands", n, n, bands=147)
+    got = y.decompose(img)
+    want = ref.image_synth(sp).decompose()
+    assert got.edge_count == 147
+    for a, b in zip(as_tuple(got), want):
+        assert np.array_equal(a, b)
+
+
 def test_decompose_cxx_dropin(gpu):
     """ychg::b200::decompose returns the reference's own Hypergraph type, equal to
     ychg::decompose (tests/cpp/decompose_dropin.cpp, built by `make -C oracle dropin`)."""
