@@ -636,7 +636,8 @@ def run_ours(a):
                        "strip_width_per_gpu": Ws, "halo_cols": s.halo_cols,
                        "path": "counts+flags+boundaries" + ("" if a.counts_only else "+hyperedges"),
                        "l2": f"rotating {nbuf} device copies per GPU ({nbuf * pitch * H / 1e6:.0f} MB > L2 {L2 / 1e6:.0f} MB)",
-                       "parallelism": f"{world} column strips, one NCCL all-gather per step" if world > 1 else "1 GPU",
+                       "parallelism": (f"{world} column strips, one {'gloo (shared-GPU function test)' if share else 'NCCL'} "
+                                       "all-gather per step") if world > 1 else "1 GPU",
                        "plan": {"grid": info.grid, "n_strips": info.n_strips, "seg_per_strip": info.seg_per_strip,
                                 "skip_unchanged_blocks": not a.no_skip}},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
